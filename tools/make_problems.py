@@ -1,0 +1,206 @@
+#!/usr/bin/env python3
+"""Author the Blackwell (sm_100a) loop problems in the reference's problem
+format (`/root/reference/proj/src/ir.cpp:93-229`: machine + graph, strict keys)
+and, with --solve, run them through the reference scheduler (oracle/_ref, the
+unmodified weftsched built in place) to produce the golden schedules the
+B200 executor consumes.
+
+Outputs (paper_2512_18134_b200/schedules/):
+  <name>.raw.json        raw B200 cycle costs
+  <name>.json            normalized problem (reference `normalize`, U given)
+  <name>.solution.json   reference `joint` output (pinned backend)
+  <name>.listing.txt     reference `codegen` listing of that solution
+  <name>.meta.json       cost map, F, backend, solve seconds
+
+Raw costs (B200, one 128-key KV tile, one 128-row Q sub-tile, d = 128):
+  QK^T / PV GEMM  128x128x128 bf16 = 2.1 MMAC / 4096 MAC/clk/SM  = 512 clk (TC)
+  EX  16384 exp2 at 16/clk/SM (MUFU)                              = 1024 clk
+  MX  tcgen05.ld of S + 16384 FMNMX at 64/clk                      = 256 clk
+  CR  tcgen05.ld/st of O (64 KiB round trip) + 16384 FMUL          = 256 clk
+  spill (row statistics through shared memory + mbarrier)         = 256 clk
+  TMA tile load (32 KiB)                                           = 512 clk
+Everything is a power-of-two multiple of 256, so normalization at U >= 7 is
+exact (F = 0) with one unit = 256 SM cycles.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+OUT = os.path.join(ROOT, "paper_2512_18134_b200", "schedules")
+
+
+def node(id_, unit, cycles, **kw):
+    n = {"id": id_, "rrt": {unit: [1] * cycles} if unit else {}, "cycles": cycles}
+    n.update(kw)
+    return n
+
+
+def edge(src, dst, d, delta=0, blocking=False):
+    e = {"src": src, "dst": dst, "d": d}
+    if delta:
+        e["delta"] = delta
+    if blocking:
+        e["blocking"] = True
+    return e
+
+
+def fa_forward_problem():
+    """FA-forward loop body on sm_100a: two 128-row Q sub-tiles (k = 0, 1)
+    share one 128-key K/V tile per iteration.
+
+    Warps: 16 (4 aligned warpgroup slots); warp 15 is the variable-latency
+    (TMA) warp, so warpgroup ops can use slots 0, 4, 8 only. Per-warp register
+    budget 224 models a softmax warpgroup after setmaxnreg: one tile's S row
+    (MX, 128 regs) and packed P / row sum (EX, 64) fit, a second tile or a
+    correction working set (CR, 64) does not.
+    Tensor memory: 512 columns; S/P and O of each sub-tile take 128 each.
+    The causal variant runs the same loop body (masking only changes the
+    per-tile trip count and applies the mask inside MX on diagonal tiles), so
+    it shares this problem and its schedule.
+    Blocking edges are the mbarrier waits of the realized kernel: TMA landed
+    (LD -> GEMM), MMA committed (S -> MX, PV -> CR), P stored (EX -> PV),
+    O rescaled (CR -> PV).
+    """
+    T = 256  # raw clk per unit (see module docstring)
+    machine = {
+        "units": [{"name": "TC", "capacity": 1}, {"name": "TMA", "capacity": 1},
+                  {"name": "MUFU", "capacity": 1}, {"name": "ALU", "capacity": 1},
+                  {"name": "FMA", "capacity": 1}],
+        "memories": [{"name": "tmem", "capacity": 512}],
+        "num_warps": 16,
+        "reg_limit": 224,
+        "vl_warp": 15,
+    }
+    nodes = [
+        node("LDK", "TMA", 2 * T // T, variable_latency=True),
+        node("LDV", "TMA", 2 * T // T, variable_latency=True),
+    ]
+    edges = []
+    for k in (0, 1):
+        nodes += [
+            node(f"S{k}", "TC", 2, footprint={"tmem": 128}),
+            node(f"MX{k}", "ALU", 1, regs=128, spill_cost=1, warps_required=4),
+            node(f"EX{k}", "MUFU", 4, regs=64, warps_required=4),
+            node(f"CR{k}", "FMA", 1, regs=64, warps_required=4),
+            node(f"PV{k}", "TC", 2, footprint={"tmem": 128}),
+        ]
+        edges += [
+            edge("LDK", f"S{k}", 0, blocking=True),
+            edge(f"S{k}", f"MX{k}", 2, blocking=True),
+            edge(f"MX{k}", f"EX{k}", 1),
+            edge(f"MX{k}", f"MX{k}", 1, delta=1),
+            edge(f"EX{k}", f"EX{k}", 4, delta=1),
+            edge(f"MX{k}", f"CR{k}", 1),
+            edge(f"EX{k}", f"PV{k}", 4, blocking=True),
+            edge("LDV", f"PV{k}", 0, blocking=True),
+            edge(f"CR{k}", f"PV{k}", 1, blocking=True),
+            edge(f"PV{k}", f"CR{k}", 2, delta=1, blocking=True),
+            edge(f"PV{k}", f"PV{k}", 2, delta=1),
+            edge(f"PV{k}", f"S{k}", 0, delta=1),
+        ]
+    # scale to raw cycles
+    for n in nodes:
+        n["cycles"] *= T
+        n["rrt"] = {u: [1] * n["cycles"] for u in n["rrt"]}
+        if n.get("spill_cost"):
+            n["spill_cost"] *= T
+    for e in edges:
+        e["d"] *= T
+    return {"machine": machine, "graph": {"nodes": nodes, "edges": edges}}
+
+
+def gemm_problem():
+    """GEMM mainloop (BASELINE config 2): per k-block, TMA loads of the A and B
+    tiles feed one 128x256x64 tcgen05 MMA chain into a TMEM accumulator.
+    128x256x64 = 2 MMAC = 512 clk on TC; TMA of 48 KiB = 512 clk."""
+    T = 512
+    machine = {
+        "units": [{"name": "TC", "capacity": 1}, {"name": "TMA", "capacity": 1}],
+        "memories": [{"name": "smem", "capacity": 4}],
+        "num_warps": 2,
+        "reg_limit": 0,
+        "vl_warp": 1,
+    }
+    nodes = [
+        node("LDA", "TMA", T, variable_latency=True, footprint={"smem": 1}),
+        node("LDB", "TMA", T, variable_latency=True, footprint={"smem": 1}),
+        node("MMA", "TC", T),
+    ]
+    nodes[0]["rrt"] = {"TMA": [1] * T}
+    nodes[1]["rrt"] = {"TMA": [1] * T}
+    edges = [
+        edge("LDA", "MMA", 0, blocking=True),
+        edge("LDB", "MMA", 0, blocking=True),
+        edge("MMA", "MMA", T, delta=1),
+    ]
+    return {"machine": machine, "graph": {"nodes": nodes, "edges": edges}}
+
+
+def load_ref():
+    sys.path.insert(0, os.path.join(ROOT, "oracle", "_ref"))
+    import _weftsched  # noqa: E402  (oracle: the unmodified reference)
+    return _weftsched
+
+
+def solve(name, raw, resolution, stream_depth, solver=""):
+    w = load_ref()
+    os.makedirs(OUT, exist_ok=True)
+    raw_text = json.dumps(raw, indent=2) + "\n"
+    open(os.path.join(OUT, name + ".raw.json"), "w").write(raw_text)
+    t0 = time.time()
+    norm = w.normalize(raw_text, resolution)
+    t1 = time.time()
+    prob = json.dumps(json.loads(norm["problem"]), indent=2) + "\n"
+    open(os.path.join(OUT, name + ".json"), "w").write(prob)
+    r = w.joint(prob, 0, stream_depth, solver)
+    t2 = time.time()
+    meta = {
+        "resolution": resolution,
+        "cost_map": {str(k): v for k, v in norm["cost_map"].items()},
+        "F": norm["F"],
+        "backend": solver or "internal",
+        "stream_depth": stream_depth,
+        "normalize_s": round(t1 - t0, 4),
+        "joint_s": round(t2 - t1, 4),
+        "status": r["status"],
+    }
+    if r["status"] != "sat":
+        meta["message"] = r.get("message")
+        print(name, json.dumps(meta), file=sys.stderr)
+        return meta
+    open(os.path.join(OUT, name + ".solution.json"), "w").write(r["solution_json"])
+    listing = w.codegen(prob, r["solution_json"], "text")
+    open(os.path.join(OUT, name + ".listing.txt"), "w").write(listing)
+    meta.update({"I": r["I"], "L": r["L"], "M": r["M"], "A": r["A"]})
+    meta["validate"] = w.validate(prob, r["solution_json"])
+    json.dump(meta, open(os.path.join(OUT, name + ".meta.json"), "w"), indent=2)
+    print(name, json.dumps(meta))
+    return meta
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--solve", action="store_true")
+    ap.add_argument("--resolution", type=int, default=7)
+    ap.add_argument("--solver", default="")
+    ap.add_argument("--only", default="")
+    args = ap.parse_args()
+    probs = {
+        "gemm_mainloop": (gemm_problem(), 4),
+        "fa_fwd": (fa_forward_problem(), 2),
+    }
+    for name, (raw, depth) in probs.items():
+        if args.only and name != args.only:
+            continue
+        if args.solve:
+            solve(name, raw, args.resolution, depth, args.solver)
+        else:
+            print(json.dumps(raw, indent=2))
+
+
+if __name__ == "__main__":
+    main()
