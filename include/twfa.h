@@ -1,0 +1,100 @@
+/* twfa.h -- C ABI of the B200 (sm_100a) executor for Twill schedules.
+ *
+ * Drop-in boundary. The reference (weftsched, /root/reference/proj) exposes
+ * its scheduler as C++ (the headers under include/weftsched/), a CLI (`weftsched joint |
+ * codegen | sim | validate`, src/cli.cpp:376-473) and pybind11 bindings that
+ * exchange the SAME JSON documents (bindings/module.cpp:219-249). Its only
+ * consumer of a solved schedule is `synthesize` (codegen.cpp:43-189 /
+ * codegen.hpp:49), which renders a text listing that the paper then
+ * hand-compiled to CUDA. This library is the compiled
+ * consumer in that position: it takes the problem JSON and the solution JSON
+ * exactly as `weftsched joint` writes them (solution_to_json, cli.cpp:68-94)
+ * and executes the loop on the GPU. Nothing here re-solves a schedule.
+ *
+ * Conventions (mirroring the reference, cli.hpp:11-13, cli.cpp:462-471):
+ *   return 0 success, 1 domain error (malformed document, schedule the
+ *   executor cannot realize), 2 usage error (bad arguments / unsupported
+ *   shape), 3 CUDA error. The message of the last failure on the calling
+ *   thread is returned by twfa_last_error(). No C++ exception crosses this
+ *   boundary. Plans are immutable after creation and may be shared between
+ *   threads and devices; launches are ordered on the caller's stream.
+ * Device buffers are caller-owned (raw device pointers, e.g. torch tensors).
+ */
+#ifndef TWFA_H
+#define TWFA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TWFA_OK 0
+#define TWFA_EDOMAIN 1
+#define TWFA_EUSAGE 2
+#define TWFA_ECUDA 3
+
+typedef struct twfa_plan twfa_plan;
+
+/* Interface version of this header (bumped on ABI changes). */
+int twfa_abi_version(void);
+
+/* Thread-local message of the last failed call ("" after a success). */
+const char* twfa_last_error(void);
+
+/* Lower a solved schedule into an executable plan.
+ * Replaces the reference consumer chain solution_from_json (cli.cpp:96-155)
+ * -> reconstruct (cli.cpp:161-168) -> synthesize (codegen.cpp:43-189):
+ * same document checks (unknown keys, M covering every node inside
+ * [0, L - eff], streaming rewrite re-applied when streaming_depths is set),
+ * same stage / region semantics. On success *out owns the plan. */
+int twfa_plan_create(const char* problem_json, const char* solution_json, twfa_plan** out);
+
+/* Release a plan (NULL is ignored). */
+void twfa_plan_destroy(twfa_plan* plan);
+
+/* JSON description of the lowered plan (I, L, copies, per-node stage, slot
+ * and warp, per-warp trip programs, ring depths). Writes at most `cap` bytes
+ * including the terminating NUL; *needed receives the full size. Plays the
+ * role of emit_listing / program_to_json (codegen.hpp:51-56). */
+int twfa_plan_describe(const twfa_plan* plan, char* buf, size_t cap, size_t* needed);
+
+/* Copy the raw device plan (struct TwfaDevicePlan, plan.h) for inspection. */
+int twfa_plan_raw(const twfa_plan* plan, void* dst, size_t cap, size_t* needed);
+
+/* FA forward, bf16, head dim 128, on the calling device:
+ *   O = softmax(scale * Q K^T [+ causal mask]) V,   lse = log-sum-exp per row.
+ * q, k, v, o: [B, H, S, 128] contiguous bf16 device buffers; lse: [B, H, S]
+ * fp32 or NULL. causal: key j visible to query i iff j <= i. stream: a
+ * cudaStream_t (NULL = legacy default stream). The plan must come from an
+ * FA-forward loop problem. */
+int twfa_fa_fwd(const twfa_plan* plan, const void* q, const void* k, const void* v, void* o, float* lse,
+                int B, int H, int S, int D, int causal, float softmax_scale, void* stream);
+
+/* Same as twfa_fa_fwd, additionally recording the issue trace of CTA 0:
+ * per warp w, trace[w * cap * 4] = number of records n, followed by n records
+ * of 4 uint32 {node, iteration, trip, clock} (device buffer of
+ * num_warps * cap * 4 uint32, zeroed by the caller). */
+int twfa_fa_fwd_traced(const twfa_plan* plan, const void* q, const void* k, const void* v, void* o,
+                       float* lse, int B, int H, int S, int D, int causal, float softmax_scale,
+                       uint32_t* trace, uint32_t cap, void* stream);
+
+/* Host-buffer form of twfa_fa_fwd for CPU callers (the reference's C++ host,
+ * the CLI): copies Q, K, V to the device, runs, copies O (and lse) back,
+ * synchronously. Device staging buffers are cached per thread. */
+int twfa_fa_fwd_host(const twfa_plan* plan, const uint16_t* q, const uint16_t* k, const uint16_t* v,
+                     uint16_t* o, float* lse, int B, int H, int S, int D, int causal, float softmax_scale);
+
+/* GEMM mainloop plan: C[M,N] = A[M,K] * B[N,K]^T, bf16 in/out, fp32 accumulate.
+ * M % 128 == 0, N % 256 == 0, K % 64 == 0. */
+int twfa_gemm(const twfa_plan* plan, const void* a, const void* b, void* c, int M, int N, int K,
+              void* stream);
+
+/* Persistent grid size used by the launches (number of SMs of the current device). */
+int twfa_grid_size(int* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,90 @@
+"""Build libtwfa.so in-tree (sm_100a only) with explicit nvcc/g++ commands.
+
+The library is the product: the CUDA kernels (fa_fwd_sm100.cu, gemm_sm100.cu),
+the schedule lowering (lowering.cpp) and the extern "C" boundary (capi.cpp,
+include/twfa.h). No torch types cross it.
+"""
+import os
+import shutil
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+OBJ = os.path.join(PKG, "_obj")
+LIB = os.path.join(PKG, "libtwfa.so")
+
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+CUDA_HOME = os.path.dirname(os.path.dirname(NVCC))
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def json_include():
+    import sysconfig
+    p = os.path.join(sysconfig.get_paths()["purelib"], "include", "cudnn_frontend", "thirdparty", "nlohmann")
+    if not os.path.exists(os.path.join(p, "json.hpp")):
+        raise RuntimeError("nlohmann/json.hpp not found at " + p)
+    return p
+
+
+def host_cxx():
+    # the /opt/gcc wrapper works for plain C++; prefer the system compiler
+    return "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
+
+
+def run(cmd, verbose):
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("build step failed: " + " ".join(cmd[:3]))
+    return r.stdout + r.stderr
+
+
+def sources():
+    cu = [os.path.join(CSRC, f) for f in ("fa_fwd_sm100.cu", "gemm_sm100.cu")]
+    cpp = [os.path.join(CSRC, f) for f in ("lowering.cpp", "capi.cpp")]
+    return cu, cpp
+
+
+def stale():
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "twfa.h")]
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(force=False, verbose=False, ptxas_info=False):
+    if not force and not stale():
+        return LIB
+    os.makedirs(OBJ, exist_ok=True)
+    cu, cpp = sources()
+    inc = ["-I" + CSRC, "-I" + os.path.join(ROOT, "include"), "-I" + json_include()]
+    objs = []
+    log = ""
+    for src in cu:
+        obj = os.path.join(OBJ, os.path.basename(src) + ".o")
+        cmd = [NVCC, *ARCH, "-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-c", src, "-o", obj, *inc,
+               "--use_fast_math", "-Xptxas", "-v" if ptxas_info else "-O3"]
+        log += run(cmd, verbose)
+        objs.append(obj)
+    for src in cpp:
+        obj = os.path.join(OBJ, os.path.basename(src) + ".o")
+        cmd = [host_cxx(), "-std=c++17", "-O2", "-fPIC", "-Wall", "-c", src, "-o", obj, *inc,
+               "-I" + os.path.join(CUDA_HOME, "include")]
+        log += run(cmd, verbose)
+        objs.append(obj)
+    tmp = LIB + ".tmp"
+    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"]
+    log += run(cmd, verbose)
+    shutil.move(tmp, LIB)
+    if ptxas_info:
+        print(log)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose=True, ptxas_info="--ptxas" in sys.argv)

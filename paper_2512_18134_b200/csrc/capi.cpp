@@ -1,0 +1,274 @@
+// extern "C" boundary of libtwfa (include/twfa.h). Exceptions stop here and
+// become the 0/1/2/3 return codes of the reference's CLI (cli.cpp:462-471).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/twfa.h"
+#include "fa_fwd.h"
+#include "lowering.h"
+
+struct twfa_plan {
+  twfa::LoweredSchedule sched;
+  std::string description;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    g_last_error.clear();
+    return f();
+  } catch (const twfa::UsageError& e) {
+    return fail(TWFA_EUSAGE, e.what());
+  } catch (const twfa::DomainError& e) {
+    return fail(TWFA_EDOMAIN, e.what());
+  } catch (const CudaError& e) {
+    return fail(TWFA_ECUDA, e.what());
+  } catch (const std::exception& e) {
+    return fail(TWFA_EDOMAIN, e.what());
+  } catch (...) {
+    return fail(TWFA_EDOMAIN, "unknown error");
+  }
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point, so the
+// library does not link libcuda directly.
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  if (!fn) throw CudaError("cuTensorMapEncodeTiled is unavailable");
+  return fn;
+}
+
+// bf16 tensor of `rank` dims (innermost first), 128-byte swizzled boxes
+CUtensorMap make_map(const void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides_bytes,
+                     const cuuint32_t* box) {
+  CUtensorMap m;
+  cuuint32_t elem[3] = {1, 1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, static_cast<cuuint32_t>(rank),
+                           const_cast<void*>(base), dims, strides_bytes, box, elem,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+  return m;
+}
+
+int sm_count() {
+  int dev = 0, n = 0;
+  check(cudaGetDevice(&dev), "cudaGetDevice");
+  check(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev), "cudaDeviceGetAttribute");
+  return n;
+}
+
+void require_aligned(const void* p, const char* what) {
+  if (p == nullptr) throw twfa::UsageError(std::string(what) + " is NULL");
+  if (reinterpret_cast<uintptr_t>(p) % 16 != 0) throw twfa::UsageError(std::string(what) + " is not 16-byte aligned");
+}
+
+int fa_fwd_impl(const twfa_plan* plan, const void* q, const void* k, const void* v, void* o, float* lse, int B,
+                int H, int S, int D, int causal, float scale, uint32_t* trace, uint32_t cap, void* stream) {
+  if (!plan) throw twfa::UsageError("plan is NULL");
+  const TwfaDevicePlan& p = plan->sched.plan;
+  if (p.family != TWFA_FAMILY_FA_FWD) throw twfa::UsageError("plan is not an FA-forward plan");
+  if (D != 128) throw twfa::UsageError("head dim must be 128");
+  if (B < 1 || H < 1 || S < 1) throw twfa::UsageError("B, H, S must be positive");
+  if (!(scale > 0.f) || !std::isfinite(scale)) throw twfa::UsageError("softmax_scale must be positive");
+  if (p.num_tiles != 2) throw twfa::UsageError("the kernel runs two 128-row Q sub-tiles per CTA");
+  require_aligned(q, "q");
+  require_aligned(k, "k");
+  require_aligned(v, "v");
+  require_aligned(o, "o");
+  const cuuint64_t bh = static_cast<cuuint64_t>(B) * H;
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(S), bh};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 2, static_cast<cuuint64_t>(S) * D * 2};
+  const cuuint32_t box[3] = {64, 128, 1};
+  const CUtensorMap tq = make_map(q, 3, dims, strides, box);
+  const CUtensorMap tk = make_map(k, 3, dims, strides, box);
+  const CUtensorMap tv = make_map(v, 3, dims, strides, box);
+  twfa::FaArgs a{};
+  a.o = static_cast<__nv_bfloat16*>(o);
+  a.lse = lse;
+  a.trace = trace;
+  a.trace_cap = cap;
+  a.B = B;
+  a.H = H;
+  a.S = S;
+  a.causal = causal ? 1 : 0;
+  a.scale_log2 = scale * 1.4426950408889634f;
+  const long long work = static_cast<long long>(bh) * ((S + 255) / 256);
+  const int grid = static_cast<int>(std::min<long long>(work, sm_count()));
+  check(twfa::fa_fwd_launch(tq, tk, tv, p, a, grid, static_cast<cudaStream_t>(stream)), "fa_fwd launch");
+  return TWFA_OK;
+}
+
+struct HostStaging {
+  void* buf = nullptr;
+  size_t bytes = 0;
+  ~HostStaging() {
+    if (buf) cudaFree(buf);
+  }
+  void* get(size_t n) {
+    if (n > bytes) {
+      if (buf) cudaFree(buf);
+      buf = nullptr;
+      check(cudaMalloc(&buf, n), "cudaMalloc");
+      bytes = n;
+    }
+    return buf;
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+int twfa_abi_version(void) { return 1; }
+
+const char* twfa_last_error(void) { return g_last_error.c_str(); }
+
+int twfa_plan_create(const char* problem_json, const char* solution_json, twfa_plan** out) {
+  return guarded([&] {
+    if (!problem_json || !solution_json || !out) throw twfa::UsageError("NULL argument");
+    auto* p = new twfa_plan{twfa::lower(problem_json, solution_json), {}};
+    p->description = twfa::describe(p->sched);
+    *out = p;
+    return TWFA_OK;
+  });
+}
+
+void twfa_plan_destroy(twfa_plan* plan) { delete plan; }
+
+int twfa_plan_describe(const twfa_plan* plan, char* buf, size_t cap, size_t* needed) {
+  return guarded([&] {
+    if (!plan) throw twfa::UsageError("plan is NULL");
+    const std::string& d = plan->description;
+    if (needed) *needed = d.size() + 1;
+    if (buf && cap > 0) {
+      const size_t n = std::min(cap - 1, d.size());
+      std::memcpy(buf, d.data(), n);
+      buf[n] = '\0';
+    }
+    return TWFA_OK;
+  });
+}
+
+int twfa_plan_raw(const twfa_plan* plan, void* dst, size_t cap, size_t* needed) {
+  return guarded([&] {
+    if (!plan) throw twfa::UsageError("plan is NULL");
+    if (needed) *needed = sizeof(TwfaDevicePlan);
+    if (dst) {
+      if (cap < sizeof(TwfaDevicePlan)) throw twfa::UsageError("buffer too small");
+      std::memcpy(dst, &plan->sched.plan, sizeof(TwfaDevicePlan));
+    }
+    return TWFA_OK;
+  });
+}
+
+int twfa_fa_fwd(const twfa_plan* plan, const void* q, const void* k, const void* v, void* o, float* lse, int B,
+                int H, int S, int D, int causal, float softmax_scale, void* stream) {
+  return guarded(
+      [&] { return fa_fwd_impl(plan, q, k, v, o, lse, B, H, S, D, causal, softmax_scale, nullptr, 0, stream); });
+}
+
+int twfa_fa_fwd_traced(const twfa_plan* plan, const void* q, const void* k, const void* v, void* o, float* lse,
+                       int B, int H, int S, int D, int causal, float softmax_scale, uint32_t* trace, uint32_t cap,
+                       void* stream) {
+  return guarded([&] {
+    if (!trace || cap < 2) throw twfa::UsageError("trace buffer missing");
+    return fa_fwd_impl(plan, q, k, v, o, lse, B, H, S, D, causal, softmax_scale, trace, cap, stream);
+  });
+}
+
+int twfa_fa_fwd_host(const twfa_plan* plan, const uint16_t* q, const uint16_t* k, const uint16_t* v, uint16_t* o,
+                     float* lse, int B, int H, int S, int D, int causal, float softmax_scale) {
+  return guarded([&] {
+    if (!q || !k || !v || !o) throw twfa::UsageError("NULL host buffer");
+    if (B < 1 || H < 1 || S < 1 || D != 128) throw twfa::UsageError("unsupported shape");
+    thread_local HostStaging staging;
+    const size_t elems = static_cast<size_t>(B) * H * S * D;
+    const size_t tb = elems * 2;
+    const size_t lb = lse ? static_cast<size_t>(B) * H * S * 4 : 0;
+    uint8_t* base = static_cast<uint8_t*>(staging.get(4 * tb + lb + 64));
+    void* dq = base;
+    void* dk = base + tb;
+    void* dv = base + 2 * tb;
+    void* dout = base + 3 * tb;
+    float* dl = lse ? reinterpret_cast<float*>(base + 4 * tb) : nullptr;
+    check(cudaMemcpy(dq, q, tb, cudaMemcpyHostToDevice), "H2D q");
+    check(cudaMemcpy(dk, k, tb, cudaMemcpyHostToDevice), "H2D k");
+    check(cudaMemcpy(dv, v, tb, cudaMemcpyHostToDevice), "H2D v");
+    int rc = fa_fwd_impl(plan, dq, dk, dv, dout, dl, B, H, S, D, causal, softmax_scale, nullptr, 0, nullptr);
+    if (rc != TWFA_OK) return rc;
+    check(cudaMemcpy(o, dout, tb, cudaMemcpyDeviceToHost), "D2H o");
+    if (lse) check(cudaMemcpy(lse, dl, lb, cudaMemcpyDeviceToHost), "D2H lse");
+    return TWFA_OK;
+  });
+}
+
+int twfa_gemm(const twfa_plan* plan, const void* a, const void* b, void* c, int M, int N, int K, void* stream) {
+  return guarded([&] {
+    if (!plan) throw twfa::UsageError("plan is NULL");
+    const TwfaDevicePlan& p = plan->sched.plan;
+    if (p.family != TWFA_FAMILY_GEMM) throw twfa::UsageError("plan is not a GEMM plan");
+    if (M <= 0 || N <= 0 || K <= 0 || M % 128 || N % 256 || K % 64)
+      throw twfa::UsageError("GEMM needs M % 128 == 0, N % 256 == 0, K % 64 == 0");
+    if (p.k_depth < 1 || p.k_depth > 4) throw twfa::UsageError("GEMM ring depth must be 1..4");
+    require_aligned(a, "a");
+    require_aligned(b, "b");
+    require_aligned(c, "c");
+    const cuuint64_t da[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(M)};
+    const cuuint64_t db[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(N)};
+    const cuuint64_t st[1] = {static_cast<cuuint64_t>(K) * 2};
+    const cuuint32_t ba[2] = {64, 128};
+    const cuuint32_t bb[2] = {64, 256};
+    const CUtensorMap ta = make_map(a, 2, da, st, ba);
+    const CUtensorMap tb = make_map(b, 2, db, st, bb);
+    twfa::GemmArgs ga{static_cast<__nv_bfloat16*>(c), M, N, K};
+    const int tiles = (M / 128) * (N / 256);
+    const int grid = std::min(tiles, sm_count());
+    check(twfa::gemm_launch(ta, tb, p, ga, grid, static_cast<cudaStream_t>(stream)), "gemm launch");
+    return TWFA_OK;
+  });
+}
+
+int twfa_grid_size(int* out) {
+  return guarded([&] {
+    if (!out) throw twfa::UsageError("NULL argument");
+    *out = sm_count();
+    return TWFA_OK;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,36 @@
+// Launch interfaces of the sm_100a kernels (internal to libtwfa).
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "plan.h"
+
+namespace twfa {
+
+struct FaArgs {
+  __nv_bfloat16* o;    // [B, H, S, 128]
+  float* lse;          // [B, H, S] natural log-sum-exp, or nullptr
+  uint32_t* trace;     // per-warp issue records of CTA 0 (debug), or nullptr
+  uint32_t trace_cap;  // records per warp (entry 0 of each warp = count)
+  int B, H, S;
+  int causal;
+  float scale_log2;    // softmax_scale * log2(e)
+};
+
+size_t fa_fwd_smem_bytes(const TwfaDevicePlan& plan);
+cudaError_t fa_fwd_launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                          const TwfaDevicePlan& plan, const FaArgs& args, int grid, cudaStream_t stream);
+
+struct GemmArgs {
+  __nv_bfloat16* c;  // [M, N] row-major
+  int M, N, K;
+};
+
+size_t gemm_smem_bytes(const TwfaDevicePlan& plan);
+cudaError_t gemm_launch(const CUtensorMap& ta, const CUtensorMap& tb, const TwfaDevicePlan& plan,
+                        const GemmArgs& args, int grid, cudaStream_t stream);
+
+}  // namespace twfa

@@ -1,0 +1,410 @@
+// Schedule -> kernel lowering. See lowering.h for the contract.
+#include "lowering.h"
+
+#include <algorithm>
+#include <cstring>
+#include <set>
+
+#include "json.hpp"
+
+namespace twfa {
+namespace {
+
+using json = nlohmann::json;
+
+void require_keys(const json& obj, const char* what, std::initializer_list<const char*> allowed) {
+  for (auto it = obj.begin(); it != obj.end(); ++it) {
+    bool ok = false;
+    for (const char* k : allowed) ok = ok || it.key() == k;
+    if (!ok) throw DomainError(std::string(what) + " has unknown key \"" + it.key() + "\"");
+  }
+}
+
+int64_t get_int(const json& obj, const char* what, const char* key, bool required, int64_t dflt) {
+  auto it = obj.find(key);
+  if (it == obj.end()) {
+    if (required) throw DomainError(std::string(what) + " requires \"" + key + "\"");
+    return dflt;
+  }
+  if (!it->is_number_integer()) throw DomainError(std::string(what) + " key \"" + key + "\" must be an integer");
+  return it->get<int64_t>();
+}
+
+// ---- problem: the subset of ir.cpp:93-229 the executor needs, same strictness
+void parse_problem(const std::string& text, LoweredSchedule& s) {
+  json root;
+  try {
+    root = json::parse(text);
+  } catch (const json::exception& e) {
+    throw DomainError(std::string("problem is not valid JSON: ") + e.what());
+  }
+  if (!root.is_object()) throw DomainError("problem top level must be an object");
+  require_keys(root, "problem", {"machine", "graph"});
+  if (!root.contains("machine") || !root.contains("graph"))
+    throw DomainError("problem requires \"machine\" and \"graph\"");
+  const json& mj = root["machine"];
+  if (!mj.is_object()) throw DomainError("\"machine\" must be an object");
+  require_keys(mj, "machine", {"units", "memories", "num_warps", "reg_limit", "vl_warp"});
+  s.num_warps = static_cast<int>(get_int(mj, "machine", "num_warps", true, 1));
+  s.vl_warp = static_cast<int>(get_int(mj, "machine", "vl_warp", true, 0));
+  if (s.num_warps <= 0) throw DomainError("num_warps must be positive");
+  if (s.vl_warp < 0 || s.vl_warp >= s.num_warps) throw DomainError("vl_warp must lie in [0, num_warps)");
+  if (!mj.contains("units") || !mj["units"].is_array()) throw DomainError("machine requires a \"units\" array");
+
+  const json& gj = root["graph"];
+  if (!gj.is_object()) throw DomainError("\"graph\" must be an object");
+  require_keys(gj, "graph", {"nodes", "edges"});
+  if (!gj.contains("nodes") || !gj["nodes"].is_array() || gj["nodes"].empty())
+    throw DomainError("graph requires a nonempty \"nodes\" array");
+  std::map<std::string, int> index;
+  for (const json& nj : gj["nodes"]) {
+    if (!nj.is_object()) throw DomainError("node entries must be objects");
+    require_keys(nj, "node", {"id", "rrt", "cycles", "regs", "footprint", "spill_cost",
+                              "variable_latency", "warps_required"});
+    LNode n;
+    if (!nj.contains("id") || !nj["id"].is_string()) throw DomainError("node requires a string \"id\"");
+    n.id = nj["id"].get<std::string>();
+    if (n.id.empty()) throw DomainError("node id must be nonempty");
+    if (index.count(n.id)) throw DomainError("duplicate node \"" + n.id + "\"");
+    n.cycles = get_int(nj, "node", "cycles", true, 1);
+    if (n.cycles < 1) throw DomainError("node \"" + n.id + "\" cycles must be >= 1");
+    n.warps_required = static_cast<int>(get_int(nj, "node", "warps_required", false, 1));
+    if (n.warps_required < 1) throw DomainError("warps_required must be >= 1");
+    n.spill_cost = get_int(nj, "node", "spill_cost", false, 0);
+    if (nj.contains("variable_latency")) {
+      if (!nj["variable_latency"].is_boolean()) throw DomainError("variable_latency must be a boolean");
+      n.variable_latency = nj["variable_latency"].get<bool>();
+    }
+    index[n.id] = static_cast<int>(s.nodes.size());
+    s.nodes.push_back(n);
+  }
+  if (gj.contains("edges")) {
+    if (!gj["edges"].is_array()) throw DomainError("\"edges\" must be an array");
+    for (const json& ej : gj["edges"]) {
+      if (!ej.is_object()) throw DomainError("edge entries must be objects");
+      require_keys(ej, "edge", {"src", "dst", "d", "delta", "blocking"});
+      LEdge e;
+      if (!ej.contains("src") || !ej["src"].is_string() || !ej.contains("dst") || !ej["dst"].is_string())
+        throw DomainError("edge requires string \"src\" and \"dst\"");
+      auto si = index.find(ej["src"].get<std::string>());
+      auto di = index.find(ej["dst"].get<std::string>());
+      if (si == index.end() || di == index.end()) throw DomainError("edge references an undeclared node");
+      e.src = si->second;
+      e.dst = di->second;
+      e.d = get_int(ej, "edge", "d", true, 0);
+      e.delta = static_cast<int>(get_int(ej, "edge", "delta", false, 0));
+      if (e.d < 0 || e.delta < 0) throw DomainError("edge d and delta must be >= 0");
+      if (ej.contains("blocking")) e.blocking = ej["blocking"].get<bool>();
+      s.edges.push_back(e);
+    }
+  }
+  for (const LNode& n : s.nodes)
+    if (n.warps_required > s.num_warps) throw DomainError("node \"" + n.id + "\" needs more warps than the machine has");
+}
+
+// ---- solution: solution_from_json (cli.cpp:96-155) + reconstruct (:161-168)
+void parse_solution(const std::string& text, LoweredSchedule& s) {
+  json j;
+  try {
+    j = json::parse(text);
+  } catch (const json::exception& e) {
+    throw DomainError(std::string("invalid solution JSON: ") + e.what());
+  }
+  if (!j.is_object()) throw DomainError("solution JSON must be an object");
+  require_keys(j, "solution", {"I", "L", "M", "A", "streaming_depths", "search_report"});
+  if (!j.contains("I") || !j["I"].is_number_integer() || j["I"].get<int64_t>() < 1)
+    throw DomainError("solution needs a positive integer I");
+  if (!j.contains("L") || !j["L"].is_number_integer() || j["L"].get<int64_t>() < 1)
+    throw DomainError("solution needs a positive integer L");
+  if (!j.contains("M") || !j["M"].is_object()) throw DomainError("solution needs an M object");
+  s.ii = j["I"].get<int64_t>();
+  s.length = j["L"].get<int64_t>();
+  const size_t n = s.nodes.size();
+  s.m.assign(n, 0);
+  s.a.assign(n, 0);
+  auto node_of = [&](const std::string& id) {
+    for (size_t v = 0; v < n; ++v)
+      if (s.nodes[v].id == id) return static_cast<int>(v);
+    return -1;
+  };
+  for (auto it = j["M"].begin(); it != j["M"].end(); ++it) {
+    int v = node_of(it.key());
+    if (v < 0) throw DomainError("M names unknown node " + it.key());
+    if (!it.value().is_number_integer()) throw DomainError("M[" + it.key() + "] must be an integer");
+    s.m[static_cast<size_t>(v)] = it.value().get<int64_t>();
+  }
+  if (j["M"].size() != n) throw DomainError("M must cover every node exactly once");
+  if (j.contains("A")) {
+    if (!j["A"].is_object()) throw DomainError("A must be an object");
+    for (auto it = j["A"].begin(); it != j["A"].end(); ++it) {
+      int v = node_of(it.key());
+      if (v < 0) throw DomainError("A names unknown node " + it.key());
+      if (!it.value().is_number_integer()) throw DomainError("A[" + it.key() + "] must be an integer");
+      s.a[static_cast<size_t>(v)] = it.value().get<int>();
+    }
+  }
+  if (j.contains("streaming_depths")) {
+    if (!j["streaming_depths"].is_object()) throw DomainError("streaming_depths must be an object");
+    for (auto it = j["streaming_depths"].begin(); it != j["streaming_depths"].end(); ++it) {
+      if (!it.value().is_number_integer()) throw DomainError("streaming depth must be an integer");
+      s.streaming_depths[it.key()] = it.value().get<int64_t>();
+    }
+  }
+  // The graph the tables expand against is the streamed one whenever depths
+  // were recorded: variable-latency ops without predecessors issue in zero
+  // cycles (jointsolve.cpp:511-524).
+  if (!s.streaming_depths.empty()) {
+    std::vector<int> indeg(n, 0);
+    for (const LEdge& e : s.edges) ++indeg[static_cast<size_t>(e.dst)];
+    for (size_t v = 0; v < n; ++v)
+      if (s.nodes[v].variable_latency && indeg[v] == 0) s.nodes[v].cycles = 0;
+  }
+  for (size_t v = 0; v < n; ++v) {
+    const int64_t eff = std::max<int64_t>(1, s.nodes[v].cycles);
+    if (s.m[v] < 0 || s.m[v] > s.length - eff)
+      throw DomainError("M[" + s.nodes[v].id + "] = " + std::to_string(s.m[v]) + " does not fit in L");
+    const int wr = std::max(1, s.nodes[v].warps_required);
+    if (s.a[v] < 0 || s.a[v] + wr > s.num_warps || s.a[v] % wr != 0)
+      throw DomainError("A[" + s.nodes[v].id + "] is not an aligned warp range of the machine");
+  }
+  s.copies = (s.length + s.ii - 1) / s.ii;
+}
+
+// Node id -> executor op. The ids are the names the FA / GEMM loop problems
+// use (tools/make_problems.py); anything else cannot be realized.
+bool classify(const std::string& id, uint8_t& kind, uint8_t& tile) {
+  struct Pfx { const char* p; uint8_t k; };
+  static const Pfx fixed[] = {{"LDK", TWFA_OP_LDK}, {"LDV", TWFA_OP_LDV}, {"LDA", TWFA_OP_LDA},
+                              {"LDB", TWFA_OP_LDB}, {"MMA", TWFA_OP_MMA}};
+  for (const Pfx& f : fixed)
+    if (id == f.p) { kind = f.k; tile = 0; return true; }
+  static const Pfx tiled[] = {{"MX", TWFA_OP_MX}, {"EX", TWFA_OP_EX}, {"CR", TWFA_OP_CR},
+                              {"PV", TWFA_OP_PV}, {"S", TWFA_OP_S}};
+  for (const Pfx& f : tiled) {
+    const size_t l = std::strlen(f.p);
+    if (id.size() == l + 1 && id.compare(0, l, f.p) == 0 && id[l] >= '0' && id[l] < '0' + TWFA_MAX_TILES) {
+      kind = f.k;
+      tile = static_cast<uint8_t>(id[l] - '0');
+      return true;
+    }
+  }
+  return false;
+}
+
+void derive(LoweredSchedule& s) {
+  const size_t n = s.nodes.size();
+  if (n > TWFA_MAX_NODES) throw DomainError("graph has more nodes than the executor supports");
+  if (s.num_warps > TWFA_MAX_WARPS) throw DomainError("machine has more warps than a CTA of the executor");
+  TwfaDevicePlan& p = s.plan;
+  std::memset(&p, 0, sizeof(p));
+  p.ii = static_cast<int32_t>(s.ii);
+  p.length = static_cast<int32_t>(s.length);
+  p.copies = static_cast<int32_t>(s.copies);
+  p.num_nodes = static_cast<int32_t>(n);
+  p.num_warps = s.num_warps;
+  s.stage.assign(n, 0);
+  s.slot.assign(n, 0);
+  std::set<int> kinds;
+  int max_stage = 0;
+  for (size_t v = 0; v < n; ++v) {
+    TwfaPlanOp& op = p.ops[v];
+    uint8_t kind = 0, tile = 0;
+    if (!classify(s.nodes[v].id, kind, tile))
+      throw DomainError("node \"" + s.nodes[v].id + "\" has no sm_100a realization");
+    s.stage[v] = s.m[v] / s.ii;
+    s.slot[v] = s.m[v] % s.ii;
+    if (s.stage[v] > 250) throw DomainError("schedule too deep");
+    max_stage = std::max<int>(max_stage, static_cast<int>(s.stage[v]));
+    op.node = static_cast<uint8_t>(v);
+    op.kind = kind;
+    op.tile = tile;
+    op.stage = static_cast<uint8_t>(s.stage[v]);
+    op.slot = static_cast<uint8_t>(s.slot[v]);
+    op.warp_start = static_cast<uint8_t>(s.a[v]);
+    op.warp_count = static_cast<uint8_t>(std::max(1, s.nodes[v].warps_required));
+    kinds.insert(kind);
+  }
+  p.max_stage = max_stage;
+
+  // per-warp trip programs: ops covering the warp, ordered by their cycle in
+  // the trip and then by declaration order -- the same key the reference's
+  // program synthesis sorts a region by (codegen.cpp:179-183)
+  s.warp_prog.assign(static_cast<size_t>(s.num_warps), {});
+  for (int w = 0; w < s.num_warps; ++w) {
+    std::vector<int>& prog = s.warp_prog[static_cast<size_t>(w)];
+    for (size_t v = 0; v < n; ++v)
+      if (p.ops[v].warp_start <= w && w < p.ops[v].warp_start + p.ops[v].warp_count)
+        prog.push_back(static_cast<int>(v));
+    std::stable_sort(prog.begin(), prog.end(), [&](int x, int y) {
+      return std::make_pair(s.slot[static_cast<size_t>(x)], x) < std::make_pair(s.slot[static_cast<size_t>(y)], y);
+    });
+    p.prog_len[w] = static_cast<uint8_t>(prog.size());
+    for (size_t i = 0; i < prog.size(); ++i) {
+      p.prog[w][i] = static_cast<uint8_t>(prog[i]);
+      if (w == p.ops[prog[i]].warp_start) p.ops[prog[i]].order = static_cast<uint8_t>(i);
+    }
+  }
+  // Realizability of the order: a consumer that issues in the same cycle as
+  // its producer on a shared warp must come after it in the trip program,
+  // otherwise the warp would wait on itself.
+  for (const LEdge& e : s.edges) {
+    if (e.src == e.dst) continue;
+    const TwfaPlanOp& u = p.ops[e.src];
+    const TwfaPlanOp& v = p.ops[e.dst];
+    const int64_t gap = s.m[static_cast<size_t>(e.dst)] + e.delta * s.ii - s.m[static_cast<size_t>(e.src)];
+    if (gap < e.d)
+      throw DomainError("schedule violates dependence " + s.nodes[e.src].id + " -> " + s.nodes[e.dst].id);
+    const bool share = u.warp_start < v.warp_start + v.warp_count && v.warp_start < u.warp_start + u.warp_count;
+    if (gap == 0 && share && e.dst < e.src)
+      throw DomainError("same-cycle dependence " + s.nodes[e.src].id + " -> " + s.nodes[e.dst].id +
+                        " is ordered consumer-first on a shared warp");
+  }
+
+  auto depth_of = [&](const char* id) -> int32_t {
+    auto it = s.streaming_depths.find(id);
+    return it == s.streaming_depths.end() ? 0 : static_cast<int32_t>(it->second);
+  };
+  auto node_id = [&](const std::string& id) {
+    for (size_t v = 0; v < n; ++v)
+      if (s.nodes[v].id == id) return static_cast<int>(v);
+    return -1;
+  };
+  // streamed loads: ring depth must cover the stage lag to every consumer
+  auto check_ring = [&](int ld, int32_t depth) {
+    if (depth < 1) throw DomainError("streamed load " + s.nodes[ld].id + " has no ring depth");
+    for (const LEdge& e : s.edges) {
+      if (e.src != ld) continue;
+      const int64_t lag = s.stage[static_cast<size_t>(e.dst)] + e.delta - s.stage[static_cast<size_t>(ld)];
+      if (lag >= depth)
+        throw DomainError("ring depth " + std::to_string(depth) + " of " + s.nodes[ld].id +
+                          " is shallower than its consumer lag");
+    }
+  };
+
+  const bool is_fa = kinds.count(TWFA_OP_S) && kinds.count(TWFA_OP_PV);
+  const bool is_gemm = kinds.count(TWFA_OP_MMA) && kinds.count(TWFA_OP_LDA) && kinds.count(TWFA_OP_LDB);
+  if (is_fa == is_gemm) throw DomainError("graph is neither the FA-forward nor the GEMM loop");
+  if (is_gemm) {
+    p.family = TWFA_FAMILY_GEMM;
+    const int lda = node_id("LDA"), ldb = node_id("LDB"), mma = node_id("MMA");
+    if (n != 3) throw DomainError("GEMM loop must have exactly LDA, LDB, MMA");
+    if (p.ops[lda].warp_start != p.ops[ldb].warp_start)
+      throw DomainError("LDA and LDB must share the TMA warp");
+    if (p.ops[mma].warp_count != 1) throw DomainError("MMA issue is single-warp");
+    if (p.ops[mma].warp_start == p.ops[lda].warp_start)
+      throw DomainError("MMA issue cannot share the TMA warp");
+    p.load_warp = p.ops[lda].warp_start;
+    p.mma_warp = p.ops[mma].warp_start;
+    p.k_depth = depth_of("LDA");
+    p.v_depth = depth_of("LDB");
+    if (p.k_depth != p.v_depth) throw DomainError("LDA and LDB must stream with one ring depth");
+    check_ring(lda, p.k_depth);
+    check_ring(ldb, p.v_depth);
+    if (s.ii != 1 || max_stage != 0)
+      throw DomainError("GEMM mainloop realization expects the I = 1 single-stage schedule");
+    return;
+  }
+
+  p.family = TWFA_FAMILY_FA_FWD;
+  int tiles = 0;
+  while (tiles < TWFA_MAX_TILES && node_id("S" + std::to_string(tiles)) >= 0) ++tiles;
+  if (tiles < 1) throw DomainError("FA loop needs S0");
+  p.num_tiles = tiles;
+  const int ldk = node_id("LDK"), ldv = node_id("LDV");
+  if (ldk < 0 || ldv < 0) throw DomainError("FA loop needs LDK and LDV");
+  for (int k = 0; k < tiles; ++k)
+    for (const char* pre : {"S", "MX", "EX", "CR", "PV"})
+      if (node_id(pre + std::to_string(k)) < 0)
+        throw DomainError(std::string("FA loop is missing ") + pre + std::to_string(k));
+  if (static_cast<int>(n) != 2 + 5 * tiles) throw DomainError("FA loop has unexpected extra nodes");
+  if (p.ops[ldk].warp_start != p.ops[ldv].warp_start || p.ops[ldk].warp_count != 1)
+    throw DomainError("LDK and LDV must be issued by one TMA warp");
+  p.load_warp = p.ops[ldk].warp_start;
+  p.k_depth = depth_of("LDK");
+  p.v_depth = depth_of("LDV");
+  check_ring(ldk, p.k_depth);
+  check_ring(ldv, p.v_depth);
+  for (int k = 0; k < tiles; ++k) {
+    const TwfaPlanOp& mx = p.ops[node_id("MX" + std::to_string(k))];
+    const TwfaPlanOp& ex = p.ops[node_id("EX" + std::to_string(k))];
+    const TwfaPlanOp& cr = p.ops[node_id("CR" + std::to_string(k))];
+    const TwfaPlanOp& sk = p.ops[node_id("S" + std::to_string(k))];
+    const TwfaPlanOp& pv = p.ops[node_id("PV" + std::to_string(k))];
+    // TMEM lane quadrants: a 128-row tile is touched by 4 warps, one per
+    // quadrant (warp % 4), so row-wise ops need an aligned warpgroup.
+    for (const TwfaPlanOp* o : {&mx, &ex, &cr})
+      if (o->warp_count != 4 || o->warp_start % 4 != 0)
+        throw DomainError("softmax/correction ops of tile " + std::to_string(k) + " must run on a warpgroup");
+    // running max and row sum are carried in registers of one warpgroup
+    if (mx.warp_start != ex.warp_start)
+      throw DomainError("MX" + std::to_string(k) + " and EX" + std::to_string(k) + " must share a warpgroup");
+    if (sk.warp_count != 1 || pv.warp_count != 1) throw DomainError("MMA issue ops are single-warp");
+    if (sk.warp_start == p.load_warp || pv.warp_start == p.load_warp)
+      throw DomainError("MMA issue cannot share the TMA warp");
+    p.sm_warp[k] = mx.warp_start;
+    p.cr_warp[k] = cr.warp_start;
+  }
+  // smem: Q (tiles x 32 KiB) + K ring + V ring of 32 KiB slots
+  const int64_t smem = 32768LL * (tiles + p.k_depth + p.v_depth);
+  if (smem > 200 * 1024) throw DomainError("ring depths exceed shared memory");
+}
+
+}  // namespace
+
+LoweredSchedule lower(const std::string& problem_json, const std::string& solution_json) {
+  LoweredSchedule s;
+  parse_problem(problem_json, s);
+  parse_solution(solution_json, s);
+  derive(s);
+  return s;
+}
+
+std::string describe(const LoweredSchedule& s) {
+  json j;
+  const TwfaDevicePlan& p = s.plan;
+  j["family"] = p.family == TWFA_FAMILY_FA_FWD ? "fa_fwd" : "gemm";
+  j["I"] = s.ii;
+  j["L"] = s.length;
+  j["copies"] = s.copies;
+  j["max_stage"] = p.max_stage;
+  j["num_warps"] = s.num_warps;
+  j["load_warp"] = p.load_warp;
+  json nodes = json::object();
+  for (size_t v = 0; v < s.nodes.size(); ++v) {
+    json o;
+    o["M"] = s.m[v];
+    o["stage"] = s.stage[v];
+    o["slot"] = s.slot[v];
+    o["warp_start"] = s.a[v];
+    o["warp_count"] = std::max(1, s.nodes[v].warps_required);
+    nodes[s.nodes[v].id] = o;
+  }
+  j["nodes"] = nodes;
+  json progs = json::object();
+  for (size_t w = 0; w < s.warp_prog.size(); ++w) {
+    if (s.warp_prog[w].empty()) continue;
+    json arr = json::array();
+    for (int v : s.warp_prog[w]) arr.push_back(s.nodes[static_cast<size_t>(v)].id);
+    progs[std::to_string(w)] = arr;
+  }
+  j["warp_programs"] = progs;
+  json rings = json::object();
+  if (p.family == TWFA_FAMILY_FA_FWD) {
+    rings["K"] = p.k_depth;
+    rings["V"] = p.v_depth;
+    j["num_tiles"] = p.num_tiles;
+    json roles = json::object();
+    for (int k = 0; k < p.num_tiles; ++k) {
+      roles["softmax" + std::to_string(k)] = p.sm_warp[k];
+      roles["correction" + std::to_string(k)] = p.cr_warp[k];
+    }
+    j["warpgroups"] = roles;
+  } else {
+    rings["AB"] = p.k_depth;
+    j["mma_warp"] = p.mma_warp;
+  }
+  j["rings"] = rings;
+  return j.dump();
+}
+
+}  // namespace twfa

@@ -1,0 +1,67 @@
+// KernelPlan: the lowered form of a Twill joint schedule, consumed by the
+// sm_100a kernels. Plain-old-data so it can be passed by value as a kernel
+// parameter (__grid_constant__) and copied to the device unchanged.
+//
+// It is the device-side counterpart of the reference's PipelinedProgram
+// (/root/reference/proj/include/weftsched/codegen.hpp:32-42): instead of a
+// text listing per region, every hardware warp gets the ordered list of loop
+// ops it issues in one steady-state trip, each tagged with its stage
+// (M div I, codegen.cpp:63). Trip r of the realized loop runs op v on
+// iteration r - stage(v); trips with r < max_stage form the prologue and
+// trips past the last iteration the epilogue, so prologue / steady state /
+// epilogue are exactly the region split of codegen.cpp:51-52.
+#pragma once
+#include <stdint.h>
+
+#define TWFA_MAX_NODES 16
+#define TWFA_MAX_WARPS 16
+#define TWFA_MAX_TILES 2
+
+enum TwfaOpKind : uint8_t {
+  TWFA_OP_LDK = 0,  // TMA load of the K tile (streamed, variable latency)
+  TWFA_OP_LDV = 1,  // TMA load of the V tile
+  TWFA_OP_S = 2,    // S_k = Q_k K^T            (tcgen05.mma, SS, into TMEM)
+  TWFA_OP_MX = 3,   // row max of S_k, rescale factor -> correction
+  TWFA_OP_EX = 4,   // P_k = exp2(S_k - m), row sum, P -> TMEM (bf16)
+  TWFA_OP_CR = 5,   // O_k *= exp2(m_old - m_new)  (TMEM read-modify-write)
+  TWFA_OP_PV = 6,   // O_k += P_k V             (tcgen05.mma, TS, into TMEM)
+  TWFA_OP_LDA = 7,  // GEMM: TMA load of the A k-block
+  TWFA_OP_LDB = 8,  // GEMM: TMA load of the B k-block
+  TWFA_OP_MMA = 9,  // GEMM: D += A B^T over one k-block
+  TWFA_OP_COUNT = 10
+};
+
+struct TwfaPlanOp {
+  uint8_t node;        // index in the problem graph (declaration order)
+  uint8_t kind;        // TwfaOpKind
+  uint8_t tile;        // Q sub-tile k for S/MX/EX/CR/PV, else 0
+  uint8_t stage;       // M(v) div I
+  uint8_t slot;        // M(v) mod I  (cycle inside the steady-state trip)
+  uint8_t warp_start;  // A(v)
+  uint8_t warp_count;  // warps_required(v)
+  uint8_t order;       // rank inside the trip on its warp(s)
+};
+
+// Kind of the workload the plan drives.
+enum TwfaPlanFamily : int32_t { TWFA_FAMILY_FA_FWD = 1, TWFA_FAMILY_GEMM = 2 };
+
+struct TwfaDevicePlan {
+  int32_t family;      // TwfaPlanFamily
+  int32_t ii;          // I
+  int32_t length;      // L
+  int32_t copies;      // ceil(L / I)
+  int32_t max_stage;   // max over nodes of M div I (== copies - 1 or less)
+  int32_t num_nodes;
+  int32_t num_warps;   // machine.num_warps: CTA = num_warps x 32 threads (+ extra)
+  int32_t num_tiles;   // Q sub-tiles per CTA (number of S_k nodes)
+  int32_t k_depth;     // smem ring depth of the streamed K (or A) loads
+  int32_t v_depth;     // smem ring depth of the streamed V (or B) loads
+  int32_t load_warp;   // warp issuing the TMA loads (and the per-tile Q load)
+  int32_t cr_warp[TWFA_MAX_TILES];  // warpgroup start running CR_k (+ epilogue of tile k)
+  int32_t sm_warp[TWFA_MAX_TILES];  // warpgroup start running MX_k / EX_k
+  int32_t mma_warp;                 // GEMM: warp issuing MMA
+  TwfaPlanOp ops[TWFA_MAX_NODES];
+  // per-warp trip programs: indices into ops[], in issue order
+  uint8_t prog[TWFA_MAX_WARPS][TWFA_MAX_NODES];
+  uint8_t prog_len[TWFA_MAX_WARPS];
+};

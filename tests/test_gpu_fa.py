@@ -1,0 +1,114 @@
+"""FA-forward parity on the B200: the sm_100a kernel (through the C ABI) against
+the fp32 CPU oracle on the same bf16-rounded inputs.
+
+Tolerance (bf16 output of an fp32-accumulated attention with P rounded to bf16
+before the PV GEMM, N(0,1) inputs, d = 128): max |err| <= 2e-2 and mean |err|
+<= 2e-3 on O; |err| <= 1e-2 on the natural-log LSE. The bf16 rounding of O
+alone contributes up to 2^-9 relative (~4e-3 at |O| ~ 1) and the bf16 P adds
+a comparable relative error per term, averaged over >= 128 keys.
+"""
+import numpy as np
+import pytest
+import torch
+
+from tests import oracle_lib
+
+pytestmark = pytest.mark.gpu
+
+TOL_MAX, TOL_MEAN, TOL_LSE = 2e-2, 2e-3, 1e-2
+
+
+@pytest.fixture(scope="module")
+def plan(twfa):
+    return twfa.Plan(*twfa.load_schedule("fa_fwd"))
+
+
+def _inputs(B, H, S, D, seed):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    return [torch.randn(B, H, S, D, generator=g).to(torch.bfloat16) for _ in range(3)]
+
+
+def _check(twfa, plan, B, H, S, causal, seed, scale=None):
+    q, k, v = _inputs(B, H, S, 128, seed)
+    dev = torch.device("cuda:0")
+    o, lse = twfa.fa_fwd(plan, q.to(dev), k.to(dev), v.to(dev), causal=causal, softmax_scale=scale,
+                         return_lse=True)
+    torch.cuda.synchronize()
+    ro, rl = oracle_lib.attention(q.float().numpy(), k.float().numpy(), v.float().numpy(), causal=causal,
+                                  scale=scale)
+    err = np.abs(o.float().cpu().numpy() - ro)
+    lerr = np.abs(lse.cpu().numpy() - rl)
+    assert np.isfinite(o.float().cpu().numpy()).all()
+    assert err.max() <= TOL_MAX, f"max err {err.max()}"
+    assert err.mean() <= TOL_MEAN, f"mean err {err.mean()}"
+    assert lerr.max() <= TOL_LSE, f"lse err {lerr.max()}"
+
+
+@pytest.mark.parametrize("S", [128, 256, 512, 1024])
+def test_noncausal_matches_oracle(twfa, plan, S):
+    _check(twfa, plan, 1, 2, S, False, 7)
+
+
+@pytest.mark.parametrize("S", [256, 512, 1024])
+def test_causal_matches_oracle(twfa, plan, S):
+    _check(twfa, plan, 1, 2, S, True, 8)
+
+
+@pytest.mark.parametrize("S,causal", [(100, False), (300, False), (300, True), (640, True), (1, False)])
+def test_ragged_sequence_lengths(twfa, plan, S, causal):
+    _check(twfa, plan, 2, 1, S, causal, 9)
+
+
+def test_many_work_tiles_per_cta(twfa, plan):
+    # more (b, h, q-block) tiles than SMs: exercises the persistent loop and
+    # the barrier phases carried across work tiles
+    _check(twfa, plan, 2, 96, 512, False, 10)
+    _check(twfa, plan, 2, 96, 512, True, 11)
+
+
+def test_softmax_scale(twfa, plan):
+    _check(twfa, plan, 1, 2, 256, False, 12, scale=0.3)
+
+
+def test_host_buffer_entry_point(twfa, plan):
+    q, k, v = _inputs(1, 2, 384, 128, 13)
+    bits = [x.view(torch.int16).numpy().view(np.uint16) for x in (q, k, v)]
+    o, lse = twfa.fa_fwd_host(plan, *bits, return_lse=True)
+    ro, rl = oracle_lib.attention(q.float().numpy(), k.float().numpy(), v.float().numpy())
+    err = np.abs(oracle_lib.from_bf16_bits(o) - ro)
+    assert err.max() <= TOL_MAX and err.mean() <= TOL_MEAN
+    assert np.abs(lse - rl).max() <= TOL_LSE
+
+
+def test_full_size_against_cudnn_sdpa(twfa, plan):
+    """BASELINE config 3 shape (B=4 H=32 S=8192): the oracle cannot finish at
+    this size, so compare against torch SDPA (cuDNN / flash, also bf16) on the
+    whole tensor and against the oracle on sampled (b, h) pairs."""
+    B, H, S = 4, 32, 8192
+    dev = torch.device("cuda:0")
+    g = torch.Generator(device=dev).manual_seed(2026)
+    q, k, v = (torch.randn(B, H, S, 128, device=dev, generator=g).to(torch.bfloat16) for _ in range(3))
+    o, lse = twfa.fa_fwd(plan, q, k, v, return_lse=True)
+    ref = torch.nn.functional.scaled_dot_product_attention(q, k, v)
+    d = (o.float() - ref.float()).abs()
+    assert d.max().item() <= 2.5e-2 and d.mean().item() <= 2e-3
+    for b, h in [(0, 0), (3, 31)]:
+        ro, rl = oracle_lib.attention(q[b:b + 1, h:h + 1, :512].float().cpu().numpy(),
+                                      k[b:b + 1, h:h + 1].float().cpu().numpy(),
+                                      v[b:b + 1, h:h + 1].float().cpu().numpy())
+        # first 512 query rows of the pair, all 8192 keys
+        err = np.abs(o[b, h, :512].float().cpu().numpy() - ro[0, 0])
+        assert err.max() <= TOL_MAX
+        assert np.abs(lse[b, h, :512].cpu().numpy() - rl[0, 0]).max() <= TOL_LSE
+
+
+def test_full_size_causal_against_cudnn_sdpa(twfa, plan):
+    """BASELINE config 4 shape (B=2 H=32 S=16384, causal)."""
+    B, H, S = 2, 32, 16384
+    dev = torch.device("cuda:0")
+    g = torch.Generator(device=dev).manual_seed(2027)
+    q, k, v = (torch.randn(B, H, S, 128, device=dev, generator=g).to(torch.bfloat16) for _ in range(3))
+    o = twfa.fa_fwd(plan, q, k, v, causal=True)
+    ref = torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True)
+    d = (o.float() - ref.float()).abs()
+    assert d.max().item() <= 2.5e-2 and d.mean().item() <= 2e-3
