@@ -73,9 +73,10 @@ int twfa_fa_fwd(const twfa_plan* plan, const void* q, const void* k, const void*
                 int B, int H, int S, int D, int causal, float softmax_scale, void* stream);
 
 /* Same as twfa_fa_fwd, additionally recording the issue trace of CTA 0:
- * per warp w, trace[w * cap * 4] = number of records n, followed by n records
- * of 4 uint32 {node, iteration, trip, clock} (device buffer of
- * num_warps * cap * 4 uint32, zeroed by the caller). */
+ * per warp w, trace[w * cap * 8] = number of records n, followed by n records
+ * of 8 uint32 {node, iteration, trip, t_issue, t_ready, t_done, 0, 0}
+ * (clock64 low words; device buffer of num_warps * cap * 8 uint32, zeroed by
+ * the caller). */
 int twfa_fa_fwd_traced(const twfa_plan* plan, const void* q, const void* k, const void* v, void* o,
                        float* lse, int B, int H, int S, int D, int causal, float softmax_scale,
                        uint32_t* trace, uint32_t cap, void* stream);

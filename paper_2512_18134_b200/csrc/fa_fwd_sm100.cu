@@ -57,19 +57,26 @@ struct FaShared {
   FaBarriers bar;
 };
 
-__device__ __forceinline__ void trace_op(const FaArgs& a, uint32_t warp, int node, int it, int trip) {
-  if (a.trace != nullptr && blockIdx.x == 0 && lane_id() == 0) {
-    uint32_t* slot = a.trace + warp * a.trace_cap * 4;
-    uint32_t n = slot[0];  // entry 0 holds the count
-    if (n + 1 < a.trace_cap) {
-      uint32_t* e = slot + (n + 1) * 4;
-      e[0] = static_cast<uint32_t>(node);
-      e[1] = static_cast<uint32_t>(it);
-      e[2] = static_cast<uint32_t>(trip);
-      e[3] = static_cast<uint32_t>(clock64());
-      slot[0] = n + 1;
-    }
-  }
+// Issue trace of CTA 0 (debug / schedule-realization evidence). Per warp:
+// word 0 = record count, then records of kTraceWords uint32:
+// {node, iteration, trip, t_issue, t_ready (inputs waited), t_done}.
+constexpr int kTraceWords = 8;
+
+__device__ __forceinline__ uint32_t* trace_begin(const FaArgs& a, uint32_t warp, int node, int it, int trip) {
+  if (a.trace == nullptr || blockIdx.x != 0 || lane_id() != 0) return nullptr;
+  uint32_t* base = a.trace + static_cast<size_t>(warp) * a.trace_cap * kTraceWords;
+  const uint32_t n = base[0];
+  if (n + 1 >= a.trace_cap) return nullptr;
+  uint32_t* e = base + (n + 1) * kTraceWords;
+  e[0] = static_cast<uint32_t>(node);
+  e[1] = static_cast<uint32_t>(it);
+  e[2] = static_cast<uint32_t>(trip);
+  e[3] = static_cast<uint32_t>(clock64());
+  base[0] = n + 1;
+  return e;
+}
+__device__ __forceinline__ void trace_mark(uint32_t* e, int field) {
+  if (e != nullptr) e[field] = static_cast<uint32_t>(clock64());
 }
 
 }  // namespace
@@ -180,7 +187,7 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
         if (it < 0 || it >= N) continue;
         const uint32_t g = gbase + static_cast<uint32_t>(it);
         const int k = op.tile;
-        trace_op(args, warp, op.node, it, r);
+        uint32_t* tr = trace_begin(args, warp, op.node, it, r);
         switch (op.kind) {
           case TWFA_OP_LDK:
           case TWFA_OP_LDV: {
@@ -193,6 +200,7 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
               uint8_t* dst = (is_k ? k_smem : v_smem) + s * kTileBytes;
               const CUtensorMap* map = is_k ? &tm_k : &tm_v;
               mbar_wait(empty, ph ^ 1);
+              trace_mark(tr, 4);
               mbar_arrive_expect_tx(full, kTileBytes);
               tma_load_3d(dst, map, full, 0, it * kBlockK, bh, pol_kv);
               tma_load_3d(dst + kHalfBytes, map, full, 64, it * kBlockK, bh, pol_kv);
@@ -205,6 +213,7 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
               mbar_wait(&bar.k_full[s], (g / kd) & 1);
               if (it == 0) mbar_wait(&bar.q_full[k], tcount & 1);
               if (g > 0) mbar_wait(&bar.o_done[k], (g - 1) & 1);  // P_k(g-1) consumed
+              trace_mark(tr, 4);
               tc_fence_after();
               const uint32_t qa = smem_u32(q_smem + k * kTileBytes);
               const uint32_t ka = smem_u32(k_smem + s * kTileBytes);
@@ -223,6 +232,7 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
           }
           case TWFA_OP_MX: {
             mbar_wait(&bar.s_full[k], g & 1);
+            trace_mark(tr, 4);
             tc_fence_after();
             const int row = q0 + k * kBlockQ + quad * 32 + lane;
             const int key0 = it * kBlockK;
@@ -262,6 +272,7 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
             const int row_lo = q0 + k * kBlockQ + quad * 32;
             const bool mask = (args.causal && key0 + kBlockK - 1 > row_lo) || key0 + kBlockK > S;
             const float m_safe = m_run[k] == -INFINITY ? 0.f : m_run[k];
+            trace_mark(tr, 4);
             float sum = 0.f;
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
@@ -302,6 +313,7 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
             mbar_arrive(&bar.st_empty[k][sb]);
             if (it > 0) {
               mbar_wait(&bar.o_done[k], (g - 1) & 1);
+              trace_mark(tr, 4);
               tc_fence_after();
               if (!__all_sync(0xffffffffu, alpha == 1.f)) {
 #pragma unroll 1
@@ -327,6 +339,7 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
               mbar_wait(&bar.v_full[s], (g / vd) & 1);
               mbar_wait(&bar.p_full[k], g & 1);
               mbar_wait(&bar.o_ready[k], g & 1);
+              trace_mark(tr, 4);
               tc_fence_after();
               const uint32_t va = smem_u32(v_smem + s * kTileBytes);
 #pragma unroll
@@ -344,6 +357,7 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
           default:
             break;
         }
+        trace_mark(tr, 5);
       }
     }
 

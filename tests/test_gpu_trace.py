@@ -35,16 +35,17 @@ def _ref():
 def realized_schedule(twfa, plan, B=1, H=1, S=2048, causal=False, cap=512):
     desc = plan.describe()
     nw = desc["num_warps"]
-    trace = torch.zeros(nw * cap * 4, dtype=torch.int32, device="cuda")
+    trace = torch.zeros(nw * cap * 8, dtype=torch.int32, device="cuda")
     dev = torch.device("cuda:0")
     q, k, v = (torch.randn(B, H, S, 128, device=dev).to(torch.bfloat16) for _ in range(3))
     twfa.fa_fwd(plan, q, k, v, causal=causal, trace=trace, trace_cap=cap)
     torch.cuda.synchronize()
-    t = trace.cpu().numpy().view(np.uint32).reshape(nw, cap, 4)
+    t = trace.cpu().numpy().view(np.uint32).reshape(nw, cap, 8)
     per_warp = {}
     for w in range(nw):
         n = int(t[w, 0, 0])
-        per_warp[w] = [tuple(int(x) for x in t[w, 1 + i]) for i in range(n)]
+        # (node, iteration, trip, t_issue, t_ready, t_done)
+        per_warp[w] = [tuple(int(x) for x in t[w, 1 + i, :6]) for i in range(n)]
     return desc, per_warp
 
 
@@ -60,7 +61,7 @@ def test_realized_schedule_is_the_solution(twfa):
     realized_warps = {v: set() for v in ids}
     realized_stage = {v: set() for v in ids}
     for w, recs in per_warp.items():
-        for node, it, trip, _clk in recs:
+        for node, it, trip, *_clk in recs:
             realized_warps[ids[node]].add(w)
             realized_stage[ids[node]].add(trip - it)
     for v in ids:
