@@ -1,0 +1,367 @@
+#!/usr/bin/env python3
+"""Benchmark of the Twill-scheduled FA-forward executor on B200.
+
+Metric (BASELINE.json): FA-fwd TFLOPS (bf16, d=128) & tensor-pipe utilisation
+at 1/2/4/8 B200. One step = one FA-forward pass (one kernel launch) over the
+rank's shard of synthetic bf16 Q/K/V resident in HBM.
+
+Workload (default, BASELINE config 3): non-causal, d = 128, B = 4, H = 32,
+S = 8192 per GPU. With --gpus N (torchrun, one process per GPU) every rank
+owns the batch slice [4r, 4r + 4) of a B = 4N job (B x H sharding, no
+collective on the data path): weak scaling. FLOPs per step = 4 B H S^2 d
+(two GEMMs; causal counts the unmasked triangle, 2 B H S^2 d).
+Inputs (768 MiB per rank) exceed the 126 MB L2, so no flush is needed
+between steps.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c3|c4|c5] [--seq S]
+
+--impl reference times the reference's CPU path on the host cores of this
+box: the unmodified weftsched solver (oracle/_ref) on the committed FA problem
+plus the fp32 host attention restatement (oracle/) on a bounded sample of the
+same workload.
+"""
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FA-fwd TFLOPS/GPU (bf16, d=128) & tensor-pipe util at 1/2/4/8 B200"
+UNIT = "TFLOPS"
+CONFIGS = {
+    # name: (B per GPU, H, S, causal, description)
+    "c3": (4, 32, 8192, False, "BASELINE config 3: FA fwd bf16 non-causal d=128 B=4 H=32 S=8192 per GPU"),
+    "c4": (2, 32, 16384, True, "BASELINE config 4: FA fwd bf16 causal d=128 B=2 H=32 S=16384 per GPU"),
+    "c5": (16, 64, 8192, False, "BASELINE config 5 point: FA fwd bf16 non-causal d=128 B=16 H=64 per GPU"),
+}
+
+
+def fa_flops(B, H, S, D, causal):
+    f = 4.0 * B * H * S * S * D
+    return f / 2 if causal else f
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return j.get("bf16_tflops", 1590.0), j.get("hbm_gbs", 6650.0), "measured"
+    return 1590.0, 6650.0, "fallback"
+
+
+class ClockSampler:
+    """Samples SM clocks and throttle reasons through NVML during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            names = {
+                "hw_slowdown": getattr(pynvml, "nvmlClocksThrottleReasonHwSlowdown", 0x8),
+                "sw_thermal_slowdown": getattr(pynvml, "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20),
+                "hw_thermal_slowdown": getattr(pynvml, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40),
+                "sw_power_cap": getattr(pynvml, "nvmlClocksThrottleReasonSwPowerCap", 0x4),
+                "hw_power_brake": getattr(pynvml, "nvmlClocksThrottleReasonHwPowerBrakeSlowdown", 0x80),
+            }
+
+            def run():
+                while not self._stop.is_set():
+                    try:
+                        self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                        r = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                        for n, bit in names.items():
+                            if r & bit:
+                                self.reasons.add(n)
+                    except Exception:
+                        pass
+                    time.sleep(0.005)
+
+            self._t = threading.Thread(target=run, daemon=True)
+            self._t.start()
+        except Exception as e:  # NVML unavailable: record why
+            self.reasons.add(f"nvml_unavailable:{type(e).__name__}")
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        s = sorted(self.samples)
+        med = s[len(s) // 2] if s else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(s)}
+
+
+def dist_setup(gpus):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def load_traffic(workload):
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        j = json.load(f)
+    e = j.get(workload)
+    return e.get("dram_bytes_per_launch") if e else None
+
+
+def cpu_attention_sample(target_s=10.0, threads=0):
+    """fp32 host attention (oracle restatement) on a bounded sample of the
+    workload: the first `rows` query rows of H heads against S = 8192 keys.
+    Returns (tflops, seconds, sample description, threads)."""
+    import numpy as np
+    from tests import oracle_lib
+    S, D = 8192, 128
+    threads = threads or os.cpu_count()
+    rng = np.random.default_rng(7)
+
+    def run(H, rows):
+        q = oracle_lib.round_bf16(rng.standard_normal((1, H, rows, D), dtype=np.float32))
+        k = oracle_lib.round_bf16(rng.standard_normal((1, H, S, D), dtype=np.float32))
+        v = oracle_lib.round_bf16(rng.standard_normal((1, H, S, D), dtype=np.float32))
+        t0 = time.perf_counter()
+        oracle_lib.attention(q, k, v, online=True, tile=128, threads=threads)
+        return time.perf_counter() - t0
+
+    probe = run(1, 64)
+    flops_probe = 4.0 * 64 * S * D
+    rate = flops_probe / max(probe, 1e-6)
+    rows = 256
+    H = max(1, min(64, int(round(target_s * rate / (4.0 * rows * S * D)))))
+    secs = run(H, rows)
+    flops = 4.0 * H * rows * S * D
+    return flops / secs / 1e12, secs, f"fp32 online-softmax host attention, H={H} heads x {rows} query rows x S={S} keys, d={D}", threads
+
+
+def solver_time():
+    """The reference's own CPU path: weftsched joint_search on the committed
+    FA-forward problem with the pinned backend (z3 -in), via oracle/_ref."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle", "_ref"))
+    try:
+        import _weftsched
+    except ImportError as e:
+        return {"unavailable": f"oracle/_ref not built: {e}"}
+    import paper_2512_18134_b200 as twfa
+    prob, _ = twfa.load_schedule("fa_fwd")
+    meta = json.load(open(os.path.join(twfa.schedule_dir(), "fa_fwd.meta.json")))
+    backend = meta["backend"]
+    z3 = os.path.join(os.path.dirname(sys.executable), "z3")
+    cmd = backend if backend == "internal" else backend.replace("z3", z3 if os.path.exists(z3) else "z3", 1)
+    t0 = time.perf_counter()
+    r = _weftsched.joint(prob, 0, meta["stream_depth"], "" if backend == "internal" else cmd)
+    secs = time.perf_counter() - t0
+    sol = json.loads(twfa.load_schedule("fa_fwd")[1])
+    same = r.get("status") == "sat" and r["M"] == sol["M"] and r["A"] == sol["A"] and r["I"] == sol["I"]
+    return {"seconds": round(secs, 3), "backend": backend, "cores": 1, "I": r.get("I"),
+            "matches_committed_schedule": bool(same)}
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    B, H, S, causal, desc = CONFIGS[args.config]
+    S = args.seq or S
+    import numpy as np
+    from tests import oracle_lib
+    threads = os.cpu_count()
+    rows, Hs, Sk, D = 128, 1, S, 128
+    rng = np.random.default_rng(11)
+    q = oracle_lib.round_bf16(rng.standard_normal((1, Hs, rows, D), dtype=np.float32))
+    k = oracle_lib.round_bf16(rng.standard_normal((1, Hs, Sk, D), dtype=np.float32))
+    v = oracle_lib.round_bf16(rng.standard_normal((1, Hs, Sk, D), dtype=np.float32))
+    flops = 4.0 * Hs * rows * Sk * D / (2 if causal else 1)
+    for _ in range(args.warmup):
+        oracle_lib.attention(q, k, v, causal=causal, online=True, threads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle_lib.attention(q, k, v, causal=causal, online=True, threads=threads)
+    secs = time.perf_counter() - t0
+    tflops = flops * args.steps / secs / 1e12
+    solver = solver_time()
+    sample = (f"per step: fp32 online-softmax host attention (oracle restatement; the reference has no "
+              f"attention numerics) for {rows} query rows x {Sk} keys x d={D} of one (b,h) pair")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": tflops, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic N(0,1) rounded to bf16",
+        "config": {"workload": desc, "B": B, "H": H, "S": S, "d": 128, "causal": causal},
+        "cpu_baseline": {"value": tflops, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "solver": solver,
+        "e2e": {"value": tflops, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, world, rank, local):
+    import torch
+    import paper_2512_18134_b200 as twfa
+    from __graft_entry__ import build_lib
+    build_lib()
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    B, H, S, causal, desc = CONFIGS[args.config]
+    S = args.seq or S
+    D = 128
+    plan = twfa.Plan(*twfa.load_schedule("fa_fwd"))
+    g = torch.Generator(device=dev).manual_seed(2026 + rank)
+    q, k, v = (torch.randn(B, H, S, D, device=dev, generator=g).to(torch.bfloat16) for _ in range(3))
+    o = torch.empty_like(q)
+    flops = fa_flops(B, H, S, D, causal)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        twfa.fa_fwd(plan, q, k, v, causal=causal, out=o)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        barrier(world)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    ms_local = e0.elapsed_time(e1)
+    ms = max_over_ranks(ms_local, world)
+    ms_per_step = ms / args.steps
+    total_flops = flops * world * args.steps
+    value = total_flops / (ms * 1e-3) / 1e12
+    per_launch_ms = ms_local / args.steps
+    achieved = flops / (per_launch_ms * 1e-3) / 1e12
+
+    # end to end through the public API with host buffers: pinned H2D of
+    # Q, K, V, the kernel, D2H of O, every step
+    hq, hk, hv = (x.cpu().pin_memory() for x in (q, k, v))
+    ho = torch.empty_like(hq).pin_memory()
+    dq, dk, dv = (torch.empty_like(q) for _ in range(3))
+
+    def e2e_step():
+        dq.copy_(hq, non_blocking=True)
+        dk.copy_(hk, non_blocking=True)
+        dv.copy_(hv, non_blocking=True)
+        twfa.fa_fwd(plan, dq, dk, dv, causal=causal, out=o)
+        ho.copy_(o, non_blocking=True)
+
+    e2e_steps = max(1, min(args.steps, 10))
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    barrier(world)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1), world)
+    e2e_value = flops * world * e2e_steps / (e2e_ms * 1e-3) / 1e12
+    h2d = 3 * q.numel() * q.element_size()
+    d2h = o.numel() * o.element_size()
+
+    if rank != 0:
+        return
+    peak, _, peak_kind = measured_peaks()
+    workload = f"fa_fwd_{args.config}" + (f"_S{S}" if args.seq else "")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic N(0,1) bf16 Q/K/V generated on device (seed 2026 + rank)",
+        "config": {"workload": desc, "B_per_gpu": B, "B_total": B * world, "H": H, "S": S, "d": D,
+                   "causal": causal, "parallelism": f"bh-shard x{world}, no collective",
+                   "schedule": "fa_fwd.solution.json (z3 -in, I=9)",
+                   "l2": "inputs 3x%d MiB per rank > 126 MB L2; no flush" % (q.numel() * 2 >> 20)},
+        "per_gpu_tflops": value / world,
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": load_traffic(workload),
+                     "peak_kind": f"{peak_kind} bf16 burst (MEASURED_PEAKS.json)",
+                     "kernel": "twfa::fa_fwd_kernel", "flops_per_launch": flops,
+                     "launch_ms": per_launch_ms},
+        "clocks": clocks.summary(),
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "steps": e2e_steps, "path": "pinned host -> device copies + twfa fa_fwd + device -> host O"},
+        "gpu_launches": args.steps,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        tfl, secs, sample, threads = cpu_attention_sample()
+        line["cpu_baseline"] = {"value": tfl, "unit": UNIT, "cores": threads, "kind": "port",
+                                "sample": sample, "seconds": round(secs, 2),
+                                "solver": solver_time()}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--seq", type=int, default=0, help="override S (C5 sweep points)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        rank = int(os.environ.get("RANK", "0"))
+        run_reference(args, world, rank)
+        return
+    world, rank, local = dist_setup(args.gpus)
+    run_ours(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

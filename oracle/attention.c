@@ -28,22 +28,23 @@ static void set_threads(int threads) {
 }
 
 void oracle_attention(const float* q, const float* k, const float* v, float* o,
-                      float* lse, int B, int H, int S, int D, int causal,
-                      float scale, int threads) {
+                      float* lse, int B, int H, int Sq, int Sk, int D,
+                      int causal, float scale, int threads) {
   set_threads(threads);
-  const int64_t rows = (int64_t)B * H * S;
+  const int S = Sk;
+  const int64_t rows = (int64_t)B * H * Sq;
 #pragma omp parallel
   {
     double* p = (double*)malloc(sizeof(double) * (size_t)S);
     double* acc = (double*)malloc(sizeof(double) * (size_t)D);
 #pragma omp for schedule(dynamic, 16)
     for (int64_t r = 0; r < rows; ++r) {
-      const int64_t bh = r / S;
-      const int i = (int)(r % S);
+      const int64_t bh = r / Sq;
+      const int i = (int)(r % Sq);
       const float* qi = q + r * D;
       const float* kb = k + bh * (int64_t)S * D;
       const float* vb = v + bh * (int64_t)S * D;
-      const int nkeys = causal ? i + 1 : S;
+      const int nkeys = causal ? (i + 1 < S ? i + 1 : S) : S;
       double m = -INFINITY;
       for (int j = 0; j < nkeys; ++j) {
         const float* kj = kb + (int64_t)j * D;
@@ -74,23 +75,25 @@ void oracle_attention(const float* q, const float* k, const float* v, float* o,
 }
 
 void oracle_attention_online(const float* q, const float* k, const float* v,
-                             float* o, float* lse, int B, int H, int S, int D,
-                             int causal, float scale, int tile, int threads) {
+                             float* o, float* lse, int B, int H, int Sq, int Sk,
+                             int D, int causal, float scale, int tile,
+                             int threads) {
   set_threads(threads);
   if (tile <= 0) tile = 128;
-  const int64_t rows = (int64_t)B * H * S;
+  const int S = Sk;
+  const int64_t rows = (int64_t)B * H * Sq;
 #pragma omp parallel
   {
     float* s = (float*)malloc(sizeof(float) * (size_t)tile);
     float* acc = (float*)malloc(sizeof(float) * (size_t)D);
 #pragma omp for schedule(dynamic, 16)
     for (int64_t r = 0; r < rows; ++r) {
-      const int64_t bh = r / S;
-      const int i = (int)(r % S);
+      const int64_t bh = r / Sq;
+      const int i = (int)(r % Sq);
       const float* qi = q + r * D;
       const float* kb = k + bh * (int64_t)S * D;
       const float* vb = v + bh * (int64_t)S * D;
-      const int nkeys = causal ? i + 1 : S;
+      const int nkeys = causal ? (i + 1 < S ? i + 1 : S) : S;
       float m = -INFINITY, l = 0.0f;
       for (int c = 0; c < D; ++c) acc[c] = 0.0f;
       for (int j0 = 0; j0 < nkeys; j0 += tile) {

@@ -23,19 +23,21 @@ extern "C" {
 #endif
 
 /* Plain two-pass softmax attention, fp32 inputs, double accumulation.
- * q,k,v,o: [B,H,S,D] contiguous; lse: [B,H,S] natural-log sum-exp of the
- * scaled scores (may be NULL). causal: key j visible to query i iff j <= i. */
+ * q,o: [B,H,Sq,D], k,v: [B,H,Sk,D] contiguous (the queries are the first Sq
+ * rows of the sequence); lse: [B,H,Sq] natural-log sum-exp of the scaled
+ * scores (may be NULL). causal: key j visible to query i iff j <= i. */
 void oracle_attention(const float* q, const float* k, const float* v, float* o,
-                      float* lse, int B, int H, int S, int D, int causal,
-                      float scale, int threads);
+                      float* lse, int B, int H, int Sq, int Sk, int D,
+                      int causal, float scale, int threads);
 
 /* Online-softmax restatement in the loop order of the Twill FA body:
  * per KV tile of `tile` keys: S = Q K^T (fp32), running max m, P = exp(S - m),
  * O = O * exp(m_old - m) + P V, l likewise; O /= l at the end. fp32 throughout.
  * Same layouts as oracle_attention. */
 void oracle_attention_online(const float* q, const float* k, const float* v,
-                             float* o, float* lse, int B, int H, int S, int D,
-                             int causal, float scale, int tile, int threads);
+                             float* o, float* lse, int B, int H, int Sq, int Sk,
+                             int D, int causal, float scale, int tile,
+                             int threads);
 
 /* C[M,N] = A[M,K] * B[N,K]^T (both operands K-contiguous), fp32 with double
  * accumulation. */

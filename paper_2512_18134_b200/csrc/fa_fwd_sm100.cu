@@ -62,21 +62,92 @@ struct FaShared {
 // {node, iteration, trip, t_issue, t_ready (inputs waited), t_done}.
 constexpr int kTraceWords = 8;
 
-__device__ __forceinline__ uint32_t* trace_begin(const FaArgs& a, uint32_t warp, int node, int it, int trip) {
+__device__ __forceinline__ uint32_t* trace_begin(const FaArgs& a, uint32_t warp, uint32_t& n, int node, int it,
+                                                 int trip) {
   if (a.trace == nullptr || blockIdx.x != 0 || lane_id() != 0) return nullptr;
   uint32_t* base = a.trace + static_cast<size_t>(warp) * a.trace_cap * kTraceWords;
-  const uint32_t n = base[0];
   if (n + 1 >= a.trace_cap) return nullptr;
   uint32_t* e = base + (n + 1) * kTraceWords;
   e[0] = static_cast<uint32_t>(node);
   e[1] = static_cast<uint32_t>(it);
   e[2] = static_cast<uint32_t>(trip);
   e[3] = static_cast<uint32_t>(clock64());
-  base[0] = n + 1;
+  base[0] = ++n;  // count kept in a register; the store is fire-and-forget
   return e;
 }
 __device__ __forceinline__ void trace_mark(uint32_t* e, int field) {
   if (e != nullptr) e[field] = static_cast<uint32_t>(clock64());
+}
+
+// Number of leading keys of this K/V tile that row `row` may attend to
+// (the rest are past the sequence end or above the causal diagonal).
+__device__ __forceinline__ int valid_keys(const FaArgs& a, int row, int key0) {
+  const int end = a.causal ? min(a.S, row + 1) : a.S;
+  return max(0, min(kBlockK, end - key0));
+}
+
+template <bool kMask>
+__device__ __forceinline__ void max_chunk(const uint32_t (&v)[32], int col0, int limit, float (&acc)[4]) {
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    float x = __uint_as_float(v[i]);
+    if (kMask) x = (col0 + i < limit) ? x : -INFINITY;
+    acc[i & 3] = fmaxf(acc[i & 3], x);
+  }
+}
+
+// MX: row max of the 128 scores of this thread's TMEM lane (raw, unscaled).
+template <bool kMask>
+__device__ __forceinline__ float tile_row_max(uint32_t taddr, int limit) {
+  float acc[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+  for (int c = 0; c < 4; c += 2) {
+    uint32_t a[32], b[32];
+    tmem_ld32(taddr + c * 32, a);
+    tmem_ld32(taddr + (c + 1) * 32, b);
+    tmem_ld_wait();
+    max_chunk<kMask>(a, c * 32, limit, acc);
+    max_chunk<kMask>(b, (c + 1) * 32, limit, acc);
+  }
+  return fmaxf(fmaxf(acc[0], acc[1]), fmaxf(acc[2], acc[3]));
+}
+
+template <bool kMask>
+__device__ __forceinline__ void exp_chunk(const uint32_t (&v)[32], int col0, int limit, float sl, float neg_m,
+                                          float (&acc)[4], uint32_t (&pk)[16]) {
+#pragma unroll
+  for (int i = 0; i < 32; i += 2) {
+    float p0 = fast_exp2(fmaf(__uint_as_float(v[i]), sl, neg_m));
+    float p1 = fast_exp2(fmaf(__uint_as_float(v[i + 1]), sl, neg_m));
+    if (kMask) {
+      p0 = (col0 + i < limit) ? p0 : 0.f;
+      p1 = (col0 + i + 1 < limit) ? p1 : 0.f;
+    }
+    acc[(i >> 1) & 3] += p0 + p1;
+    pk[i >> 1] = pack_bf16(p0, p1);
+  }
+}
+
+// EX: P = exp2(S * scale*log2e - m) written as bf16 pairs over the first 64
+// columns of the S tile (the TS-MMA A operand); returns the row sum of P.
+template <bool kMask>
+__device__ __forceinline__ float tile_exp_to_p(uint32_t taddr, int limit, float sl, float m) {
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  const float neg_m = -m;
+#pragma unroll
+  for (int c = 0; c < 4; c += 2) {
+    uint32_t a[32], b[32];
+    tmem_ld32(taddr + c * 32, a);
+    tmem_ld32(taddr + (c + 1) * 32, b);
+    tmem_ld_wait();
+    uint32_t pa[16], pb[16];
+    exp_chunk<kMask>(a, c * 32, limit, sl, neg_m, acc, pa);
+    exp_chunk<kMask>(b, (c + 1) * 32, limit, sl, neg_m, acc, pb);
+    tmem_st16(taddr + c * 16, pa);
+    tmem_st16(taddr + (c + 1) * 16, pb);
+  }
+  tmem_st_wait();
+  return (acc[0] + acc[1]) + (acc[2] + acc[3]);
 }
 
 }  // namespace
@@ -151,6 +222,7 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
 
   const int plen = plan.prog_len[warp];
   uint32_t gbase = 0;  // global K/V iteration index of this work tile's iteration 0
+  uint32_t trace_n = 0;
   uint32_t tcount = 0;
   for (int work = blockIdx.x; work < num_work; work += gridDim.x, ++tcount) {
     int qb, bh;
@@ -187,7 +259,7 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
         if (it < 0 || it >= N) continue;
         const uint32_t g = gbase + static_cast<uint32_t>(it);
         const int k = op.tile;
-        uint32_t* tr = trace_begin(args, warp, op.node, it, r);
+        uint32_t* tr = trace_begin(args, warp, trace_n, op.node, it, r);
         switch (op.kind) {
           case TWFA_OP_LDK:
           case TWFA_OP_LDV: {
@@ -234,26 +306,10 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
             mbar_wait(&bar.s_full[k], g & 1);
             trace_mark(tr, 4);
             tc_fence_after();
-            const int row = q0 + k * kBlockQ + quad * 32 + lane;
-            const int key0 = it * kBlockK;
-            const int row_lo = q0 + k * kBlockQ + quad * 32;
-            const bool mask = (args.causal && key0 + kBlockK - 1 > row_lo) || key0 + kBlockK > S;
-            float mx = -INFINITY;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              uint32_t v[32];
-              tmem_ld32(tmem + lane_off + k * 128 + c * 32, v);
-              tmem_ld_wait();
-#pragma unroll
-              for (int i = 0; i < 32; ++i) {
-                float x = __uint_as_float(v[i]);
-                if (mask) {
-                  const int key = key0 + c * 32 + i;
-                  if (key >= S || (args.causal && key > row)) x = -INFINITY;
-                }
-                mx = fmaxf(mx, x);
-              }
-            }
+            const uint32_t taddr = tmem + lane_off + k * 128;
+            const int limit = valid_keys(args, q0 + k * kBlockQ + quad * 32 + lane, it * kBlockK);
+            const bool mask = !__all_sync(0xffffffffu, limit >= kBlockK);
+            const float mx = mask ? tile_row_max<true>(taddr, limit) : tile_row_max<false>(taddr, limit);
             const float m_old = m_run[k];
             const float m_new = fmaxf(m_old, mx * scale_log2);
             const float m_safe = m_new == -INFINITY ? 0.f : m_new;
@@ -267,34 +323,13 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
             break;
           }
           case TWFA_OP_EX: {
-            const int row = q0 + k * kBlockQ + quad * 32 + lane;
-            const int key0 = it * kBlockK;
-            const int row_lo = q0 + k * kBlockQ + quad * 32;
-            const bool mask = (args.causal && key0 + kBlockK - 1 > row_lo) || key0 + kBlockK > S;
+            const uint32_t taddr = tmem + lane_off + k * 128;
+            const int limit = valid_keys(args, q0 + k * kBlockQ + quad * 32 + lane, it * kBlockK);
+            const bool mask = !__all_sync(0xffffffffu, limit >= kBlockK);
             const float m_safe = m_run[k] == -INFINITY ? 0.f : m_run[k];
             trace_mark(tr, 4);
-            float sum = 0.f;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              uint32_t v[32];
-              tmem_ld32(tmem + lane_off + k * 128 + c * 32, v);
-              tmem_ld_wait();
-              uint32_t pk[16];
-#pragma unroll
-              for (int i = 0; i < 32; i += 2) {
-                float p0 = fast_exp2(fmaf(__uint_as_float(v[i]), scale_log2, -m_safe));
-                float p1 = fast_exp2(fmaf(__uint_as_float(v[i + 1]), scale_log2, -m_safe));
-                if (mask) {
-                  const int key = key0 + c * 32 + i;
-                  if (key >= S || (args.causal && key > row)) p0 = 0.f;
-                  if (key + 1 >= S || (args.causal && key + 1 > row)) p1 = 0.f;
-                }
-                sum += p0 + p1;
-                pk[i >> 1] = pack_bf16(p0, p1);
-              }
-              tmem_st16(tmem + lane_off + k * 128 + c * 16, pk);
-            }
-            tmem_st_wait();
+            const float sum = mask ? tile_exp_to_p<true>(taddr, limit, scale_log2, m_safe)
+                                   : tile_exp_to_p<false>(taddr, limit, scale_log2, m_safe);
             l_run[k] = l_run[k] * alpha_cur[k] + sum;
             tc_fence_before();
             mbar_arrive(&bar.p_full[k]);

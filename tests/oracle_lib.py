@@ -27,8 +27,8 @@ def load():
         build()
         L = ctypes.CDLL(LIB)
         vp, i32, f32 = ctypes.c_void_p, ctypes.c_int, ctypes.c_float
-        L.oracle_attention.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, i32, i32, f32, i32]
-        L.oracle_attention_online.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, i32, i32, f32, i32, i32]
+        L.oracle_attention.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, i32, i32, i32, f32, i32]
+        L.oracle_attention_online.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, i32, i32, i32, f32, i32, i32]
         L.oracle_gemm_tn.argtypes = [vp, vp, vp, i32, i32, i32, i32]
         L.oracle_round_bf16.argtypes = [vp, ctypes.c_int64]
         _lib = L
@@ -40,17 +40,20 @@ def _p(a):
 
 
 def attention(q, k, v, causal=False, scale=None, online=False, tile=128, threads=0):
-    """q, k, v: float32 [B, H, S, D]. Returns (o, lse)."""
+    """q: float32 [B, H, Sq, D]; k, v: [B, H, Sk, D] (queries = the first Sq
+    positions). Returns (o, lse)."""
     L = load()
     q, k, v = (np.ascontiguousarray(x, dtype=np.float32) for x in (q, k, v))
-    B, H, S, D = q.shape
+    B, H, Sq, D = q.shape
+    Sk = k.shape[2]
     scale = float(scale if scale is not None else 1.0 / np.sqrt(D))
     o = np.empty_like(q)
-    lse = np.empty((B, H, S), dtype=np.float32)
+    lse = np.empty((B, H, Sq), dtype=np.float32)
     if online:
-        L.oracle_attention_online(_p(q), _p(k), _p(v), _p(o), _p(lse), B, H, S, D, int(causal), scale, tile, threads)
+        L.oracle_attention_online(_p(q), _p(k), _p(v), _p(o), _p(lse), B, H, Sq, Sk, D, int(causal), scale, tile,
+                                  threads)
     else:
-        L.oracle_attention(_p(q), _p(k), _p(v), _p(o), _p(lse), B, H, S, D, int(causal), scale, threads)
+        L.oracle_attention(_p(q), _p(k), _p(v), _p(o), _p(lse), B, H, Sq, Sk, D, int(causal), scale, threads)
     return o, lse
 
 

@@ -93,10 +93,10 @@ def test_full_size_against_cudnn_sdpa(twfa, plan):
     d = (o.float() - ref.float()).abs()
     assert d.max().item() <= 2.5e-2 and d.mean().item() <= 2e-3
     for b, h in [(0, 0), (3, 31)]:
+        # first 512 query rows of the pair against all 8192 keys
         ro, rl = oracle_lib.attention(q[b:b + 1, h:h + 1, :512].float().cpu().numpy(),
                                       k[b:b + 1, h:h + 1].float().cpu().numpy(),
                                       v[b:b + 1, h:h + 1].float().cpu().numpy())
-        # first 512 query rows of the pair, all 8192 keys
         err = np.abs(o[b, h, :512].float().cpu().numpy() - ro[0, 0])
         assert err.max() <= TOL_MAX
         assert np.abs(lse[b, h, :512].cpu().numpy() - rl[0, 0]).max() <= TOL_LSE
