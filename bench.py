@@ -172,7 +172,7 @@ def cpu_attention_sample(target_s=10.0, threads=0):
     flops_probe = 4.0 * 64 * S * D
     rate = flops_probe / max(probe, 1e-6)
     rows = 256
-    H = max(1, min(64, int(round(target_s * rate / (4.0 * rows * S * D)))))
+    H = max(1, min(1024, int(round(target_s * rate / (4.0 * rows * S * D)))))
     secs = run(H, rows)
     flops = 4.0 * H * rows * S * D
     return flops / secs / 1e12, secs, f"fp32 online-softmax host attention, H={H} heads x {rows} query rows x S={S} keys, d={D}", threads

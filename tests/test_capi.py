@@ -1,0 +1,56 @@
+"""The C-ABI library (libtwfa.so) loads and exports every function declared in
+include/twfa.h; argument / document errors come back as the reference's exit
+codes (1 domain, 2 usage) with a message, without a GPU."""
+import ctypes
+import os
+import re
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_functions():
+    text = open(os.path.join(ROOT, "include", "twfa.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(twfa_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_every_declared_symbol_is_exported(twfa):
+    lib = ctypes.CDLL(twfa._LIB_PATH)
+    names = declared_functions()
+    assert len(names) >= 10
+    for n in names:
+        assert hasattr(lib, n), n
+
+
+def test_error_codes_and_messages(twfa):
+    L = twfa.lib()
+    h = ctypes.c_void_p()
+    assert L.twfa_plan_create(b"{}", b"{}", ctypes.byref(h)) == 1
+    assert b"machine" in L.twfa_last_error()
+    assert L.twfa_plan_create(None, b"{}", ctypes.byref(h)) == 2
+    prob, sol = twfa.load_schedule("gemm_mainloop")
+    assert L.twfa_plan_create(prob.encode(), sol.encode(), ctypes.byref(h)) == 0
+    assert L.twfa_last_error() == b""
+    # an FA launch with a GEMM plan is a usage error, detected before any CUDA call
+    rc = L.twfa_fa_fwd(h, None, None, None, None, None, 1, 1, 128, 128, 0, 1.0, None)
+    assert rc == 2 and b"not an FA-forward plan" in L.twfa_last_error()
+    rc = L.twfa_gemm(h, None, None, None, 100, 256, 64, None)
+    assert rc == 2
+    need = ctypes.c_size_t()
+    assert L.twfa_plan_raw(h, None, 0, ctypes.byref(need)) == 0 and need.value > 0
+    L.twfa_plan_destroy(h)
+    assert L.twfa_abi_version() == 1
+
+
+def test_plan_survives_threads(twfa):
+    import threading
+    prob, sol = twfa.load_schedule("fa_fwd")
+    out = []
+
+    def work():
+        out.append(twfa.Plan(prob, sol).describe()["I"])
+
+    ts = [threading.Thread(target=work) for _ in range(8)]
+    [t.start() for t in ts]
+    [t.join() for t in ts]
+    assert out == [9] * 8

@@ -1,0 +1,139 @@
+"""The lowering (solution JSON -> per-warp trip programs) against the
+reference's own consumer of the same documents.
+
+The unmodified reference (weftsched, built in place into oracle/_ref) renders
+a solution with `codegen` (synthesize, /root/reference/proj/src/codegen.cpp:
+43-189). Its steady-state region lists every op once with its warp range, its
+cycle inside the trip (M mod I) and the copy it belongs to (copy = copies - 1 -
+stage). The executor's plan must carry exactly that: same I, same warp ranges,
+same stages, and per warp the same op order as the reference's region order.
+Document-level errors must be rejected like the reference rejects them
+(solution_from_json, cli.cpp:96-155 -> ValueError in Python)."""
+import json
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def ws():
+    sys.path.insert(0, os.path.join(ROOT, "oracle", "_ref"))
+    try:
+        import _weftsched
+    except ImportError:
+        pytest.skip("oracle/_ref not built")
+    return _weftsched
+
+
+def steady_programs_from_reference(ws, prob, sol):
+    prog = json.loads(ws.codegen(prob, sol, "json"))
+    copies = prog["copies"]
+    per_warp, stage, warp = {}, {}, {}
+    for ins in prog["steady_state"]:
+        if ins["kind"] != "op":
+            continue
+        stage[ins["node"]] = copies - 1 - ins["copy"]
+        warp[ins["node"]] = (ins["warp_start"], ins["warp_count"])
+        for w in range(ins["warp_start"], ins["warp_start"] + ins["warp_count"]):
+            per_warp.setdefault(w, []).append(ins["node"])
+    return prog, per_warp, stage, warp
+
+
+@pytest.mark.parametrize("name", ["fa_fwd", "gemm_mainloop"])
+def test_plan_equals_reference_program(twfa, ws, name):
+    prob, sol = twfa.load_schedule(name)
+    d = twfa.Plan(prob, sol).describe()
+    prog, per_warp, stage, warp = steady_programs_from_reference(ws, prob, sol)
+    s = json.loads(sol)
+    assert d["I"] == prog["I"] == s["I"]
+    assert d["L"] == s["L"] and d["copies"] == prog["copies"]
+    for v, nd in d["nodes"].items():
+        assert nd["stage"] == stage[v] == s["M"][v] // s["I"]
+        assert nd["slot"] == s["M"][v] % s["I"]
+        assert (nd["warp_start"], nd["warp_count"]) == warp[v]
+        assert nd["warp_start"] == s["A"][v]
+    assert {int(w): p for w, p in d["warp_programs"].items()} == per_warp
+
+
+def test_golden_solution_is_valid_under_the_reference(twfa, ws):
+    for name in ("fa_fwd", "gemm_mainloop"):
+        prob, sol = twfa.load_schedule(name)
+        assert ws.validate(prob, sol) == []
+
+
+def test_golden_problem_normalizes_to_committed(twfa, ws):
+    """The committed normalized problem is the reference `normalize` of the raw
+    B200 cost model (exact at U = 7, F = 0)."""
+    d = twfa.schedule_dir()
+    raw = open(os.path.join(d, "fa_fwd.raw.json")).read()
+    meta = json.load(open(os.path.join(d, "fa_fwd.meta.json")))
+    r = ws.normalize(raw, meta["resolution"])
+    assert json.loads(r["problem"]) == json.loads(open(os.path.join(d, "fa_fwd.json")).read())
+    assert r["F"] == 0
+
+
+def test_gemm_stream_depth_sets_ring(twfa, ws):
+    prob, _ = twfa.load_schedule("gemm_mainloop")
+    for depth in (2, 3, 4):
+        r = ws.joint(prob, 0, depth, "")
+        d = twfa.Plan(prob, r["solution_json"]).describe()
+        assert d["rings"]["AB"] == depth
+        assert d["mma_warp"] == r["A"]["MMA"] and d["load_warp"] == r["A"]["LDA"]
+
+
+def test_fa_ring_depth_follows_solution(twfa):
+    prob, sol = twfa.load_schedule("fa_fwd")
+    s = json.loads(sol)
+    assert twfa.Plan(prob, sol).describe()["rings"] == {"K": 2, "V": 2}
+    # two 32 KiB Q tiles + 2 + 2 ring slots fill the 227 KiB of shared memory;
+    # a deeper ring than the solution's is not realizable and must say so
+    s["streaming_depths"] = {"LDK": 3, "LDV": 2}
+    with pytest.raises(ValueError, match="shared memory"):
+        twfa.Plan(prob, json.dumps(s))
+
+
+@pytest.mark.parametrize("mutate,msg", [
+    (lambda s: s.update(I=0), "positive integer I"),
+    (lambda s: s.update(bogus=1), "unknown key"),
+    (lambda s: s["M"].pop("S0"), "cover every node"),
+    (lambda s: s["M"].update(S0=99), "does not fit in L"),
+    (lambda s: s["A"].update(MX0=3), "aligned warp range"),
+    (lambda s: s["A"].update(EX0=8, MX0=4), "share a warpgroup"),
+    (lambda s: s["A"].update(S0=15), "cannot share the TMA warp"),
+    (lambda s: s.update(streaming_depths={"LDK": 1, "LDV": 1}), "shallower than its consumer lag"),
+])
+def test_bad_or_unrealizable_solutions_are_rejected(twfa, mutate, msg):
+    prob, sol = twfa.load_schedule("fa_fwd")
+    s = json.loads(sol)
+    mutate(s)
+    with pytest.raises(ValueError, match=msg):
+        twfa.Plan(prob, json.dumps(s))
+
+
+def test_reference_fixtures_without_a_b200_realization_are_rejected(twfa, ws):
+    # the reference's own Fig. 1 attention problem (S, P, O on TC/MFU,
+    # proj/tests/testutil.hpp:16-40) names ops the executor has no kernel for
+    prob = json.dumps({
+        "machine": {"units": [{"name": "TC", "capacity": 1}, {"name": "MFU", "capacity": 1}],
+                    "memories": [{"name": "smem", "capacity": 1024}], "num_warps": 4, "reg_limit": 256,
+                    "vl_warp": 3},
+        "graph": {"nodes": [{"id": "S", "rrt": {"TC": [1]}, "cycles": 1},
+                            {"id": "P", "rrt": {"MFU": [1]}, "cycles": 1},
+                            {"id": "O", "rrt": {"TC": [1]}, "cycles": 1}],
+                  "edges": [{"src": "S", "dst": "P", "d": 1}, {"src": "P", "dst": "O", "d": 1},
+                            {"src": "O", "dst": "O", "d": 1, "delta": 1}]}})
+    r = ws.joint(prob)
+    assert (r["I"], r["L"], r["M"]) == (2, 4, {"S": 0, "P": 2, "O": 3})  # reference golden
+    with pytest.raises(ValueError, match="no sm_100a realization"):
+        twfa.Plan(prob, r["solution_json"])
+
+
+def test_malformed_problem_is_rejected(twfa):
+    _, sol = twfa.load_schedule("fa_fwd")
+    with pytest.raises(ValueError):
+        twfa.Plan("{not json", sol)
+    with pytest.raises(ValueError, match="unknown key"):
+        twfa.Plan(json.dumps({"machine": {}, "graph": {}, "extra": 1}), sol)
