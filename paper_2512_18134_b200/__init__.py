@@ -32,7 +32,8 @@ __all__ = [
 ]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_PKG, "libtwfa.so")
+# TWFA_LIB selects an alternative in-tree build (kernel-variant experiments)
+_LIB_PATH = os.environ.get("TWFA_LIB") or os.path.join(_PKG, "libtwfa.so")
 _lib = None
 
 

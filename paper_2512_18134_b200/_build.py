@@ -57,34 +57,40 @@ def stale():
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force=False, verbose=False, ptxas_info=False):
-    if not force and not stale():
+def build(force=False, verbose=False, ptxas_info=False, defines=(), out=None):
+    """Compile libtwfa.so (or, with `defines`/`out`, a kernel variant for experiments)."""
+    lib = out or LIB
+    if not force and not defines and out is None and not stale():
         return LIB
-    os.makedirs(OBJ, exist_ok=True)
+    obj_dir = OBJ if not defines else os.path.join(OBJ, "v_" + "_".join(d.replace("=", "") for d in defines))
+    os.makedirs(obj_dir, exist_ok=True)
     cu, cpp = sources()
     inc = ["-I" + CSRC, "-I" + os.path.join(ROOT, "include"), "-I" + json_include()]
     objs = []
     log = ""
     for src in cu:
-        obj = os.path.join(OBJ, os.path.basename(src) + ".o")
+        obj = os.path.join(obj_dir, os.path.basename(src) + ".o")
         cmd = [NVCC, *ARCH, "-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-c", src, "-o", obj, *inc,
-               "--use_fast_math", "-Xptxas", "-v" if ptxas_info else "-O3"]
+               "--use_fast_math", "-Xptxas", "-v" if ptxas_info else "-O3", *["-D" + d for d in defines]]
         log += run(cmd, verbose)
         objs.append(obj)
     for src in cpp:
-        obj = os.path.join(OBJ, os.path.basename(src) + ".o")
+        obj = os.path.join(obj_dir, os.path.basename(src) + ".o")
         cmd = [host_cxx(), "-std=c++17", "-O2", "-fPIC", "-Wall", "-c", src, "-o", obj, *inc,
                "-I" + os.path.join(CUDA_HOME, "include")]
         log += run(cmd, verbose)
         objs.append(obj)
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"]
     log += run(cmd, verbose)
-    shutil.move(tmp, LIB)
+    shutil.move(tmp, lib)
     if ptxas_info:
         print(log)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True, ptxas_info="--ptxas" in sys.argv)
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a[6:] for a in sys.argv[1:] if a.startswith("--out=")]
+    build(force="--force" in sys.argv, verbose=True, ptxas_info="--ptxas" in sys.argv, defines=defs,
+          out=outs[0] if outs else None)

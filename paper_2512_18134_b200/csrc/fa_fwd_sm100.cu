@@ -37,6 +37,10 @@ constexpr int kHeadDim = 128;
 constexpr uint32_t kTileBytes = kBlockQ * kHeadDim * 2;  // 32 KiB, two 16 KiB SW128 column halves
 constexpr uint32_t kHalfBytes = kTileBytes / 2;
 constexpr int kMaxRing = 4;
+#ifndef TWFA_POLY_EVERY
+#define TWFA_POLY_EVERY 4
+#endif
+constexpr int kPolyEvery = TWFA_POLY_EVERY;  // 1 in kPolyEvery exp2 pairs on the FMA pipe
 constexpr uint32_t kIdescS = idesc_bf16_f32(128, kBlockK, 0);    // K-major Q, K-major K
 constexpr uint32_t kIdescPV = idesc_bf16_f32(128, kHeadDim, 1);  // TMEM P, MN-major V
 
@@ -48,6 +52,7 @@ struct __align__(8) FaBarriers {
   uint64_t o_ready[TWFA_MAX_TILES], o_done[TWFA_MAX_TILES];
   uint64_t st_full[TWFA_MAX_TILES][2], st_empty[TWFA_MAX_TILES][2];
   uint64_t l_full[TWFA_MAX_TILES], l_empty[TWFA_MAX_TILES];
+  uint64_t mufu_tok[TWFA_MAX_TILES];  // EX_k may use MUFU (schedule's unit order)
   uint32_t tmem_base;
 };
 
@@ -117,8 +122,13 @@ __device__ __forceinline__ void exp_chunk(const uint32_t (&v)[32], int col0, int
                                           float (&acc)[4], uint32_t (&pk)[16]) {
 #pragma unroll
   for (int i = 0; i < 32; i += 2) {
-    float p0 = fast_exp2(fmaf(__uint_as_float(v[i]), sl, neg_m));
-    float p1 = fast_exp2(fmaf(__uint_as_float(v[i + 1]), sl, neg_m));
+    // kPolyEvery-th pairs go to the FMA pipe, the rest to MUFU (ex2), to
+    // balance the two pipes (MUFU alone co-bounds the loop at d = 128)
+    const bool poly = (i >> 1) % kPolyEvery == 0;
+    const float x0 = fmaf(__uint_as_float(v[i]), sl, neg_m);
+    const float x1 = fmaf(__uint_as_float(v[i + 1]), sl, neg_m);
+    float p0 = poly ? poly_exp2(x0) : fast_exp2(x0);
+    float p1 = poly ? poly_exp2(x1) : fast_exp2(x1);
     if (kMask) {
       p0 = (col0 + i < limit) ? p0 : 0.f;
       p1 = (col0 + i + 1 < limit) ? p1 : 0.f;
@@ -183,6 +193,7 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
       }
       mbar_init(&bar.l_full[k], 128);
       mbar_init(&bar.l_empty[k], 128);
+      mbar_init(&bar.mufu_tok[k], 128);
     }
     for (int s = 0; s < kd; ++s) {
       mbar_init(&bar.k_full[s], 1);
@@ -250,21 +261,22 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
       m_run[k] = -INFINITY;
       l_run[k] = 0.f;
     }
+    int k_next = 0, v_next = 0;  // next K / V iteration to load (load warp)
 
     const int trips = N + plan.max_stage;
     for (int r = 0; r < trips; ++r) {
       for (int j = 0; j < plen; ++j) {
         const TwfaPlanOp op = plan.ops[plan.prog[warp][j]];
-        const int it = r - static_cast<int>(op.stage);
-        if (it < 0 || it >= N) continue;
-        const uint32_t g = gbase + static_cast<uint32_t>(it);
-        const int k = op.tile;
-        uint32_t* tr = trace_begin(args, warp, trace_n, op.node, it, r);
-        switch (op.kind) {
-          case TWFA_OP_LDK:
-          case TWFA_OP_LDV: {
+        if (op.kind == TWFA_OP_LDK || op.kind == TWFA_OP_LDV) {
+          // streamed load: top the ring up to iteration r - stage + prefetch
+          const bool is_k = op.kind == TWFA_OP_LDK;
+          const int target = min(N - 1, r - static_cast<int>(op.stage) + (is_k ? plan.k_prefetch : plan.v_prefetch));
+          int& next = is_k ? k_next : v_next;
+          while (next <= target) {
+            const int lit = next++;
+            uint32_t* tr = trace_begin(args, warp, trace_n, op.node, lit, r);
             if (lane == 0) {
-              const bool is_k = op.kind == TWFA_OP_LDK;
+              const uint32_t g = gbase + static_cast<uint32_t>(lit);
               const int depth = is_k ? kd : vd;
               const uint32_t s = g % depth, ph = (g / depth) & 1;
               uint64_t* full = is_k ? &bar.k_full[s] : &bar.v_full[s];
@@ -274,11 +286,19 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
               mbar_wait(empty, ph ^ 1);
               trace_mark(tr, 4);
               mbar_arrive_expect_tx(full, kTileBytes);
-              tma_load_3d(dst, map, full, 0, it * kBlockK, bh, pol_kv);
-              tma_load_3d(dst + kHalfBytes, map, full, 64, it * kBlockK, bh, pol_kv);
+              tma_load_3d(dst, map, full, 0, lit * kBlockK, bh, pol_kv);
+              tma_load_3d(dst + kHalfBytes, map, full, 64, lit * kBlockK, bh, pol_kv);
             }
-            break;
+            trace_mark(tr, 5);
           }
+          continue;
+        }
+        const int it = r - static_cast<int>(op.stage);
+        if (it < 0 || it >= N) continue;
+        const uint32_t g = gbase + static_cast<uint32_t>(it);
+        const int k = op.tile;
+        uint32_t* tr = trace_begin(args, warp, trace_n, op.node, it, r);
+        switch (op.kind) {
           case TWFA_OP_S: {
             if (lane == 0) {
               const uint32_t s = g % kd;
@@ -327,9 +347,16 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
             const int limit = valid_keys(args, q0 + k * kBlockQ + quad * 32 + lane, it * kBlockK);
             const bool mask = !__all_sync(0xffffffffu, limit >= kBlockK);
             const float m_safe = m_run[k] == -INFINITY ? 0.f : m_run[k];
+            int ring_pos = -1;
+#ifndef TWFA_NO_MUFU_TOKEN
+            for (int i = 0; i < plan.ex_ring_len; ++i)
+              if (plan.ex_ring[i] == k) ring_pos = i;
+#endif
+            if (ring_pos >= 0) mbar_wait(&bar.mufu_tok[k], (g & 1) ^ (ring_pos == 0 ? 1u : 0u));
             trace_mark(tr, 4);
             const float sum = mask ? tile_exp_to_p<true>(taddr, limit, scale_log2, m_safe)
                                    : tile_exp_to_p<false>(taddr, limit, scale_log2, m_safe);
+            if (ring_pos >= 0) mbar_arrive(&bar.mufu_tok[plan.ex_ring[(ring_pos + 1) % plan.ex_ring_len]]);
             l_run[k] = l_run[k] * alpha_cur[k] + sum;
             tc_fence_before();
             mbar_arrive(&bar.p_full[k]);

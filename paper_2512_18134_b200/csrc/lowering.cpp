@@ -270,15 +270,31 @@ void derive(LoweredSchedule& s) {
     return -1;
   };
   // streamed loads: ring depth must cover the stage lag to every consumer
-  auto check_ring = [&](int ld, int32_t depth) {
+  // Streamed load of depth D: iteration j is loaded in trip j + stage - p
+  // (prefetch distance p) into slot j % D, after the consumers of iteration
+  // j - D released that slot. p = D - 1 unless a consumer on the load's own
+  // warp would release the slot only later in program order.
+  auto prefetch_of = [&](int ld, int32_t depth) -> int32_t {
     if (depth < 1) throw DomainError("streamed load " + s.nodes[ld].id + " has no ring depth");
+    const TwfaPlanOp& L = p.ops[ld];
+    int64_t pf = depth - 1;
     for (const LEdge& e : s.edges) {
       if (e.src != ld) continue;
+      const TwfaPlanOp& C = p.ops[e.dst];
       const int64_t lag = s.stage[static_cast<size_t>(e.dst)] + e.delta - s.stage[static_cast<size_t>(ld)];
       if (lag >= depth)
         throw DomainError("ring depth " + std::to_string(depth) + " of " + s.nodes[ld].id +
                           " is shallower than its consumer lag");
+      const bool share = L.warp_start < C.warp_start + C.warp_count && C.warp_start < L.warp_start + L.warp_count;
+      if (!share) continue;
+      const bool before = std::make_pair(s.slot[static_cast<size_t>(e.dst)], e.dst) <
+                          std::make_pair(s.slot[static_cast<size_t>(ld)], ld);
+      pf = std::min<int64_t>(pf, depth - lag - (before ? 0 : 1));
     }
+    if (pf < 0)
+      throw DomainError("ring depth " + std::to_string(depth) + " of " + s.nodes[ld].id +
+                        " cannot cover a consumer on its own warp");
+    return static_cast<int32_t>(pf);
   };
 
   const bool is_fa = kinds.count(TWFA_OP_S) && kinds.count(TWFA_OP_PV);
@@ -298,8 +314,8 @@ void derive(LoweredSchedule& s) {
     p.k_depth = depth_of("LDA");
     p.v_depth = depth_of("LDB");
     if (p.k_depth != p.v_depth) throw DomainError("LDA and LDB must stream with one ring depth");
-    check_ring(lda, p.k_depth);
-    check_ring(ldb, p.v_depth);
+    p.k_prefetch = prefetch_of(lda, p.k_depth);
+    p.v_prefetch = prefetch_of(ldb, p.v_depth);
     if (s.ii != 1 || max_stage != 0)
       throw DomainError("GEMM mainloop realization expects the I = 1 single-stage schedule");
     return;
@@ -322,8 +338,8 @@ void derive(LoweredSchedule& s) {
   p.load_warp = p.ops[ldk].warp_start;
   p.k_depth = depth_of("LDK");
   p.v_depth = depth_of("LDV");
-  check_ring(ldk, p.k_depth);
-  check_ring(ldv, p.v_depth);
+  p.k_prefetch = prefetch_of(ldk, p.k_depth);
+  p.v_prefetch = prefetch_of(ldv, p.v_depth);
   for (int k = 0; k < tiles; ++k) {
     const TwfaPlanOp& mx = p.ops[node_id("MX" + std::to_string(k))];
     const TwfaPlanOp& ex = p.ops[node_id("EX" + std::to_string(k))];
@@ -339,10 +355,23 @@ void derive(LoweredSchedule& s) {
     if (mx.warp_start != ex.warp_start)
       throw DomainError("MX" + std::to_string(k) + " and EX" + std::to_string(k) + " must share a warpgroup");
     if (sk.warp_count != 1 || pv.warp_count != 1) throw DomainError("MMA issue ops are single-warp");
-    if (sk.warp_start == p.load_warp || pv.warp_start == p.load_warp)
-      throw DomainError("MMA issue cannot share the TMA warp");
     p.sm_warp[k] = mx.warp_start;
     p.cr_warp[k] = cr.warp_start;
+  }
+  // MUFU reservation order of the EX ops (all EX share the unit; realized as a
+  // token ring when they share a stage so every trip holds each of them once)
+  {
+    std::vector<int> ex;
+    for (int k = 0; k < tiles; ++k) ex.push_back(node_id("EX" + std::to_string(k)));
+    bool same_stage = true;
+    for (int v : ex) same_stage = same_stage && s.stage[static_cast<size_t>(v)] == s.stage[static_cast<size_t>(ex[0])];
+    if (same_stage && ex.size() >= 2) {
+      std::stable_sort(ex.begin(), ex.end(), [&](int x, int y) {
+        return std::make_pair(s.slot[static_cast<size_t>(x)], x) < std::make_pair(s.slot[static_cast<size_t>(y)], y);
+      });
+      p.ex_ring_len = static_cast<int32_t>(ex.size());
+      for (size_t i = 0; i < ex.size(); ++i) p.ex_ring[i] = p.ops[ex[i]].tile;
+    }
   }
   // smem: Q (tiles x 32 KiB) + K ring + V ring of 32 KiB slots
   const int64_t smem = 32768LL * (tiles + p.k_depth + p.v_depth);
@@ -392,6 +421,7 @@ std::string describe(const LoweredSchedule& s) {
   if (p.family == TWFA_FAMILY_FA_FWD) {
     rings["K"] = p.k_depth;
     rings["V"] = p.v_depth;
+    j["prefetch"] = {{"LDK", p.k_prefetch}, {"LDV", p.v_prefetch}};
     j["num_tiles"] = p.num_tiles;
     json roles = json::object();
     for (int k = 0; k < p.num_tiles; ++k) {
@@ -399,6 +429,9 @@ std::string describe(const LoweredSchedule& s) {
       roles["correction" + std::to_string(k)] = p.cr_warp[k];
     }
     j["warpgroups"] = roles;
+    json ring = json::array();
+    for (int i = 0; i < p.ex_ring_len; ++i) ring.push_back("EX" + std::to_string(p.ex_ring[i]));
+    j["mufu_order"] = ring;
   } else {
     rings["AB"] = p.k_depth;
     j["mma_warp"] = p.mma_warp;

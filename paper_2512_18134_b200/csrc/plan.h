@@ -57,9 +57,20 @@ struct TwfaDevicePlan {
   int32_t k_depth;     // smem ring depth of the streamed K (or A) loads
   int32_t v_depth;     // smem ring depth of the streamed V (or B) loads
   int32_t load_warp;   // warp issuing the TMA loads (and the per-tile Q load)
+  // Streamed loads issue `prefetch` iterations ahead of their schedule slot:
+  // the ring of depth D hides the load latency (the reference's streaming
+  // rewrite, jointsolve.cpp:511-524), bounded so a same-warp consumer never
+  // waits on a slot its own warp frees later.
+  int32_t k_prefetch;
+  int32_t v_prefetch;
   int32_t cr_warp[TWFA_MAX_TILES];  // warpgroup start running CR_k (+ epilogue of tile k)
   int32_t sm_warp[TWFA_MAX_TILES];  // warpgroup start running MX_k / EX_k
   int32_t mma_warp;                 // GEMM: warp issuing MMA
+  // Unit-order tokens: the EX ops share one capacity-1 unit (MUFU) and the
+  // modulo schedule orders them inside the trip; the kernel realizes that
+  // reservation order with a token passed EX -> EX in slot order.
+  int32_t ex_ring_len;              // 0 = no token (stages differ / single EX)
+  uint8_t ex_ring[TWFA_MAX_TILES];  // tiles of the EX ops in slot order
   TwfaPlanOp ops[TWFA_MAX_NODES];
   // per-warp trip programs: indices into ops[], in issue order
   uint8_t prog[TWFA_MAX_WARPS][TWFA_MAX_NODES];

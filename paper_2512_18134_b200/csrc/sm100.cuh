@@ -30,6 +30,8 @@ TWFA_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
+// try_wait without a suspend-time hint: a long hint (e.g. 10 ms) was measured
+// to add wake-up latency on the critical path (FA C3: 589 vs 773 TFLOPS).
 TWFA_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -177,6 +179,19 @@ __host__ __device__ constexpr uint32_t idesc_bf16_f32(uint32_t m, uint32_t n, ui
 TWFA_DEV uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
+}
+// 2^x on the FMA/ALU pipes (no MUFU): round-to-nearest split x = j + r,
+// r in [-1/2, 1/2], 2^r by a degree-3 polynomial (max rel. error 7.5e-5,
+// far below the bf16 rounding of P), 2^j added into the exponent field.
+// Valid for x <= 0; x is clamped at -125 so the result stays normal.
+TWFA_DEV float poly_exp2(float x) {
+  x = fmaxf(x, -125.f);
+  const float t = x + 12582912.f;  // 1.5 * 2^23: low mantissa bits = round(x)
+  const float r = x - (t - 12582912.f);
+  float p = fmaf(0.05516934758823426f, r, 0.24260797973345152f);
+  p = fmaf(p, r, 0.6932611265906696f);
+  p = fmaf(p, r, 0.9999282790611532f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 TWFA_DEV float fast_exp2(float x) {
   float y;

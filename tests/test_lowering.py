@@ -102,7 +102,7 @@ def test_fa_ring_depth_follows_solution(twfa):
     (lambda s: s["M"].update(S0=99), "does not fit in L"),
     (lambda s: s["A"].update(MX0=3), "aligned warp range"),
     (lambda s: s["A"].update(EX0=8, MX0=4), "share a warpgroup"),
-    (lambda s: s["A"].update(S0=15), "cannot share the TMA warp"),
+    (lambda s: s["A"].update(S0=16), "aligned warp range"),
     (lambda s: s.update(streaming_depths={"LDK": 1, "LDV": 1}), "shallower than its consumer lag"),
 ])
 def test_bad_or_unrealizable_solutions_are_rejected(twfa, mutate, msg):

@@ -48,7 +48,7 @@ def edge(src, dst, d, delta=0, blocking=False):
     return e
 
 
-def fa_forward_problem():
+def fa_forward_problem(tc_variable_latency=False):
     """FA-forward loop body on sm_100a: two 128-row Q sub-tiles (k = 0, 1)
     share one 128-key K/V tile per iteration.
 
@@ -102,6 +102,15 @@ def fa_forward_problem():
             edge(f"PV{k}", f"PV{k}", 2, delta=1),
             edge(f"PV{k}", f"S{k}", 0, delta=1),
         ]
+    if tc_variable_latency:
+        # tcgen05.mma is asynchronous: its completion is only observed through
+        # an mbarrier (tcgen05.commit) and its latency depends on what else
+        # occupies the tensor pipe. Marked variable-latency, the GEMMs share the
+        # reserved warp with the TMA loads (they are not streamed: they have
+        # predecessors, so they keep their cycles and TC reservations).
+        for n in nodes:
+            if n["id"][0] in "SP":
+                n["variable_latency"] = True
     # scale to raw cycles
     for n in nodes:
         n["cycles"] *= T
@@ -192,6 +201,7 @@ def main():
     probs = {
         "gemm_mainloop": (gemm_problem(), 4),
         "fa_fwd": (fa_forward_problem(), 2),
+        "fa_fwd_tcvl": (fa_forward_problem(tc_variable_latency=True), 2),
     }
     for name, (raw, depth) in probs.items():
         if args.only and name != args.only:
