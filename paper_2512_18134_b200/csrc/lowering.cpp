@@ -357,7 +357,19 @@ void derive(LoweredSchedule& s) {
     if (sk.warp_count != 1 || pv.warp_count != 1) throw DomainError("MMA issue ops are single-warp");
     p.sm_warp[k] = mx.warp_start;
     p.cr_warp[k] = cr.warp_start;
+    p.heavy_wg_mask |= 1 << (mx.warp_start / 4);
+    // fuse MX_k -> EX_k when EX_k is the next op of every warp of the group
+    const int mxi = node_id("MX" + std::to_string(k)), exi = node_id("EX" + std::to_string(k));
+    bool adjacent = s.stage[static_cast<size_t>(mxi)] == s.stage[static_cast<size_t>(exi)];
+    for (int w = mx.warp_start; w < mx.warp_start + 4 && adjacent; ++w) {
+      const std::vector<int>& prog = s.warp_prog[static_cast<size_t>(w)];
+      auto it = std::find(prog.begin(), prog.end(), mxi);
+      adjacent = it != prog.end() && it + 1 != prog.end() && *(it + 1) == exi;
+    }
+    if (adjacent) p.ops[mxi].flags |= TWFA_OPF_FUSE_NEXT;
   }
+  if (__builtin_popcount(static_cast<unsigned>(p.heavy_wg_mask)) > 2)
+    throw DomainError("softmax of more than two warpgroups exceeds the register file");
   // MUFU reservation order of the EX ops (all EX share the unit; realized as a
   // token ring when they share a stage so every trip holds each of them once)
   {
@@ -429,6 +441,10 @@ std::string describe(const LoweredSchedule& s) {
       roles["correction" + std::to_string(k)] = p.cr_warp[k];
     }
     j["warpgroups"] = roles;
+    json fused = json::array();
+    for (int v = 0; v < p.num_nodes; ++v)
+      if (p.ops[v].flags & TWFA_OPF_FUSE_NEXT) fused.push_back(s.nodes[static_cast<size_t>(v)].id);
+    j["register_resident_softmax"] = fused;
     json ring = json::array();
     for (int i = 0; i < p.ex_ring_len; ++i) ring.push_back("EX" + std::to_string(p.ex_ring[i]));
     j["mufu_order"] = ring;

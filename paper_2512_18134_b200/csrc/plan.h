@@ -31,7 +31,7 @@ enum TwfaOpKind : uint8_t {
   TWFA_OP_COUNT = 10
 };
 
-struct TwfaPlanOp {
+struct alignas(16) TwfaPlanOp {  // 16 bytes: one vector load on the device
   uint8_t node;        // index in the problem graph (declaration order)
   uint8_t kind;        // TwfaOpKind
   uint8_t tile;        // Q sub-tile k for S/MX/EX/CR/PV, else 0
@@ -40,7 +40,14 @@ struct TwfaPlanOp {
   uint8_t warp_start;  // A(v)
   uint8_t warp_count;  // warps_required(v)
   uint8_t order;       // rank inside the trip on its warp(s)
+  uint8_t flags;       // TWFA_OPF_*
+  uint8_t pad[7];
 };
+
+// MX_k is immediately followed by EX_k (same stage) in the trip program of
+// every warp of its warpgroup: the kernel keeps the S row in registers
+// between the two ops instead of re-reading it from tensor memory.
+#define TWFA_OPF_FUSE_NEXT 1
 
 // Kind of the workload the plan drives.
 enum TwfaPlanFamily : int32_t { TWFA_FAMILY_FA_FWD = 1, TWFA_FAMILY_GEMM = 2 };
@@ -69,6 +76,7 @@ struct TwfaDevicePlan {
   // Unit-order tokens: the EX ops share one capacity-1 unit (MUFU) and the
   // modulo schedule orders them inside the trip; the kernel realizes that
   // reservation order with a token passed EX -> EX in slot order.
+  int32_t heavy_wg_mask;            // bit w: warpgroup w runs MX/EX (gets the big register budget)
   int32_t ex_ring_len;              // 0 = no token (stages differ / single EX)
   uint8_t ex_ring[TWFA_MAX_TILES];  // tiles of the EX ops in slot order
   TwfaPlanOp ops[TWFA_MAX_NODES];

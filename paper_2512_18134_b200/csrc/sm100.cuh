@@ -25,6 +25,13 @@ TWFA_DEV void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.clus
 TWFA_DEV void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// One arrival per warp (barrier count = warps): the lanes' prior shared /
+// tensor-memory writes are ordered before lane 0's release-arrive by the warp
+// barrier. 32 per-lane arrivals on one mbarrier serialize (~500 cycles).
+TWFA_DEV void warp_arrive(uint64_t* bar) {
+  __syncwarp();
+  if ((threadIdx.x & 31u) == 0) mbar_arrive(bar);
+}
 TWFA_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes)
@@ -43,11 +50,55 @@ TWFA_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-// Blocking wait on the phase with the given parity. try_wait suspends in
-// hardware for a bounded time; loop until the phase completed.
+TWFA_DEV bool mbar_try_wait_hint(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(ns)
+      : "memory");
+  return ok != 0;
+}
+// Blocking wait on the phase with the given parity. Waiting warps share the
+// issue slots of their SM sub-partition with the warps doing the softmax, so
+// the retry loop backs off (TWFA_WAIT_MODE selects the policy).
+#ifndef TWFA_WAIT_MODE
+#define TWFA_WAIT_MODE 0
+#endif
 TWFA_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if TWFA_WAIT_MODE == 0
   while (!mbar_try_wait(bar, parity)) {
   }
+#elif TWFA_WAIT_MODE == 1
+  while (!mbar_try_wait_hint(bar, parity, 200)) {
+  }
+#elif TWFA_WAIT_MODE == 2
+  if (mbar_try_wait(bar, parity)) return;
+  while (!mbar_try_wait(bar, parity)) __nanosleep(32);
+#else
+  if (mbar_try_wait(bar, parity)) return;
+  while (!mbar_try_wait(bar, parity)) __nanosleep(128);
+#endif
+}
+
+// Wait on several barriers at once: the try_waits are issued back to back so
+// their latencies overlap (a try_wait on an already completed phase still
+// costs a shared-memory round trip), then only the incomplete ones retry.
+TWFA_DEV void mbar_wait_all(uint64_t* b0, uint32_t p0, uint64_t* b1, uint32_t p1) {
+  bool d0 = mbar_try_wait(b0, p0);
+  bool d1 = mbar_try_wait(b1, p1);
+  while (!d0) d0 = mbar_try_wait(b0, p0);
+  while (!d1) d1 = mbar_try_wait(b1, p1);
+}
+TWFA_DEV void mbar_wait_all(uint64_t* b0, uint32_t p0, uint64_t* b1, uint32_t p1, uint64_t* b2, uint32_t p2) {
+  bool d0 = mbar_try_wait(b0, p0);
+  bool d1 = mbar_try_wait(b1, p1);
+  bool d2 = mbar_try_wait(b2, p2);
+  while (!d0) d0 = mbar_try_wait(b0, p0);
+  while (!d1) d1 = mbar_try_wait(b1, p1);
+  while (!d2) d2 = mbar_try_wait(b2, p2);
 }
 
 // ---------------------------------------------------------------- TMA
@@ -174,6 +225,45 @@ TWFA_DEV uint64_t sdesc_sw128(uint32_t smem_addr, uint32_t lbo_bytes, uint32_t s
 //   bit 15 A major (0 = K), bit 16 B major (0 = K, 1 = MN), 17-22 N >> 3, 24-28 M >> 4
 __host__ __device__ constexpr uint32_t idesc_bf16_f32(uint32_t m, uint32_t n, uint32_t b_mn_major) {
   return (1u << 4) | (1u << 7) | (1u << 10) | (b_mn_major << 16) | ((n >> 3) << 17) | ((m >> 4) << 24);
+}
+
+// packed fp32x2 arithmetic (Blackwell FFMA2 / FADD2 / FMUL2: two lanes per issue)
+TWFA_DEV float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+TWFA_DEV float2 fadd2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+TWFA_DEV float2 fmul2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+
+// per-warpgroup register budget (all warps of the warpgroup execute it)
+template <uint32_t kRegs>
+TWFA_DEV void setmaxnreg_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegs));
+}
+template <uint32_t kRegs>
+TWFA_DEV void setmaxnreg_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegs));
 }
 
 TWFA_DEV uint32_t pack_bf16(float lo, float hi) {

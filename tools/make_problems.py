@@ -48,7 +48,7 @@ def edge(src, dst, d, delta=0, blocking=False):
     return e
 
 
-def fa_forward_problem(tc_variable_latency=False):
+def fa_forward_problem(tc_variable_latency=False, calibrated=False):
     """FA-forward loop body on sm_100a: two 128-row Q sub-tiles (k = 0, 1)
     share one 128-key K/V tile per iteration.
 
@@ -66,6 +66,11 @@ def fa_forward_problem(tc_variable_latency=False):
     O rescaled (CR -> PV).
     """
     T = 256  # raw clk per unit (see module docstring)
+    # per-op durations in units of T: datasheet throughput (default) or the
+    # values measured on B200 by the in-kernel trace (tools/timeline.py):
+    # MX ~500 clk (TMEM load of the S row + max + handoff), EX ~1500 clk
+    # (MUFU-bound exp of a 128x128 tile + bf16 pack + TMEM store)
+    cost = dict(S=2, PV=2, MX=1, EX=4, CR=1) if not calibrated else dict(S=2, PV=2, MX=2, EX=6, CR=1)
     machine = {
         "units": [{"name": "TC", "capacity": 1}, {"name": "TMA", "capacity": 1},
                   {"name": "MUFU", "capacity": 1}, {"name": "ALU", "capacity": 1},
@@ -82,25 +87,27 @@ def fa_forward_problem(tc_variable_latency=False):
     edges = []
     for k in (0, 1):
         nodes += [
-            node(f"S{k}", "TC", 2, footprint={"tmem": 128}),
-            node(f"MX{k}", "ALU", 1, regs=128, spill_cost=1, warps_required=4),
-            node(f"EX{k}", "MUFU", 4, regs=64, warps_required=4),
-            node(f"CR{k}", "FMA", 1, regs=64, warps_required=4),
-            node(f"PV{k}", "TC", 2, footprint={"tmem": 128}),
+            node(f"S{k}", "TC", cost["S"], footprint={"tmem": 128}),
+            node(f"MX{k}", "ALU", cost["MX"], regs=128, spill_cost=1, warps_required=4),
+            node(f"EX{k}", "MUFU", cost["EX"], regs=64, warps_required=4),
+            node(f"CR{k}", "FMA", cost["CR"], regs=64, warps_required=4),
+            node(f"PV{k}", "TC", cost["PV"], footprint={"tmem": 128}),
         ]
         edges += [
             edge("LDK", f"S{k}", 0, blocking=True),
-            edge(f"S{k}", f"MX{k}", 2, blocking=True),
-            edge(f"MX{k}", f"EX{k}", 1),
-            edge(f"MX{k}", f"MX{k}", 1, delta=1),
-            edge(f"EX{k}", f"EX{k}", 4, delta=1),
-            edge(f"MX{k}", f"CR{k}", 1),
-            edge(f"EX{k}", f"PV{k}", 4, blocking=True),
+            edge(f"S{k}", f"MX{k}", cost["S"], blocking=True),
+            edge(f"MX{k}", f"EX{k}", cost["MX"]),
+            edge(f"MX{k}", f"MX{k}", cost["MX"], delta=1),
+            edge(f"EX{k}", f"EX{k}", cost["EX"], delta=1),
+            edge(f"MX{k}", f"CR{k}", cost["MX"]),
+            edge(f"EX{k}", f"PV{k}", cost["EX"], blocking=True),
             edge("LDV", f"PV{k}", 0, blocking=True),
-            edge(f"CR{k}", f"PV{k}", 1, blocking=True),
-            edge(f"PV{k}", f"CR{k}", 2, delta=1, blocking=True),
-            edge(f"PV{k}", f"PV{k}", 2, delta=1),
-            edge(f"PV{k}", f"S{k}", 0, delta=1),
+            edge(f"CR{k}", f"PV{k}", cost["CR"], blocking=True),
+            edge(f"PV{k}", f"CR{k}", cost["PV"], delta=1, blocking=True),
+            edge(f"PV{k}", f"PV{k}", cost["PV"], delta=1),
+            # S_k(i+1) overwrites the TMEM columns P_k(i) is read from: the
+            # calibrated model waits for PV_k's completion (cross-warp commit)
+            edge(f"PV{k}", f"S{k}", cost["PV"] if calibrated else 0, delta=1),
         ]
     if tc_variable_latency:
         # tcgen05.mma is asynchronous: its completion is only observed through
@@ -202,6 +209,7 @@ def main():
         "gemm_mainloop": (gemm_problem(), 4),
         "fa_fwd": (fa_forward_problem(), 2),
         "fa_fwd_tcvl": (fa_forward_problem(tc_variable_latency=True), 2),
+        "fa_fwd_cal": (fa_forward_problem(calibrated=True), 2),
     }
     for name, (raw, depth) in probs.items():
         if args.only and name != args.only:

@@ -6,7 +6,12 @@ sys.path.insert(0, os.getcwd())
 import paper_2512_18134_b200 as twfa
 from tests import oracle_lib
 import numpy as np
-p = twfa.Plan(*twfa.load_schedule(os.environ.get("SCHED", "fa_fwd")))
+_sched = os.environ.get("SCHED", "fa_fwd")
+if ":" in _sched:  # problem:solution-path (experiments)
+    _pn, _sp = _sched.split(":")
+    p = twfa.Plan(twfa.load_schedule(_pn)[0], open(os.path.join(twfa.schedule_dir(), _sp + ".solution.json")).read())
+else:
+    p = twfa.Plan(*twfa.load_schedule(_sched))
 B, H, S = [int(x) for x in os.environ.get("SHAPE", "4,32,8192").split(",")]
 causal = os.environ.get("CAUSAL", "0") == "1"
 q, k, v = (torch.randn(B, H, S, 128, device="cuda").to(torch.bfloat16) for _ in range(3))
