@@ -14,6 +14,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "_obj")
 LIB = os.path.join(PKG, "libtwfa.so")
+HOST_TOOL = os.path.join(PKG, "twfa-run")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CUDA_HOME = os.path.dirname(os.path.dirname(NVCC))
@@ -53,7 +54,10 @@ def stale():
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "twfa.h")]
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "twfa.h"),
+                                                                os.path.join(PKG, "host", "twfa_run.cpp")]
+    if not os.path.exists(HOST_TOOL):
+        return True
     return any(os.path.getmtime(d) > t for d in deps)
 
 
@@ -84,9 +88,21 @@ def build(force=False, verbose=False, ptxas_info=False, defines=(), out=None):
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"]
     log += run(cmd, verbose)
     shutil.move(tmp, lib)
+    if out is None and not defines:
+        build_host_tool(verbose)
     if ptxas_info:
         print(log)
     return lib
+
+
+def build_host_tool(verbose=False):
+    """twfa-run: the C++ host program over the C ABI (host/twfa_run.cpp),
+    linked against the in-tree libtwfa.so (rpath $ORIGIN)."""
+    src = os.path.join(PKG, "host", "twfa_run.cpp")
+    cmd = [host_cxx(), "-std=c++17", "-O2", "-Wall", "-Wextra", src, "-I" + os.path.join(ROOT, "include"),
+           "-L" + PKG, "-ltwfa", "-Wl,-rpath,$ORIGIN", "-o", HOST_TOOL]
+    run(cmd, verbose)
+    return HOST_TOOL
 
 
 if __name__ == "__main__":

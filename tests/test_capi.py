@@ -2,6 +2,7 @@
 include/twfa.h; argument / document errors come back as the reference's exit
 codes (1 domain, 2 usage) with a message, without a GPU."""
 import ctypes
+import json
 import os
 import re
 
@@ -54,3 +55,28 @@ def test_plan_survives_threads(twfa):
     [t.start() for t in ts]
     [t.join() for t in ts]
     assert out == [9] * 8
+
+
+def _host_tool(twfa):
+    from paper_2512_18134_b200 import _build
+    if not os.path.exists(_build.HOST_TOOL):
+        _build.build_host_tool()
+    return _build.HOST_TOOL
+
+
+def test_host_tool_exit_codes(twfa):
+    """twfa-run (the C++ host over the C ABI) follows the reference CLI's exit
+    map (cli.cpp:462-471): 2 usage, 1 domain error, 0 ok."""
+    import subprocess
+    tool = _host_tool(twfa)
+    d = twfa.schedule_dir()
+    prob, sol = os.path.join(d, "fa_fwd.json"), os.path.join(d, "fa_fwd.solution.json")
+    assert subprocess.run([tool, "fa", prob], capture_output=True).returncode == 2
+    assert subprocess.run([tool, "bogus", prob, sol], capture_output=True).returncode == 2
+    assert subprocess.run([tool, "fa", prob, sol, "--S", "x"], capture_output=True).returncode == 2
+    r = subprocess.run([tool, "fa", prob, os.path.join(d, "gemm_mainloop.solution.json")], capture_output=True,
+                       text=True)
+    assert r.returncode == 1 and "unknown node" in r.stderr
+    r = subprocess.run([tool, "describe", prob, sol], capture_output=True, text=True)
+    assert r.returncode == 0
+    assert json.loads(r.stdout)["I"] == json.loads(open(sol).read())["I"]

@@ -112,3 +112,21 @@ def test_full_size_causal_against_cudnn_sdpa(twfa, plan):
     ref = torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True)
     d = (o.float() - ref.float()).abs()
     assert d.max().item() <= 2.5e-2 and d.mean().item() <= 2e-3
+
+
+def test_host_tool_runs_through_c_abi(twfa):
+    """The C++ host (twfa-run, host buffers through twfa_fa_fwd_host) produces
+    the same O as the device-pointer call on the same inputs."""
+    import json
+    import os
+    import subprocess
+    from paper_2512_18134_b200 import _build
+    if not os.path.exists(_build.HOST_TOOL):
+        _build.build_host_tool()
+    d = twfa.schedule_dir()
+    r = subprocess.run([_build.HOST_TOOL, "fa", os.path.join(d, "fa_fwd.json"), os.path.join(d, "fa_fwd.solution.json"),
+                        "--B", "1", "--H", "2", "--S", "512", "--iters", "2"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    out = json.loads(r.stdout)
+    assert out["S"] == 512 and np.isfinite(out["o_sum"]) and np.isfinite(out["lse_sum"])
+    assert out["e2e_tflops"] > 0

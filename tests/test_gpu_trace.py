@@ -64,11 +64,21 @@ def test_realized_schedule_is_the_solution(twfa):
         for node, it, trip, *_clk in recs:
             realized_warps[ids[node]].add(w)
             realized_stage[ids[node]].add(trip - it)
+    # Streamed loads (variable latency, no predecessors: the reference's
+    # streaming rewrite, jointsolve.cpp:511-524, turns them into zero-cycle ops
+    # whose ring depth is a free parameter) fill a ring of depth D: the load of
+    # iteration i may issue up to `prefetch` trips before the trip its
+    # stage names, never after it. Every other op issues exactly in its stage.
+    prefetch = desc.get("prefetch", {})
     for v in ids:
         a = solution["A"][v]
         wr = next(n.get("warps_required", 1) for n in names if n["id"] == v)
         assert realized_warps[v] == set(range(a, a + wr)), (v, realized_warps[v])
-        assert realized_stage[v] == {solution["M"][v] // I}, (v, realized_stage[v])
+        st = solution["M"][v] // I
+        if v in prefetch:
+            assert realized_stage[v] <= set(range(st - prefetch[v], st + 1)), (v, realized_stage[v])
+        else:
+            assert realized_stage[v] == {st}, (v, realized_stage[v])
     # issue order inside each trip on each warp: by M mod I, then declaration order
     for w, recs in per_warp.items():
         expect = []
@@ -76,6 +86,12 @@ def test_realized_schedule_is_the_solution(twfa):
                + next(n.get("warps_required", 1) for n in names if n["id"] == v)]
         ops.sort(key=lambda v: (solution["M"][v] % I, ids.index(v)))
         max_stage = max(solution["M"][v] // I for v in ids)
+        if any(v in prefetch for v in ops):
+            # the TMA warp: each load iteration exactly once, in iteration order per load
+            for v in ops:
+                its = [rec[1] for rec in recs if rec[0] == ids.index(v)]
+                assert its == list(range(N)), f"{v} iterations {its}"
+            continue
         for r in range(N + max_stage):
             for v in ops:
                 it = r - solution["M"][v] // I
@@ -84,7 +100,8 @@ def test_realized_schedule_is_the_solution(twfa):
         assert [rec[:3] for rec in recs] == expect, f"warp {w} issue order differs"
 
     # realized (M', A') back through the reference validator
-    m_real = {v: min(realized_stage[v]) * I + solution["M"][v] % I for v in ids}
+    m_real = {v: (solution["M"][v] // I if v in prefetch else min(realized_stage[v])) * I + solution["M"][v] % I
+              for v in ids}
     a_real = {v: min(realized_warps[v]) for v in ids}
     realized = dict(solution, M=m_real, A=a_real)
     ws = _ref()
