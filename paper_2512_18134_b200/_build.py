@@ -15,6 +15,44 @@ CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "_obj")
 LIB = os.path.join(PKG, "libtwfa.so")
 HOST_TOOL = os.path.join(PKG, "twfa-run")
+GEN_TOOL = os.path.join(PKG, "twfa-gen")
+GEN_INC = os.path.join(CSRC, "gen", "fa_plans.inc")
+SCHED = os.path.join(PKG, "schedules")
+
+
+def specializations():
+    """(identifier, problem, solution) of every committed FA schedule: each
+    gets a build-time specialized kernel (csrc/gen_main.cpp)."""
+    out = []
+    for f in sorted(os.listdir(SCHED)):
+        if f.endswith(".solution.json") and f.startswith("fa_fwd"):
+            name = f[: -len(".solution.json")]
+            out.append((name, os.path.join(SCHED, name + ".json"), os.path.join(SCHED, f)))
+    exp = os.path.join(SCHED, "experiments")
+    if os.path.isdir(exp):
+        for f in sorted(os.listdir(exp)):
+            if f.endswith(".solution.json"):
+                name = f[: -len(".solution.json")]
+                out.append((name, os.path.join(SCHED, "fa_fwd.json"), os.path.join(exp, f)))
+    only = os.environ.get("TWFA_SPECIALIZE")  # comma list: limit (experiment builds)
+    if only is not None:
+        keep = set(only.split(",")) - {""}
+        out = [e for e in out if e[0] in keep]
+    return out
+
+
+def generate_plans(verbose=False):
+    """twfa-gen: lowering.cpp + gen_main.cpp on the host compiler, then the
+    committed schedules -> gen/fa_plans.inc (compile-time TwfaDevicePlans)."""
+    inc = ["-I" + CSRC, "-I" + json_include()]
+    run([host_cxx(), "-std=c++20", "-O1", "-Wall", os.path.join(CSRC, "lowering.cpp"), os.path.join(CSRC, "gen_main.cpp"),
+         *inc, "-o", GEN_TOOL], verbose)
+    os.makedirs(os.path.dirname(GEN_INC), exist_ok=True)
+    args = [GEN_TOOL, GEN_INC]
+    for name, prob, sol in specializations():
+        args += [name, prob, sol]
+    run(args, verbose)
+    return GEN_INC
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CUDA_HOME = os.path.dirname(os.path.dirname(NVCC))
@@ -54,8 +92,9 @@ def stale():
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "twfa.h"),
-                                                                os.path.join(PKG, "host", "twfa_run.cpp")]
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f != "gen"] + [
+        os.path.join(ROOT, "include", "twfa.h"), os.path.join(PKG, "host", "twfa_run.cpp")]
+    deps += [p for _, a, b in specializations() for p in (a, b)]
     if not os.path.exists(HOST_TOOL):
         return True
     return any(os.path.getmtime(d) > t for d in deps)
@@ -68,13 +107,14 @@ def build(force=False, verbose=False, ptxas_info=False, defines=(), out=None):
         return LIB
     obj_dir = OBJ if not defines else os.path.join(OBJ, "v_" + "_".join(d.replace("=", "") for d in defines))
     os.makedirs(obj_dir, exist_ok=True)
+    generate_plans(verbose)
     cu, cpp = sources()
     inc = ["-I" + CSRC, "-I" + os.path.join(ROOT, "include"), "-I" + json_include()]
     objs = []
     log = ""
     for src in cu:
         obj = os.path.join(obj_dir, os.path.basename(src) + ".o")
-        cmd = [NVCC, *ARCH, "-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-c", src, "-o", obj, *inc,
+        cmd = [NVCC, *ARCH, "-std=c++20", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-c", src, "-o", obj, *inc,
                "--use_fast_math", "-Xptxas", "-v" if ptxas_info else "-O3", *["-D" + d for d in defines]]
         log += run(cmd, verbose)
         objs.append(obj)

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -85,6 +86,13 @@ CUtensorMap make_map(const void* base, int rank, const cuuint64_t* dims, const c
   return m;
 }
 
+// TWFA_KERNEL=interpreter forces the runtime interpreter even for plans that
+// have a build-time specialization (tests compare the two realizations).
+bool allow_specialized() {
+  const char* e = std::getenv("TWFA_KERNEL");
+  return !(e && std::strcmp(e, "interpreter") == 0);
+}
+
 int sm_count() {
   int dev = 0, n = 0;
   check(cudaGetDevice(&dev), "cudaGetDevice");
@@ -129,7 +137,8 @@ int fa_fwd_impl(const twfa_plan* plan, const void* q, const void* k, const void*
   a.scale_log2 = scale * 1.4426950408889634f;
   const long long work = static_cast<long long>(bh) * ((S + 255) / 256);
   const int grid = static_cast<int>(std::min<long long>(work, sm_count()));
-  check(twfa::fa_fwd_launch(tq, tk, tv, p, a, grid, static_cast<cudaStream_t>(stream)), "fa_fwd launch");
+  check(twfa::fa_fwd_launch(tq, tk, tv, p, a, grid, static_cast<cudaStream_t>(stream), allow_specialized()),
+        "fa_fwd launch");
   return TWFA_OK;
 }
 
@@ -163,6 +172,12 @@ int twfa_plan_create(const char* problem_json, const char* solution_json, twfa_p
     if (!problem_json || !solution_json || !out) throw twfa::UsageError("NULL argument");
     auto* p = new twfa_plan{twfa::lower(problem_json, solution_json), {}};
     p->description = twfa::describe(p->sched);
+    if (p->sched.plan.family == TWFA_FAMILY_FA_FWD) {  // which kernel realizes it
+      const std::string name = twfa::fa_fwd_kernel_name(p->sched.plan);
+      const std::string kernel =
+          allow_specialized() && name != "interpreter" ? "specialized:" + name : std::string("interpreter");
+      p->description.insert(p->description.size() - 1, ",\"kernel\":\"" + kernel + "\"");
+    }
     *out = p;
     return TWFA_OK;
   });

@@ -21,8 +21,13 @@ struct FaArgs {
 };
 
 size_t fa_fwd_smem_bytes(const TwfaDevicePlan& plan);
+// Runs the build-time specialized kernel of `plan` when one was generated
+// (gen/fa_plans.inc) and allow_specialized is set, else the interpreter.
 cudaError_t fa_fwd_launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                          const TwfaDevicePlan& plan, const FaArgs& args, int grid, cudaStream_t stream);
+                          const TwfaDevicePlan& plan, const FaArgs& args, int grid, cudaStream_t stream,
+                          bool allow_specialized);
+// "specialized:<name>" or "interpreter"
+const char* fa_fwd_kernel_name(const TwfaDevicePlan& plan);
 
 struct GemmArgs {
   __nv_bfloat16* c;  // [M, N] row-major

@@ -366,7 +366,13 @@ void derive(LoweredSchedule& s) {
       auto it = std::find(prog.begin(), prog.end(), mxi);
       adjacent = it != prog.end() && it + 1 != prog.end() && *(it + 1) == exi;
     }
-    if (adjacent) p.ops[mxi].flags |= TWFA_OPF_FUSE_NEXT;
+    if (adjacent) {
+      p.ops[mxi].flags |= TWFA_OPF_FUSE_NEXT;
+      p.ops[exi].flags |= TWFA_OPF_FUSED;
+    }
+    // same issuing warp for S_k and PV_k: the realizability check above
+    // guarantees PV_k(i-1) precedes S_k(i) in that warp's program order
+    if (sk.warp_start == pv.warp_start) p.ops[node_id("S" + std::to_string(k))].flags |= TWFA_OPF_INORDER;
   }
   if (__builtin_popcount(static_cast<unsigned>(p.heavy_wg_mask)) > 2)
     throw DomainError("softmax of more than two warpgroups exceeds the register file");
@@ -441,6 +447,10 @@ std::string describe(const LoweredSchedule& s) {
       roles["correction" + std::to_string(k)] = p.cr_warp[k];
     }
     j["warpgroups"] = roles;
+    json inorder = json::array();
+    for (int v = 0; v < p.num_nodes; ++v)
+      if (p.ops[v].flags & TWFA_OPF_INORDER) inorder.push_back(s.nodes[static_cast<size_t>(v)].id);
+    j["inorder_tc_issue"] = inorder;
     json fused = json::array();
     for (int v = 0; v < p.num_nodes; ++v)
       if (p.ops[v].flags & TWFA_OPF_FUSE_NEXT) fused.push_back(s.nodes[static_cast<size_t>(v)].id);

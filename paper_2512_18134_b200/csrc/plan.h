@@ -48,6 +48,14 @@ struct alignas(16) TwfaPlanOp {  // 16 bytes: one vector load on the device
 // every warp of its warpgroup: the kernel keeps the S row in registers
 // between the two ops instead of re-reading it from tensor memory.
 #define TWFA_OPF_FUSE_NEXT 1
+// S_k is issued by the same thread as PV_k, after PV_k(i-1) in program order:
+// tcgen05.mma ops of one thread execute in issue order, so S_k(i) cannot
+// overwrite the P_k(i-1) columns before PV_k(i-1) has read them and the
+// issue needs no wait on PV_k's completion (the PV_k -> S_k, delta 1, d 0
+// edge of the loop graph is realized by program order alone).
+#define TWFA_OPF_INORDER 2
+// EX_k whose work is done by the fused MX_k right before it (FUSE_NEXT).
+#define TWFA_OPF_FUSED 4
 
 // Kind of the workload the plan drives.
 enum TwfaPlanFamily : int32_t { TWFA_FAMILY_FA_FWD = 1, TWFA_FAMILY_GEMM = 2 };

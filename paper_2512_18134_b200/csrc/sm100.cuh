@@ -16,6 +16,15 @@ TWFA_DEV uint32_t smem_u32(const void* p) {
 }
 TWFA_DEV uint32_t lane_id() { return threadIdx.x & 31u; }
 TWFA_DEV uint32_t warp_id() { return __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0); }
+// One lane of the (converged) warp: elect.sync, which ptxas knows selects a
+// single thread, so tcgen05 / TMA issue keeps its operands in uniform registers.
+TWFA_DEV bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
 
 // ---------------------------------------------------------------- mbarrier
 TWFA_DEV void mbar_init(uint64_t* bar, uint32_t count) {
@@ -246,6 +255,15 @@ TWFA_DEV float2 fadd2(float2 a, float2 b) {
       : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
   return d;
 }
+TWFA_DEV float2 fsub2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "sub.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
 TWFA_DEV float2 fmul2(float2 a, float2 b) {
   float2 d;
   asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
@@ -282,6 +300,26 @@ TWFA_DEV float poly_exp2(float x) {
   p = fmaf(p, r, 0.6932611265906696f);
   p = fmaf(p, r, 0.9999282790611532f);
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+TWFA_DEV float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+// Two 2^x on the FMA pipe with packed f32x2 arithmetic (same polynomial and
+// range as poly_exp2): 2 FMNMX + 3 FADD2 + 3 FFMA2 + 2 IMAD for the pair.
+TWFA_DEV float2 poly_exp2x2(float2 x) {
+  x.x = fmaxf(x.x, -125.f);
+  x.y = fmaxf(x.y, -125.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  const float2 t = fadd2(x, magic);
+  const float2 r = fsub2(x, fsub2(t, magic));
+  float2 p = ffma2(make_float2(0.05516934758823426f, 0.05516934758823426f), r,
+                   make_float2(0.24260797973345152f, 0.24260797973345152f));
+  p = ffma2(p, r, make_float2(0.6932611265906696f, 0.6932611265906696f));
+  p = ffma2(p, r, make_float2(0.9999282790611532f, 0.9999282790611532f));
+  return make_float2(__int_as_float(__float_as_int(t.x) * (1 << 23) + __float_as_int(p.x)),
+                     __int_as_float(__float_as_int(t.y) * (1 << 23) + __float_as_int(p.y)));
 }
 TWFA_DEV float fast_exp2(float x) {
   float y;

@@ -7,7 +7,12 @@ what = sys.argv[1]
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 dev = torch.device("cuda:0")
 if what in ("fa", "fa_causal"):
-    p = twfa.Plan(*twfa.load_schedule("fa_fwd"))
+    sched = os.environ.get("SCHED", "fa_fwd")
+    if ":" in sched:  # problem:solution-path (experiments)
+        pn, sp = sched.split(":")
+        p = twfa.Plan(twfa.load_schedule(pn)[0], open(os.path.join(twfa.schedule_dir(), sp + ".solution.json")).read())
+    else:
+        p = twfa.Plan(*twfa.load_schedule(sched))
     B, H, S = (4, 32, 8192) if what == "fa" else (2, 32, 16384)
     q, k, v = (torch.randn(B, H, S, 128, device=dev).to(torch.bfloat16) for _ in range(3))
     for _ in range(n):

@@ -8,7 +8,12 @@ import paper_2512_18134_b200 as twfa
 B, H, S = (int(x) for x in sys.argv[1:4])
 name = sys.argv[4] if len(sys.argv) > 4 else "fa_fwd"
 causal = len(sys.argv) > 5 and sys.argv[5] == "1"
-prob, sol = twfa.load_schedule(name)
+if ":" in name:  # problem:solution-path (experiments)
+    pn, sp = name.split(":")
+    prob = twfa.load_schedule(pn)[0]
+    sol = open(os.path.join(twfa.schedule_dir(), sp + ".solution.json")).read()
+else:
+    prob, sol = twfa.load_schedule(name)
 plan = twfa.Plan(prob, sol)
 ids = [n["id"] for n in json.loads(prob)["graph"]["nodes"]]
 nw, cap = plan.describe()["num_warps"], 8192
@@ -44,5 +49,5 @@ mid = 30
 start = min(r[4] for r in recs if r[3] == mid)
 print(f"\ntrip {mid}..{mid+1} of work tile 0: warp op it issue ready done")
 for r in sorted(recs, key=lambda r: r[4]):
-    if r[3] in (mid, mid + 1) and d(start, r[4]) < 20000 and r[0] % 4 in (0, 1, 2, 3) and (r[0] in (2, 4, 7, 8, 13, 14, 15, 0) ):
+    if r[3] in (mid, mid + 1) and d(start, r[4]) < 20000 and (r[0] % 4 == 0 or r[0] >= 12 or r[1][0] in "SP"):
         print(f"w{r[0]:2d} {r[1]:4s} it={r[2]:3d} trip={r[3]:3d} issue={d(start, r[4]):6d} ready={d(start, r[5]) if r[5] else -1:6d} done={d(start, r[6]):6d}")
