@@ -326,7 +326,8 @@ def run_ours(args, world, rank, local):
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": load_traffic(workload),
                      "peak_kind": f"{peak_kind} bf16 burst (MEASURED_PEAKS.json)",
-                     "kernel": "twfa::fa_fwd_kernel", "flops_per_launch": flops,
+                     "kernel": "twfa::fa_fwd_spec (" + plan.describe().get("kernel", "?") + ")",
+                     "flops_per_launch": flops,
                      "launch_ms": per_launch_ms},
         "clocks": clocks.summary(),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,

@@ -172,12 +172,15 @@ __device__ __forceinline__ float exp_store_row(const uint32_t (&s)[128], uint32_
       acc[(i >> 1) & 1] = fadd2(acc[(i >> 1) & 1], p);
       pk[i >> 1] = pack_bf16(p.x, p.y);
     }
-    tmem_st16(taddr + c * 16, pk);
-    if (c == 1) {  // keys 0-63 of P are in tensor memory: release the first half of PV
+    if (c == 2) {
+      // keys 0-63 of P (chunks 0, 1) are in tensor memory: release the first
+      // half of PV. The store wait is placed after chunk 2's exponentials so
+      // the MUFU stream does not drain behind it.
       tmem_st_wait();
       tc_fence_before();
       warp_arrive(half_bar);
     }
+    tmem_st16(taddr + c * 16, pk);
   }
   tmem_st_wait();
   return (acc[0].x + acc[0].y) + (acc[1].x + acc[1].y);

@@ -1,0 +1,2 @@
+SCHED=fa_fwd_tcvl timeout 900 ncu --set full --clock-control none --import-source on -k regex:fa_fwd -c 1 -f -o gpurun_out/tcvl_full python tools/prof_run.py fa 2 > gpurun_out/ncu_tcvl.log 2>&1
+tail -1 gpurun_out/ncu_tcvl.log

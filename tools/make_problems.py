@@ -207,8 +207,10 @@ def main():
     args = ap.parse_args()
     probs = {
         "gemm_mainloop": (gemm_problem(), 4),
-        "fa_fwd": (fa_forward_problem(), 2),
-        "fa_fwd_tcvl": (fa_forward_problem(tc_variable_latency=True), 2),
+        # production: tcgen05.mma modeled as variable latency (see fa_forward_problem)
+        "fa_fwd": (fa_forward_problem(tc_variable_latency=True), 2),
+        # comparison: MMAs as fixed-latency ops (the solver scatters them over warps)
+        "fa_fwd_fixedtc": (fa_forward_problem(), 2),
         "fa_fwd_cal": (fa_forward_problem(calibrated=True), 2),
     }
     for name, (raw, depth) in probs.items():

@@ -30,8 +30,10 @@ ro, _ = oracle_lib.attention(qs.float().numpy(), ks.float().numpy(), vs.float().
 print(f"{os.environ.get('SCHED','fa_fwd')} {os.path.basename(os.environ['TWFA_LIB'])}: {ms:.3f} ms {fl/ms/1e9:.1f} TFLOPS  maxerr {np.abs(o-ro).max():.2e}", flush=True)
 '''
 scheds = os.environ.get("SCHEDS", "fa_fwd").split(",")
-for lib in sys.argv[1:]:
+reps = int(os.environ.get("REPS", "1"))
+for rep in range(reps):  # interleaved repeats: A/B on the same box and thermal state
   for sch in scheds:
-    env = dict(os.environ, TWFA_LIB=os.path.abspath(lib), SCHED=sch)
-    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=120)
-    print(r.stdout.strip() or r.stderr[-2000:], flush=True)
+    for lib in sys.argv[1:]:
+      env = dict(os.environ, TWFA_LIB=os.path.abspath(lib), SCHED=sch)
+      r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=120)
+      print(r.stdout.strip() or r.stderr[-2000:], flush=True)
