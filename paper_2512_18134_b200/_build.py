@@ -41,14 +41,21 @@ def specializations():
     return out
 
 
-def generate_plans(verbose=False):
+def generate_plans(gen_root, verbose=False):
     """twfa-gen: lowering.cpp + gen_main.cpp on the host compiler, then the
-    committed schedules -> gen/fa_plans.inc (compile-time TwfaDevicePlans)."""
+    committed schedules -> <gen_root>/gen/: fa_plans.inc (compile-time
+    TwfaDevicePlans), one fa_spec_<id>.cu per specialization, and their
+    launcher declarations."""
     inc = ["-I" + CSRC, "-I" + json_include()]
+    tool = os.path.join(gen_root, "twfa-gen") if gen_root != CSRC else GEN_TOOL
     run([host_cxx(), "-std=c++20", "-O1", "-Wall", os.path.join(CSRC, "lowering.cpp"), os.path.join(CSRC, "gen_main.cpp"),
-         *inc, "-o", GEN_TOOL], verbose)
-    os.makedirs(os.path.dirname(GEN_INC), exist_ok=True)
-    args = [GEN_TOOL, GEN_INC]
+         *inc, "-o", tool], verbose)
+    gen = os.path.join(gen_root, "gen")
+    if os.path.isdir(gen):
+        for f in os.listdir(gen):
+            os.remove(os.path.join(gen, f))
+    os.makedirs(gen, exist_ok=True)
+    args = [tool, os.path.join(gen, "fa_plans.inc")]
     for name, prob, sol in specializations():
         args += [name, prob, sol]
     run(args, verbose)
@@ -82,8 +89,11 @@ def run(cmd, verbose):
     return r.stdout + r.stderr
 
 
-def sources():
-    cu = [os.path.join(CSRC, f) for f in ("fa_fwd_sm100.cu", "gemm_sm100.cu")]
+def sources(gen_root=CSRC):
+    gen = os.path.join(gen_root, "gen")
+    specs = sorted(os.path.join(gen, f) for f in os.listdir(gen) if f.startswith("fa_spec_") and f.endswith(".cu")) \
+        if os.path.isdir(gen) else []
+    cu = [os.path.join(CSRC, f) for f in ("fa_fwd_sm100.cu", "gemm_sm100.cu")] + specs
     cpp = [os.path.join(CSRC, f) for f in ("lowering.cpp", "capi.cpp")]
     return cu, cpp
 
@@ -107,17 +117,24 @@ def build(force=False, verbose=False, ptxas_info=False, defines=(), out=None):
         return LIB
     obj_dir = OBJ if not defines else os.path.join(OBJ, "v_" + "_".join(d.replace("=", "") for d in defines))
     os.makedirs(obj_dir, exist_ok=True)
-    generate_plans(verbose)
-    cu, cpp = sources()
-    inc = ["-I" + CSRC, "-I" + os.path.join(ROOT, "include"), "-I" + json_include()]
+    # variant builds keep their generated specializations next to their objects
+    gen_root = CSRC if (out is None and not defines) else obj_dir
+    generate_plans(gen_root, verbose)
+    cu, cpp = sources(gen_root)
+    inc = ["-I" + gen_root, "-I" + CSRC, "-I" + os.path.join(ROOT, "include"), "-I" + json_include()]
     objs = []
     log = ""
+    cmds = []
     for src in cu:
         obj = os.path.join(obj_dir, os.path.basename(src) + ".o")
-        cmd = [NVCC, *ARCH, "-std=c++20", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-c", src, "-o", obj, *inc,
-               "--use_fast_math", "-Xptxas", "-v" if ptxas_info else "-O3", *["-D" + d for d in defines]]
-        log += run(cmd, verbose)
+        cmds.append([NVCC, *ARCH, "-std=c++20", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-c", src, "-o", obj, *inc,
+                     "--use_fast_math", "-Xptxas", "-v" if ptxas_info else "-O3", *["-D" + d for d in defines]])
         objs.append(obj)
+    # the translation units are independent: compile them concurrently
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 4)) as ex:
+        for out_text in ex.map(lambda c: run(c, verbose), cmds):
+            log += out_text
     for src in cpp:
         obj = os.path.join(obj_dir, os.path.basename(src) + ".o")
         cmd = [host_cxx(), "-std=c++17", "-O2", "-fPIC", "-Wall", "-c", src, "-o", obj, *inc,

@@ -1,773 +1,11 @@
-// FA-forward on sm_100a, realized from a Twill joint schedule.
-//
-// Loop body (reference: proj/tests/testutil.hpp:13-15, PAPER.md:185-191,
-// Blackwell strategy PAPER.md:1015-1046), per 128-key K/V tile and per
-// 128-row Q sub-tile k of the CTA's 256-row query block:
-//   LDK, LDV  TMA loads into smem rings (depth = streaming_depths)
-//   S_k       S_k = Q_k K^T           tcgen05.mma SS -> TMEM cols [128k, 128k+128)
-//   MX_k      m_new = max(m, rowmax(S_k) * scale*log2e); alpha = exp2(m - m_new)
-//   EX_k      P_k = exp2(S_k*scale*log2e - m_new) -> bf16 over S_k in TMEM; l = l*alpha + rowsum
-//   CR_k      O_k *= alpha            tcgen05.ld / st on TMEM cols [256+128k, ...)
-//   PV_k      O_k += P_k V            tcgen05.mma TS (A = P from TMEM)
-//
-// Which warp runs which op, in which order and in which pipeline stage is
-// NOT hard-coded: every warp walks its trip program from the TwfaDevicePlan
-// (lowering.cpp), i.e. the solver's A(v) and M(v). Trip r runs op v on
-// iteration r - stage(v); trips before max_stage are the prologue and trips
-// past the last iteration the epilogue, exactly the region split of the
-// reference's program synthesis (codegen.cpp:43-189). Every edge of the loop
-// graph that the schedule places across warps is an mbarrier (the
-// reference's `spill_recv` / xfer sites); same-warp edges that go through the
-// asynchronous tensor core still wait on the MMA commit barrier, except
-// PV_k -> S_k when one thread issues both (tcgen05 ops of a thread execute in
-// order).
-//
-// Two kernels realize a plan, sharing every op body (exec_op):
-//  * fa_fwd_spec<P>: one instantiation per schedule generated at build time
-//    from the committed solution JSON (twfa-gen, gen/fa_plans.inc). Each
-//    warp's trip program is a compile-time sequence, so op dispatch, ring
-//    arithmetic and flags fold away.
-//  * fa_fwd_interp: walks the trip programs at run time (any other plan).
-//
-// Register classes: warpgroups that run softmax ops (MX/EX) raise their
-// register budget with setmaxnreg and keep a 128-column S row resident; the
-// other warpgroups (TMA, MMA issue, correction) lower theirs.
-#include <cuda.h>
-#include <cuda_bf16.h>
-#include <cuda_runtime.h>
-#include <stdint.h>
-
-#include <utility>
-
-#include "fa_fwd.h"
-#include "gen/fa_plans.inc"
-#include "sm100.cuh"
+// FA-forward on sm_100a: launch dispatch and the runtime interpreter.
+// The kernel bodies are in fa_fwd_kernel.cuh; every build-time specialized
+// schedule is instantiated in its own generated translation unit
+// (gen/fa_spec_<id>.cu, twfa-gen) and reached through gen/fa_spec_launch.h.
+#include "fa_fwd_kernel.cuh"
+#include <gen/fa_spec_launch.h>
 
 namespace twfa {
-
-namespace {
-
-constexpr int kBlockQ = 128;  // rows per Q sub-tile (= TMEM lanes)
-constexpr int kBlockK = 128;  // keys per K/V tile
-constexpr int kHeadDim = 128;
-constexpr uint32_t kTileBytes = kBlockQ * kHeadDim * 2;  // 32 KiB, two 16 KiB SW128 column halves
-constexpr uint32_t kHalfBytes = kTileBytes / 2;
-constexpr int kMaxRing = 4;
-#ifndef TWFA_POLY_EVERY
-#define TWFA_POLY_EVERY 1000  // measured: MUFU-only is fastest while the loop is latency-bound
-#endif
-constexpr int kPolyEvery = TWFA_POLY_EVERY;  // 1 in kPolyEvery exp2 pairs on the FMA pipe
-// Online-softmax rescale threshold (log2 units): the running max is only
-// moved when a row's max grows by more than 2^8, so P <= 256 and most
-// iterations need no O correction. The final O / l is unchanged in exact
-// arithmetic (m cancels); bf16 P and fp32 l stay far from overflow.
-constexpr float kRescaleLog2 = 8.0f;
-constexpr uint32_t kIdescS = idesc_bf16_f32(128, kBlockK, 0);    // K-major Q, K-major K
-constexpr uint32_t kIdescPV = idesc_bf16_f32(128, kHeadDim, 1);  // TMEM P, MN-major V
-
-struct __align__(8) FaBarriers {
-  uint64_t q_full[TWFA_MAX_TILES], q_empty[TWFA_MAX_TILES];
-  uint64_t k_full[kMaxRing], k_empty[kMaxRing];
-  uint64_t v_full[kMaxRing], v_empty[kMaxRing];
-  uint64_t s_full[TWFA_MAX_TILES], p_full[TWFA_MAX_TILES], p_half[TWFA_MAX_TILES];
-  uint64_t o_ready[TWFA_MAX_TILES], o_done[TWFA_MAX_TILES];
-  uint64_t st_full[TWFA_MAX_TILES][2], st_empty[TWFA_MAX_TILES][2];
-  uint64_t l_full[TWFA_MAX_TILES], l_empty[TWFA_MAX_TILES];
-  uint32_t tmem_base;
-};
-
-struct FaShared {
-  float stats[TWFA_MAX_TILES][2][kBlockQ];  // MX -> CR rescale factors, double-buffered
-  float lbuf[TWFA_MAX_TILES][2][kBlockQ];   // EX -> epilogue: running max, row sum
-  // per-warp trip programs (interpreted roles): one shared load per op
-  TwfaPlanOp prog[TWFA_MAX_WARPS][TWFA_MAX_NODES];
-  int prog_len[TWFA_MAX_WARPS];
-  FaBarriers bar;
-};
-
-// Barriers, handoff buffers and trip programs live in static shared memory so
-// every access compiles to LDS/STS/SYNCS on a known shared address.
-__shared__ FaShared g_sh;
-
-// Issue trace of CTA 0 (debug / schedule-realization evidence). Per warp:
-// word 0 = record count, then records of kTraceWords uint32:
-// {node, iteration, trip, t_issue, t_ready (inputs waited), t_done}.
-constexpr int kTraceWords = 8;
-
-template <bool kTrace>
-__device__ __forceinline__ uint32_t* trace_begin(const FaArgs& a, uint32_t warp, uint32_t& n, int node, int it,
-                                                 int trip) {
-  if (!kTrace || blockIdx.x != 0 || lane_id() != 0) return nullptr;
-  uint32_t* base = a.trace + static_cast<size_t>(warp) * a.trace_cap * kTraceWords;
-  if (n + 1 >= a.trace_cap) return nullptr;
-  uint32_t* e = base + (n + 1) * kTraceWords;
-  e[0] = static_cast<uint32_t>(node);
-  e[1] = static_cast<uint32_t>(it);
-  e[2] = static_cast<uint32_t>(trip);
-  e[3] = static_cast<uint32_t>(clock64());
-  base[0] = ++n;  // count kept in a register; the store is fire-and-forget
-  return e;
-}
-template <bool kTrace>
-__device__ __forceinline__ void trace_mark(uint32_t* e, int field) {
-  if (kTrace && e != nullptr) e[field] = static_cast<uint32_t>(clock64());
-}
-
-// ---------------------------------------------------------------- softmax pieces
-// all 128 scores of this thread's TMEM lane, one wait
-__device__ __forceinline__ void load_row(uint32_t taddr, uint32_t (&s)[128]) {
-  tmem_ld32(taddr + 0, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
-  tmem_ld32(taddr + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
-  tmem_ld32(taddr + 64, *reinterpret_cast<uint32_t(*)[32]>(&s[64]));
-  tmem_ld32(taddr + 96, *reinterpret_cast<uint32_t(*)[32]>(&s[96]));
-  tmem_ld_wait();
-}
-
-__device__ __forceinline__ void mask_row(uint32_t (&s)[128], int limit) {
-#pragma unroll
-  for (int i = 0; i < 128; ++i)
-    if (i >= limit) s[i] = __float_as_uint(-INFINITY);
-}
-
-// FMNMX3: three-operand max (sm_100), four independent chains
-__device__ __forceinline__ float row_max(const uint32_t (&s)[128]) {
-  float a[4] = {__uint_as_float(s[0]), __uint_as_float(s[1]), __uint_as_float(s[2]), __uint_as_float(s[3])};
-#pragma unroll
-  for (int i = 4; i < 124; i += 8) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) a[j] = fmax3(a[j], __uint_as_float(s[i + 2 * j]), __uint_as_float(s[i + 2 * j + 1]));
-  }
-  a[0] = fmax3(a[0], __uint_as_float(s[124]), __uint_as_float(s[125]));
-  a[1] = fmax3(a[1], __uint_as_float(s[126]), __uint_as_float(s[127]));
-  return fmax3(a[0], a[1], fmaxf(a[2], a[3]));
-}
-
-// P = exp2(S*sl - m) for the 128 resident scores: FFMA2 for the argument,
-// MUFU ex2 or the FMA-pipe polynomial (1 in kPolyEvery pairs) for the exp,
-// FADD2 for the row sum, F2FP to bf16 pairs, stored as the TS-MMA A operand
-// over the first 64 columns of the S tile. The first half of P (keys 0-63)
-// is released to PV_k on `half_bar` before the second half is computed.
-// Returns the row sum.
-template <bool kMask>
-__device__ __forceinline__ float exp_store_row(const uint32_t (&s)[128], uint32_t taddr, float sl, float m,
-                                               uint64_t* half_bar) {
-  const float2 sl2 = make_float2(sl, sl);
-  const float2 nm2 = make_float2(-m, -m);
-  float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    uint32_t pk[16];
-#pragma unroll
-    for (int i = 0; i < 32; i += 2) {
-      const float2 x =
-          ffma2(make_float2(__uint_as_float(s[c * 32 + i]), __uint_as_float(s[c * 32 + i + 1])), sl2, nm2);
-      float2 p;
-      // masked tiles (diagonal / sequence tail) hold -inf: MUFU maps it to 0
-      if (!kMask && ((i >> 1) % kPolyEvery) == kPolyEvery - 1) {
-        p = poly_exp2x2(x);
-      } else {
-        p.x = fast_exp2(x.x);
-        p.y = fast_exp2(x.y);
-      }
-      acc[(i >> 1) & 1] = fadd2(acc[(i >> 1) & 1], p);
-      pk[i >> 1] = pack_bf16(p.x, p.y);
-    }
-    if (c == 2) {
-      // keys 0-63 of P (chunks 0, 1) are in tensor memory: release the first
-      // half of PV. The store wait is placed after chunk 2's exponentials so
-      // the MUFU stream does not drain behind it.
-      tmem_st_wait();
-      tc_fence_before();
-      warp_arrive(half_bar);
-    }
-    tmem_st16(taddr + c * 16, pk);
-  }
-  tmem_st_wait();
-  return (acc[0].x + acc[0].y) + (acc[1].x + acc[1].y);
-}
-
-// ---------------------------------------------------------------- state
-struct FaCtx {
-  uint8_t* q_smem;
-  uint8_t* k_smem;
-  uint8_t* v_smem;
-  uint32_t tmem;
-  uint32_t warp, lane, quad, lane_off;
-  int S, BH, q_blocks, num_work;
-  float scale_log2;
-  uint64_t pol_q, pol_kv;
-};
-
-// the work tile (256 query rows of one (b, h)) a CTA is on
-struct WorkTile {
-  int bh, q0, N;    // N = K/V iterations of this tile
-  uint32_t gbase;   // global iteration index of its iteration 0 (ring phases)
-  uint32_t tcount;  // work tiles done by this CTA (Q / LSE buffer phases)
-};
-
-__device__ __forceinline__ WorkTile work_tile(const FaCtx& c, const FaArgs& args, int work, uint32_t gbase,
-                                              uint32_t tcount) {
-  WorkTile t;
-  int qb;
-  if (args.causal) {  // longest-processing-time first
-    qb = c.q_blocks - 1 - work / c.BH;
-    t.bh = work % c.BH;
-  } else {
-    t.bh = work / c.q_blocks;
-    qb = work % c.q_blocks;
-  }
-  t.q0 = qb * 2 * kBlockQ;
-  const int kv_end = args.causal ? min(c.S, t.q0 + 2 * kBlockQ) : c.S;
-  t.N = (kv_end + kBlockK - 1) / kBlockK;
-  t.gbase = gbase;
-  t.tcount = tcount;
-  return t;
-}
-
-// Number of leading keys of this K/V tile that row `row` may attend to
-// (the rest are past the sequence end or above the causal diagonal).
-__device__ __forceinline__ int valid_keys(const FaArgs& a, int row, int key0) {
-  const int end = a.causal ? min(a.S, row + 1) : a.S;
-  return max(0, min(kBlockK, end - key0));
-}
-
-// running per-warp state
-struct WarpState {
-  float m_run[TWFA_MAX_TILES], l_run[TWFA_MAX_TILES], alpha[TWFA_MAX_TILES];
-  int k_next, v_next;  // next K / V iteration to load (TMA warp)
-  uint32_t trace_n;
-};
-
-// per-tile scalars indexed by a (possibly runtime) tile: selects keep the
-// arrays in registers (a dynamic index would move them to local memory)
-__device__ __forceinline__ float rd(const float (&a)[TWFA_MAX_TILES], int k) { return k == 0 ? a[0] : a[1]; }
-__device__ __forceinline__ void wr(float (&a)[TWFA_MAX_TILES], int k, float x) {
-  if (k == 0) a[0] = x; else a[1] = x;
-}
-
-// Ring geometry: depths and prefetch distances of the streamed loads
-// (compile-time constants in the specialized kernels).
-struct Rings {
-  int kd, vd, kpf, vpf;
-};
-
-struct Maps {
-  const CUtensorMap* q;
-  const CUtensorMap* k;
-  const CUtensorMap* v;
-};
-
-// ---------------------------------------------------------------- op bodies
-// One op of the trip program on this warp, trip r. Shared by both kernels:
-// with a compile-time `op` and `rg` every branch below folds.
-template <bool kHeavy, bool kTrace>
-__device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const FaCtx& c, const WorkTile& t,
-                                        WarpState& st, const Rings rg, const Maps& tm, const FaArgs& args) {
-  FaBarriers& bar = g_sh.bar;
-  const uint32_t warp = c.warp, lane = c.lane;
-  const uint32_t tmem = c.tmem;
-  const int N = t.N;
-
-  if (op.kind == TWFA_OP_LDK || op.kind == TWFA_OP_LDV) {
-    if constexpr (!kHeavy) {
-      // streamed load: top the ring up to iteration r - stage + prefetch.
-      // Warp-uniform address arithmetic (uniform datapath); one elected lane
-      // issues the TMA.
-      const bool is_k = op.kind == TWFA_OP_LDK;
-      const int target = min(N - 1, r - static_cast<int>(op.stage) + (is_k ? rg.kpf : rg.vpf));
-      int& next = is_k ? st.k_next : st.v_next;
-      while (next <= target) {
-        const int lit = next++;
-        uint32_t* tr = trace_begin<kTrace>(args, warp, st.trace_n, op.node, lit, r);
-        const uint32_t g = t.gbase + static_cast<uint32_t>(lit);
-        const int depth = is_k ? rg.kd : rg.vd;
-        const uint32_t s = g % depth, ph = (g / depth) & 1;
-        uint64_t* full = is_k ? &bar.k_full[s] : &bar.v_full[s];
-        uint64_t* empty = is_k ? &bar.k_empty[s] : &bar.v_empty[s];
-        uint8_t* dst = (is_k ? c.k_smem : c.v_smem) + s * kTileBytes;
-        const CUtensorMap* map = is_k ? tm.k : tm.v;
-        mbar_wait(empty, ph ^ 1);
-        trace_mark<kTrace>(tr, 4);
-        if (elect_one()) {
-          mbar_arrive_expect_tx(full, kTileBytes);
-          tma_load_3d(dst, map, full, 0, lit * kBlockK, t.bh, c.pol_kv);
-          tma_load_3d(dst + kHalfBytes, map, full, 64, lit * kBlockK, t.bh, c.pol_kv);
-        }
-        __syncwarp();
-        trace_mark<kTrace>(tr, 5);
-      }
-    }
-    return;
-  }
-  const int it = r - static_cast<int>(op.stage);
-  if (it < 0 || it >= N) return;
-  if (op.kind == TWFA_OP_EX && (op.flags & TWFA_OPF_FUSED)) return;  // done by MX_k
-  const uint32_t g = t.gbase + static_cast<uint32_t>(it);
-  const int k = op.tile;
-  uint32_t* tr = trace_begin<kTrace>(args, warp, st.trace_n, op.node, it, r);
-
-  if (op.kind == TWFA_OP_S) {
-    // MMA issue: every lane waits and computes the (warp-uniform)
-    // descriptors, so they live in uniform registers; one elected lane
-    // issues the tcgen05.mma chain and the commits
-    const uint32_t s = g % rg.kd;
-    if (it == 0) mbar_wait(&bar.q_full[k], t.tcount & 1);
-    if (g > 0 && !(op.flags & TWFA_OPF_INORDER))  // K landed; P_k(g-1) consumed by PV_k(g-1)
-      mbar_wait_all(&bar.k_full[s], (g / rg.kd) & 1, &bar.o_done[k], (g - 1) & 1);
-    else
-      mbar_wait(&bar.k_full[s], (g / rg.kd) & 1);
-    trace_mark<kTrace>(tr, 4);
-    tc_fence_after();
-    const uint32_t qa = smem_u32(c.q_smem + k * kTileBytes);
-    const uint32_t ka = smem_u32(c.k_smem + s * kTileBytes);
-    const uint32_t d_s = tmem + k * 128;
-    if (elect_one()) {
-#pragma unroll
-      for (int kk = 0; kk < kHeadDim / 16; ++kk) {
-        const uint32_t off = (kk >> 2) * kHalfBytes + (kk & 3) * 32;
-        mma_ss(d_s, sdesc_sw128(qa + off, 16, 1024), sdesc_sw128(ka + off, 16, 1024), kIdescS, kk > 0);
-      }
-      mma_commit(&bar.s_full[k]);
-      mma_commit(&bar.k_empty[s]);
-      if (it == N - 1) mma_commit(&bar.q_empty[k]);
-    }
-    __syncwarp();
-  } else if (op.kind == TWFA_OP_PV) {
-    const uint32_t s = g % rg.vd;
-    // P_k arrives in two halves (keys 0-63, 64-127): the first four
-    // K-steps of PV_k overlap the exponentials of the second half
-    mbar_wait_all(&bar.v_full[s], (g / rg.vd) & 1, &bar.p_half[k], g & 1, &bar.o_ready[k], g & 1);
-    trace_mark<kTrace>(tr, 4);
-    tc_fence_after();
-    const uint32_t va = smem_u32(c.v_smem + s * kTileBytes);
-    const uint32_t d_o = tmem + 256 + k * 128, a_p = tmem + k * 128;
-    const uint32_t acc0 = it > 0 ? 1u : 0u;
-    if (elect_one()) {
-#pragma unroll
-      for (int kk = 0; kk < kBlockK / 32; ++kk)  // V is MN-major: 16 keys = 16 rows of 128 B
-        mma_ts(d_o, a_p + kk * 8, sdesc_sw128(va + kk * 2048, kHalfBytes, 1024), kIdescPV, kk > 0 ? 1u : acc0);
-    }
-    __syncwarp();
-    mbar_wait(&bar.p_full[k], g & 1);
-    tc_fence_after();
-    if (elect_one()) {
-#pragma unroll
-      for (int kk = kBlockK / 32; kk < kBlockK / 16; ++kk)
-        mma_ts(d_o, a_p + kk * 8, sdesc_sw128(va + kk * 2048, kHalfBytes, 1024), kIdescPV, 1u);
-      mma_commit(&bar.o_done[k]);
-      mma_commit(&bar.v_empty[s]);
-    }
-    __syncwarp();
-  } else if (op.kind == TWFA_OP_CR) {
-    const uint32_t sb = g & 1;
-    mbar_wait(&bar.st_full[k][sb], (g >> 1) & 1);
-    const float alpha = g_sh.stats[k][sb][c.quad * 32 + lane];
-    warp_arrive(&bar.st_empty[k][sb]);
-    // with the rescale threshold most iterations keep the max: then O is
-    // not touched and the correction only forwards the handoff
-    if (it > 0 && !__all_sync(0xffffffffu, alpha == 1.f)) {
-      mbar_wait(&bar.o_done[k], (g - 1) & 1);
-      trace_mark<kTrace>(tr, 4);
-      tc_fence_after();
-#pragma unroll 1
-      for (int cc = 0; cc < 4; ++cc) {
-        uint32_t v[32];
-        const uint32_t addr = tmem + c.lane_off + 256 + k * 128 + cc * 32;
-        tmem_ld32(addr, v);
-        tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          const float2 o =
-              fmul2(make_float2(__uint_as_float(v[i]), __uint_as_float(v[i + 1])), make_float2(alpha, alpha));
-          v[i] = __float_as_uint(o.x);
-          v[i + 1] = __float_as_uint(o.y);
-        }
-        tmem_st32(addr, v);
-      }
-      tmem_st_wait();
-    }
-    tc_fence_before();
-    warp_arrive(&bar.o_ready[k]);
-  } else if (op.kind == TWFA_OP_MX || op.kind == TWFA_OP_EX) {
-    if constexpr (kHeavy) {
-      const uint32_t taddr = tmem + c.lane_off + k * 128;
-      const int row = t.q0 + k * kBlockQ + c.quad * 32 + lane;
-      const int limit = valid_keys(args, row, it * kBlockK);
-      const bool mask = !__all_sync(0xffffffffu, limit >= kBlockK);
-      uint32_t srow[128];
-      if (op.kind == TWFA_OP_MX) {
-        mbar_wait(&bar.s_full[k], g & 1);
-        trace_mark<kTrace>(tr, 4);
-        tc_fence_after();
-        load_row(taddr, srow);
-        if (mask) mask_row(srow, limit);
-        const float mx = row_max(srow);
-        const float m_old = rd(st.m_run, k);
-        const float m_cand = fmaxf(m_old, mx * c.scale_log2);
-        const float m_new = (m_cand - m_old > kRescaleLog2) ? m_cand : m_old;  // m_old = -inf -> m_cand
-        const float m_safe = m_new == -INFINITY ? 0.f : m_new;
-        wr(st.alpha, k, m_new == m_old ? 1.f : fast_exp2(m_old - m_safe));
-        wr(st.m_run, k, m_new);
-        const uint32_t sb = g & 1;
-        mbar_wait(&bar.st_empty[k][sb], ((g >> 1) & 1) ^ 1);
-        g_sh.stats[k][sb][c.quad * 32 + lane] = rd(st.alpha, k);
-        warp_arrive(&bar.st_full[k][sb]);
-        trace_mark<kTrace>(tr, 5);
-        if (!(op.flags & TWFA_OPF_FUSE_NEXT)) return;
-        // EX_k is this warp's next op: run it on the resident S row
-        tr = trace_begin<kTrace>(args, warp, st.trace_n, op.node + 1, it, r);
-        trace_mark<kTrace>(tr, 4);
-      } else {
-        // unfused EX (other ops run between MX_k and EX_k on this warp):
-        // re-read S; the running max and alpha of MX_k are in registers
-        trace_mark<kTrace>(tr, 4);
-        load_row(taddr, srow);
-        if (mask) mask_row(srow, limit);
-      }
-      const float m_run = rd(st.m_run, k);
-      const float m_safe = m_run == -INFINITY ? 0.f : m_run;
-      const float sum = mask ? exp_store_row<true>(srow, taddr, c.scale_log2, m_safe, &bar.p_half[k])
-                             : exp_store_row<false>(srow, taddr, c.scale_log2, m_safe, &bar.p_half[k]);
-      wr(st.l_run, k, rd(st.l_run, k) * rd(st.alpha, k) + sum);
-      tc_fence_before();
-      warp_arrive(&bar.p_full[k]);
-      if (it == N - 1) {
-        mbar_wait(&bar.l_empty[k], (t.tcount & 1) ^ 1);
-        g_sh.lbuf[k][0][c.quad * 32 + lane] = m_run;
-        g_sh.lbuf[k][1][c.quad * 32 + lane] = rd(st.l_run, k);
-        warp_arrive(&bar.l_full[k]);
-      }
-    }
-  }
-  trace_mark<kTrace>(tr, 5);
-}
-
-// Q sub-tiles of a new work tile (TMA warp, before its trip loop)
-__device__ __forceinline__ void load_q(const FaCtx& c, const WorkTile& t, int tiles, const Maps& tm) {
-  FaBarriers& bar = g_sh.bar;
-  for (int k = 0; k < tiles; ++k) {
-    mbar_wait(&bar.q_empty[k], (t.tcount & 1) ^ 1);
-    uint8_t* dst = c.q_smem + k * kTileBytes;
-    if (elect_one()) {
-      mbar_arrive_expect_tx(&bar.q_full[k], kTileBytes);
-      tma_load_3d(dst, tm.q, &bar.q_full[k], 0, t.q0 + k * kBlockQ, t.bh, c.pol_q);
-      tma_load_3d(dst + kHalfBytes, tm.q, &bar.q_full[k], 64, t.q0 + k * kBlockQ, t.bh, c.pol_q);
-    }
-    __syncwarp();
-  }
-}
-
-// Epilogue of sub-tile k on its correction warpgroup: O / l -> bf16 -> global,
-// LSE (the accumulator is final after the last PV_k).
-__device__ __forceinline__ void epilogue(const FaCtx& c, const WorkTile& t, int k, const FaArgs& args) {
-  FaBarriers& bar = g_sh.bar;
-  const uint32_t lane = c.lane;
-  const uint32_t g_last = t.gbase + static_cast<uint32_t>(t.N - 1);
-  mbar_wait(&bar.o_done[k], g_last & 1);
-  mbar_wait(&bar.l_full[k], t.tcount & 1);
-  const float m = g_sh.lbuf[k][0][c.quad * 32 + lane];
-  const float l = g_sh.lbuf[k][1][c.quad * 32 + lane];
-  warp_arrive(&bar.l_empty[k]);
-  tc_fence_after();
-  const int row = t.q0 + k * kBlockQ + c.quad * 32 + lane;
-  const float inv = l > 0.f ? 1.f / l : 0.f;
-  __nv_bfloat16* orow = args.o + (static_cast<int64_t>(t.bh) * c.S + row) * kHeadDim;
-#pragma unroll 1
-  for (int cc = 0; cc < 4; ++cc) {
-    uint32_t v[32];
-    tmem_ld32(c.tmem + c.lane_off + 256 + k * 128 + cc * 32, v);
-    tmem_ld_wait();
-    if (row < c.S) {
-      uint4* dst = reinterpret_cast<uint4*>(orow + cc * 32);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        uint4 w;
-        w.x = pack_bf16(__uint_as_float(v[8 * i + 0]) * inv, __uint_as_float(v[8 * i + 1]) * inv);
-        w.y = pack_bf16(__uint_as_float(v[8 * i + 2]) * inv, __uint_as_float(v[8 * i + 3]) * inv);
-        w.z = pack_bf16(__uint_as_float(v[8 * i + 4]) * inv, __uint_as_float(v[8 * i + 5]) * inv);
-        w.w = pack_bf16(__uint_as_float(v[8 * i + 6]) * inv, __uint_as_float(v[8 * i + 7]) * inv);
-        dst[i] = w;
-      }
-    }
-  }
-  if (args.lse != nullptr && row < c.S)
-    args.lse[static_cast<int64_t>(t.bh) * c.S + row] = (m + __log2f(l)) * 0.69314718055994531f;
-  tc_fence_before();
-}
-
-// Work-tile loop of one warp. `trip` runs the warp's trip program for trip r.
-template <class Trip>
-__device__ __forceinline__ void work_loop(const FaCtx& c, const FaArgs& args, const Maps& tm, int tiles, int max_stage,
-                                          bool is_load_warp, const int* cr_warp, WarpState& st, Trip&& trip) {
-  uint32_t gbase = 0, tcount = 0;
-  for (int work = blockIdx.x; work < c.num_work; work += gridDim.x, ++tcount) {
-    const WorkTile t = work_tile(c, args, work, gbase, tcount);
-    if (is_load_warp) load_q(c, t, tiles, tm);
-#pragma unroll
-    for (int k = 0; k < TWFA_MAX_TILES; ++k) {
-      st.m_run[k] = -INFINITY;
-      st.l_run[k] = 0.f;
-      st.alpha[k] = 1.f;
-    }
-    st.k_next = st.v_next = 0;
-    const int trips = t.N + max_stage;
-    for (int r = 0; r < trips; ++r) trip(r, t);
-    for (int k = 0; k < tiles; ++k)
-      if (static_cast<int>(c.warp & ~3u) == cr_warp[k]) epilogue(c, t, k, args);
-    gbase += static_cast<uint32_t>(t.N);
-  }
-}
-
-// Shared prologue of both kernels: smem carve-up, barriers, TMEM allocation.
-__device__ __forceinline__ FaCtx fa_setup(int tiles, int kd, int vd, int load_warp, const FaArgs& args,
-                                          const Maps& tm, uint8_t* smem_raw) {
-  // 1 KiB alignment of the tile buffers (SW128 atoms) by offset arithmetic on
-  // the shared window address, keeping the pointer in the shared space
-  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  FaCtx c;
-  c.q_smem = smem;
-  c.k_smem = c.q_smem + tiles * kTileBytes;
-  c.v_smem = c.k_smem + kd * kTileBytes;
-  FaBarriers& bar = g_sh.bar;
-  c.warp = warp_id();
-  c.lane = lane_id();
-  if (threadIdx.x == 0) {
-    for (int k = 0; k < tiles; ++k) {
-      mbar_init(&bar.q_full[k], 1);
-      mbar_init(&bar.q_empty[k], 1);
-      mbar_init(&bar.s_full[k], 1);
-      mbar_init(&bar.p_full[k], 4);  // warp arrivals of a warpgroup
-      mbar_init(&bar.p_half[k], 4);
-      mbar_init(&bar.o_ready[k], 4);
-      mbar_init(&bar.o_done[k], 1);
-      for (int j = 0; j < 2; ++j) {
-        mbar_init(&bar.st_full[k][j], 4);
-        mbar_init(&bar.st_empty[k][j], 4);
-      }
-      mbar_init(&bar.l_full[k], 4);
-      mbar_init(&bar.l_empty[k], 4);
-    }
-    for (int s = 0; s < kd; ++s) {
-      mbar_init(&bar.k_full[s], 1);
-      mbar_init(&bar.k_empty[s], tiles);
-    }
-    for (int s = 0; s < vd; ++s) {
-      mbar_init(&bar.v_full[s], 1);
-      mbar_init(&bar.v_empty[s], tiles);
-    }
-    fence_mbar_init();
-  }
-  if (c.warp == static_cast<uint32_t>(load_warp) && c.lane == 0) {
-    tma_prefetch_desc(tm.q);
-    tma_prefetch_desc(tm.k);
-    tma_prefetch_desc(tm.v);
-  }
-  if (c.warp == 0) tmem_alloc<512>(&bar.tmem_base);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  // the CTA owns all 512 columns (one CTA per SM): the allocation starts at
-  // column 0, lane 0, so the base is the compile-time constant 0
-  if (bar.tmem_base != 0) __trap();
-  c.tmem = 0;
-  c.scale_log2 = args.scale_log2;
-  c.S = args.S;
-  c.BH = args.B * args.H;
-  c.q_blocks = (c.S + 2 * kBlockQ - 1) / (2 * kBlockQ);
-  c.num_work = c.BH * c.q_blocks;
-  c.quad = c.warp & 3u;               // TMEM lane quadrant of this warp
-  c.lane_off = (c.quad * 32u) << 16;  // TMEM address lane field
-  c.pol_q = policy_evict_first();
-  c.pol_kv = policy_evict_last();
-  return c;
-}
-
-__device__ __forceinline__ void fa_teardown(const FaCtx& c) {
-  tc_fence_before();
-  __syncthreads();
-  if (c.warp == 0) {
-    tc_fence_after();
-    tmem_dealloc<512>(c.tmem);
-  }
-}
-
-template <bool kHeavy>
-__device__ __forceinline__ void set_register_class(int heavy_wgs) {
-  if constexpr (kHeavy) {
-    if (heavy_wgs == 2) setmaxnreg_inc<192>(); else setmaxnreg_inc<232>();
-  } else {
-    if (heavy_wgs == 2) setmaxnreg_dec<64>(); else setmaxnreg_dec<80>();
-  }
-}
-
-// ---------------------------------------------------------------- interpreter
-template <bool kHeavy, bool kTrace>
-__device__ __forceinline__ void run_interp(const FaCtx& c, const Maps& tm, const FaArgs& args, int tiles,
-                                           int max_stage, int load_warp, const int* cr_warp, const Rings rg) {
-  WarpState st;
-  st.trace_n = 0;
-  int plen = 0;
-  while (plen < TWFA_MAX_NODES && g_sh.prog_len[c.warp] > plen) ++plen;
-  work_loop(c, args, tm, tiles, max_stage, !kHeavy && c.warp == static_cast<uint32_t>(load_warp), cr_warp, st,
-            [&](int r, const WorkTile& t) {
-              for (int j = 0; j < plen; ++j) exec_op<kHeavy, kTrace>(g_sh.prog[c.warp][j], r, c, t, st, rg, tm, args);
-            });
-}
-
-template <bool kTrace>
-__global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
-    fa_fwd_interp(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                  const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ TwfaDevicePlan plan,
-                  const __grid_constant__ FaArgs args) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  const Maps tm{&tm_q, &tm_k, &tm_v};
-  for (int i = threadIdx.x; i < TWFA_MAX_WARPS * TWFA_MAX_NODES; i += blockDim.x) {
-    const int w = i / TWFA_MAX_NODES, j = i % TWFA_MAX_NODES;
-    if (j < plan.prog_len[w]) g_sh.prog[w][j] = plan.ops[plan.prog[w][j]];
-    if (j == 0) g_sh.prog_len[w] = plan.prog_len[w];
-  }
-  const FaCtx c = fa_setup(plan.num_tiles, plan.k_depth, plan.v_depth, plan.load_warp, args, tm, smem_raw);
-  const Rings rg{plan.k_depth, plan.v_depth, plan.k_prefetch, plan.v_prefetch};
-  const bool heavy = (plan.heavy_wg_mask >> (c.warp >> 2)) & 1;
-  const int heavy_wgs = __popc(plan.heavy_wg_mask);
-  if (heavy) {
-    set_register_class<true>(heavy_wgs);
-    run_interp<true, kTrace>(c, tm, args, plan.num_tiles, plan.max_stage, plan.load_warp, plan.cr_warp, rg);
-  } else {
-    set_register_class<false>(heavy_wgs);
-    run_interp<false, kTrace>(c, tm, args, plan.num_tiles, plan.max_stage, plan.load_warp, plan.cr_warp, rg);
-  }
-  fa_teardown(c);
-}
-
-// ---------------------------------------------------------------- specialized
-// gen::PlanOf<I>::value is a host constexpr object: device code only reads
-// its scalar fields in constant expressions (never binds a reference to it).
-#define TWFA_PLAN(I) (gen::PlanOf<I>::value)
-
-template <int I, int W, int J>
-__device__ __forceinline__ TwfaPlanOp spec_op() {
-  constexpr int v = TWFA_PLAN(I).prog[W][J];
-  TwfaPlanOp op{};
-  op.node = TWFA_PLAN(I).ops[v].node;
-  op.kind = TWFA_PLAN(I).ops[v].kind;
-  op.tile = TWFA_PLAN(I).ops[v].tile;
-  op.stage = TWFA_PLAN(I).ops[v].stage;
-  op.slot = TWFA_PLAN(I).ops[v].slot;
-  op.warp_start = TWFA_PLAN(I).ops[v].warp_start;
-  op.warp_count = TWFA_PLAN(I).ops[v].warp_count;
-  op.order = TWFA_PLAN(I).ops[v].order;
-  op.flags = TWFA_PLAN(I).ops[v].flags;
-  return op;
-}
-
-// the interpreted roles read their trip programs from shared memory
-template <int I, int W, int... J>
-__device__ __forceinline__ void fill_warp_prog(int j, std::integer_sequence<int, J...>) {
-  ((j == J ? (void)(g_sh.prog[W][J] = spec_op<I, W, J>()) : void()), ...);
-  if (j == 0) g_sh.prog_len[W] = TWFA_PLAN(I).prog_len[W];
-}
-template <int I, int... W>
-__device__ __forceinline__ void fill_progs(int w, int j, std::integer_sequence<int, W...>) {
-  ((w == W ? fill_warp_prog<I, W>(j, std::make_integer_sequence<int, TWFA_PLAN(I).prog_len[W]>{}) : void()), ...);
-}
-
-template <int I, int W, bool kTrace, int... J>
-__device__ __forceinline__ void spec_trip(int r, const FaCtx& c, const WorkTile& t, WarpState& st, const Maps& tm,
-                                          const FaArgs& args, std::integer_sequence<int, J...>) {
-  constexpr bool kHeavy = (TWFA_PLAN(I).heavy_wg_mask >> (W / 4)) & 1;
-  constexpr Rings rg{TWFA_PLAN(I).k_depth, TWFA_PLAN(I).v_depth, TWFA_PLAN(I).k_prefetch, TWFA_PLAN(I).v_prefetch};
-  (exec_op<kHeavy, kTrace>(spec_op<I, W, J>(), r, c, t, st, rg, tm, args), ...);
-}
-
-template <int I, int W, bool kTrace>
-__device__ __forceinline__ void run_spec(const FaCtx& c, const Maps& tm, const FaArgs& args) {
-  constexpr bool kHeavy = (TWFA_PLAN(I).heavy_wg_mask >> (W / 4)) & 1;
-  constexpr int plen = TWFA_PLAN(I).prog_len[W];
-  constexpr bool kLoad = !kHeavy && W == TWFA_PLAN(I).load_warp;
-  constexpr int cr_warp[TWFA_MAX_TILES] = {TWFA_PLAN(I).cr_warp[0], TWFA_PLAN(I).cr_warp[1]};
-  WarpState st;
-  st.trace_n = 0;
-  work_loop(c, args, tm, TWFA_PLAN(I).num_tiles, TWFA_PLAN(I).max_stage, kLoad, cr_warp, st,
-            [&](int r, const WorkTile& t) {
-              spec_trip<I, W, kTrace>(r, c, t, st, tm, args, std::make_integer_sequence<int, plen>{});
-            });
-}
-
-// Light roles (TMA, MMA issue, correction) run their specialized trip
-// program, one instantiation per distinct role; softmax warpgroups run the
-// runtime interpreter over the same plan (a single shared copy of the large
-// MX/EX bodies keeps the kernel within the instruction cache).
-template <int I, bool kTrace, int... W>
-__device__ __forceinline__ void spec_dispatch_light(const FaCtx& c, const Maps& tm, const FaArgs& args,
-                                                    std::integer_sequence<int, W...>) {
-  int role = -1;
-  ((c.warp == static_cast<uint32_t>(W) ? (void)(role = gen::PlanOf<I>::role[W]) : void()), ...);
-  ((!((TWFA_PLAN(I).heavy_wg_mask >> (W / 4)) & 1) && gen::PlanOf<I>::role[W] == W && role == W
-        ? run_spec<I, W, kTrace>(c, tm, args)
-        : void()),
-   ...);
-}
-
-template <int I, bool kTrace>
-__global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
-    fa_fwd_spec(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ FaArgs args) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  const Maps tm{&tm_q, &tm_k, &tm_v};
-  for (int i = threadIdx.x; i < TWFA_MAX_WARPS * TWFA_MAX_NODES; i += blockDim.x)
-    fill_progs<I>(i / TWFA_MAX_NODES, i % TWFA_MAX_NODES, std::make_integer_sequence<int, TWFA_MAX_WARPS>{});
-  constexpr int cr_warp[TWFA_MAX_TILES] = {TWFA_PLAN(I).cr_warp[0], TWFA_PLAN(I).cr_warp[1]};
-  const FaCtx c = fa_setup(TWFA_PLAN(I).num_tiles, TWFA_PLAN(I).k_depth, TWFA_PLAN(I).v_depth,
-                           TWFA_PLAN(I).load_warp, args, tm, smem_raw);
-  // the register class is per warpgroup; the warp roles of each class are
-  // dispatched inside its branch so ptxas allocates them under that budget
-  constexpr int mask = TWFA_PLAN(I).heavy_wg_mask;
-  const int heavy_wgs = __popc(mask);
-  constexpr int nw = TWFA_PLAN(I).num_warps;
-  if ((mask >> (c.warp >> 2)) & 1) {
-    set_register_class<true>(heavy_wgs);
-    run_interp<true, kTrace>(c, tm, args, TWFA_PLAN(I).num_tiles, TWFA_PLAN(I).max_stage, TWFA_PLAN(I).load_warp,
-                             cr_warp, Rings{TWFA_PLAN(I).k_depth, TWFA_PLAN(I).v_depth, TWFA_PLAN(I).k_prefetch,
-                                            TWFA_PLAN(I).v_prefetch});
-  } else {
-    set_register_class<false>(heavy_wgs);
-    spec_dispatch_light<I, kTrace>(c, tm, args, std::make_integer_sequence<int, nw>{});
-  }
-  fa_teardown(c);
-}
-
-bool same_plan(const TwfaDevicePlan& a, const TwfaDevicePlan& b) {
-  if (a.family != b.family || a.ii != b.ii || a.max_stage != b.max_stage || a.num_nodes != b.num_nodes ||
-      a.num_warps != b.num_warps || a.num_tiles != b.num_tiles || a.k_depth != b.k_depth || a.v_depth != b.v_depth ||
-      a.load_warp != b.load_warp || a.k_prefetch != b.k_prefetch || a.v_prefetch != b.v_prefetch ||
-      a.heavy_wg_mask != b.heavy_wg_mask)
-    return false;
-  for (int k = 0; k < TWFA_MAX_TILES; ++k)
-    if (a.cr_warp[k] != b.cr_warp[k] || a.sm_warp[k] != b.sm_warp[k]) return false;
-  for (int v = 0; v < a.num_nodes; ++v) {
-    const TwfaPlanOp &x = a.ops[v], &y = b.ops[v];
-    if (x.node != y.node || x.kind != y.kind || x.tile != y.tile || x.stage != y.stage || x.slot != y.slot ||
-        x.warp_start != y.warp_start || x.warp_count != y.warp_count || x.flags != y.flags)
-      return false;
-  }
-  for (int w = 0; w < TWFA_MAX_WARPS; ++w) {
-    if (a.prog_len[w] != b.prog_len[w]) return false;
-    for (int j = 0; j < a.prog_len[w]; ++j)
-      if (a.prog[w][j] != b.prog[w][j]) return false;
-  }
-  return true;
-}
-
-template <class Kernel, class... Args>
-cudaError_t launch(Kernel kernel, size_t smem, int grid, int threads, cudaStream_t stream, Args... args) {
-  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
-  kernel<<<grid, threads, smem, stream>>>(args...);
-  return cudaGetLastError();
-}
-
-}  // namespace
 
 size_t fa_fwd_smem_bytes(const TwfaDevicePlan& plan) {
   // dynamic part only: tile buffers (+ alignment slack); FaShared is static
@@ -789,10 +27,8 @@ cudaError_t fa_fwd_launch(const CUtensorMap& tq, const CUtensorMap& tk, const CU
   const int threads = plan.num_warps * 32;
   const bool trace = args.trace != nullptr;
   if (allow_specialized) {
-#define TWFA_LAUNCH(id)                                                                          \
-  if (same_plan(plan, gen::PlanOf<id>::value))                                                   \
-    return trace ? launch(fa_fwd_spec<id, true>, smem, grid, threads, stream, tq, tk, tv, args) \
-                 : launch(fa_fwd_spec<id, false>, smem, grid, threads, stream, tq, tk, tv, args);
+#define TWFA_LAUNCH(id) \
+  if (same_plan(plan, gen::PlanOf<id>::value)) return gen::launch_spec_##id(tq, tk, tv, args, smem, grid, threads, stream, trace);
     TWFA_SPECIALIZED_PLANS(TWFA_LAUNCH)
 #undef TWFA_LAUNCH
   }

@@ -117,6 +117,28 @@ int main(int argc, char** argv) {
     std::fprintf(stderr, "error: %s\n", e.what());
     return 1;
   }
+  // one translation unit per specialization (compiled in parallel) and the
+  // declarations of their launchers
+  const std::string inc_path = argv[1];
+  const std::string dir = inc_path.substr(0, inc_path.rfind('/') + 1);
+  std::ofstream decl(dir + "fa_spec_launch.h");
+  decl << "// GENERATED by twfa-gen: launchers of the specialized FA kernels.\n#pragma once\n"
+          "#include <cuda.h>\n#include <cuda_runtime.h>\n#include <fa_fwd.h>\n\nnamespace twfa {\nnamespace gen {\n";
+  for (int i = 0; i < id; ++i) {
+    decl << "cudaError_t launch_spec_" << i
+         << "(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const FaArgs& args, size_t smem,\n"
+            "                          int grid, int threads, cudaStream_t stream, bool trace);\n";
+    std::ofstream tu(dir + "fa_spec_" + std::to_string(i) + ".cu");
+    tu << "// GENERATED by twfa-gen: kernel specialization " << i << " (gen::PlanOf<" << i << ">).\n"
+          "#include <fa_fwd_kernel.cuh>\n#include <gen/fa_spec_launch.h>\n\nnamespace twfa {\nnamespace gen {\n"
+          "cudaError_t launch_spec_" << i
+       << "(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const FaArgs& args, size_t smem,\n"
+          "                          int grid, int threads, cudaStream_t stream, bool trace) {\n"
+          "  return trace ? launch(fa_fwd_spec<" << i << ", true>, smem, grid, threads, stream, tq, tk, tv, args)\n"
+          "               : launch(fa_fwd_spec<" << i << ", false>, smem, grid, threads, stream, tq, tk, tv, args);\n"
+          "}\n}  // namespace gen\n}  // namespace twfa\n";
+  }
+  decl << "}  // namespace gen\n}  // namespace twfa\n";
   std::ofstream out(argv[1]);
   out << "// GENERATED by twfa-gen (csrc/gen_main.cpp) from the committed solution JSON.\n"
          "// Do not edit: rebuilt by paper_2512_18134_b200/_build.py.\n"

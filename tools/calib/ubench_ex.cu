@@ -65,7 +65,13 @@ __global__ void __launch_bounds__(256, 1) k(long long* cyc, float* out, int nwg)
   __syncthreads();
   float acc = 0;
   long long t_mx = 0, t_ex = 0;
-  if (wg < (uint32_t)nwg) {
+  if (nwg == 3 && wg == 1) {  // interference: the other tile's MX (TMEM row loads + max) in a loop
+    for (int it = 0; it < 200; ++it) {
+      uint32_t s[128];
+      load_row(taddr, s);
+      acc += row_max(s);
+    }
+  } else if (wg < (uint32_t)(nwg == 3 ? 1 : nwg)) {
     for (int it = 0; it < 64; ++it) {
       long long c0 = clock64();
       uint32_t s[128];
@@ -89,7 +95,7 @@ __global__ void __launch_bounds__(256, 1) k(long long* cyc, float* out, int nwg)
 int main() {
   long long* cyc; float* out;
   cudaMalloc(&cyc, 64); cudaMalloc(&out, 4096 * 4);
-  for (int nwg : {1, 2}) {
+  for (int nwg : {1, 2, 3}) {
     long long h[2];
     k<<<1, 256>>>(cyc, out, nwg); k<<<1, 256>>>(cyc, out, nwg);
     cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost);

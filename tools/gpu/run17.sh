@@ -1,0 +1,1 @@
+REPS=3 SCHEDS=fa_fwd timeout 900 python tools/variants.py paper_2512_18134_b200/variants/nosplits.so paper_2512_18134_b200/variants/splits.so 2>&1
