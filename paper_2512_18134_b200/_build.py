@@ -33,7 +33,11 @@ def specializations():
         for f in sorted(os.listdir(exp)):
             if f.endswith(".solution.json"):
                 name = f[: -len(".solution.json")]
-                out.append((name, os.path.join(SCHED, "fa_fwd.json"), os.path.join(exp, f)))
+                # hand-edited assignments (not solver output); <name>.problem names
+                # the problem they apply to (default fa_fwd)
+                pf = os.path.join(exp, name + ".problem")
+                prob = open(pf).read().strip() if os.path.exists(pf) else "fa_fwd"
+                out.append((name, os.path.join(SCHED, prob + ".json"), os.path.join(exp, f)))
     only = os.environ.get("TWFA_SPECIALIZE")  # comma list: limit (experiment builds)
     if only is not None:
         keep = set(only.split(",")) - {""}

@@ -121,10 +121,11 @@ int fa_fwd_impl(const twfa_plan* plan, const void* q, const void* k, const void*
   const cuuint64_t bh = static_cast<cuuint64_t>(B) * H;
   const cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(S), bh};
   const cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 2, static_cast<cuuint64_t>(S) * D * 2};
-  const cuuint32_t box[3] = {64, 128, 1};
-  const CUtensorMap tq = make_map(q, 3, dims, strides, box);
-  const CUtensorMap tk = make_map(k, 3, dims, strides, box);
-  const CUtensorMap tv = make_map(v, 3, dims, strides, box);
+  const cuuint32_t box_q[3] = {64, 128, 1};
+  const cuuint32_t box_kv[3] = {64, static_cast<cuuint32_t>(p.kv_tile), 1};
+  const CUtensorMap tq = make_map(q, 3, dims, strides, box_q);
+  const CUtensorMap tk = make_map(k, 3, dims, strides, box_kv);
+  const CUtensorMap tv = make_map(v, 3, dims, strides, box_kv);
   twfa::FaArgs a{};
   a.o = static_cast<__nv_bfloat16*>(o);
   a.lse = lse;

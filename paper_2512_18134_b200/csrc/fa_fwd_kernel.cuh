@@ -53,10 +53,20 @@ namespace twfa {
 namespace {
 
 constexpr int kBlockQ = 128;  // rows per Q sub-tile (= TMEM lanes)
-constexpr int kBlockK = 128;  // keys per K/V tile
 constexpr int kHeadDim = 128;
-constexpr uint32_t kTileBytes = kBlockQ * kHeadDim * 2;  // 32 KiB, two 16 KiB SW128 column halves
+constexpr uint32_t kTileBytes = kBlockQ * kHeadDim * 2;  // Q tile: 32 KiB, two 16 KiB SW128 column halves
 constexpr uint32_t kHalfBytes = kTileBytes / 2;
+
+// K/V tile of KV keys (128, or 64 when S is double-buffered in tensor memory:
+// the plan's S ring depth is 128 / KV). S_k's buffer b of iteration g is
+// g % depth at columns [128k + b*KV, ...); P_k (bf16) is aliased over it.
+template <int KV>
+struct Kv {
+  static constexpr int depth = 128 / KV;                        // S ring depth
+  static constexpr uint32_t tile = KV * kHeadDim * 2;           // K or V tile bytes
+  static constexpr uint32_t half = tile / 2;                    // one 64-column SW128 half
+  static constexpr uint32_t idesc_s = idesc_bf16_f32(128, KV, 0);  // K-major Q, K-major K
+};
 constexpr int kMaxRing = 4;
 #ifndef TWFA_POLY_EVERY
 #define TWFA_POLY_EVERY 1000  // measured: MUFU-only is fastest while the loop is latency-bound
@@ -67,22 +77,16 @@ constexpr int kPolyEvery = TWFA_POLY_EVERY;  // 1 in kPolyEvery exp2 pairs on th
 // iterations need no O correction. The final O / l is unchanged in exact
 // arithmetic (m cancels); bf16 P and fp32 l stay far from overflow.
 constexpr float kRescaleLog2 = 8.0f;
-#ifndef TWFA_SPLIT_S
-#define TWFA_SPLIT_S 0  // measured slower on B200 (C3: 1146 vs 1200 TF/s)
-#endif
-// S_k is issued as two N = 64 halves (keys 0-63, 64-127) committed to
-// separate barriers: MX_k loads and reduces the first half while the tensor
-// core computes the second.
-constexpr bool kSplitS = TWFA_SPLIT_S != 0;
-constexpr uint32_t kIdescS = idesc_bf16_f32(128, kSplitS ? kBlockK / 2 : kBlockK, 0);  // K-major Q, K-major K
 constexpr uint32_t kIdescPV = idesc_bf16_f32(128, kHeadDim, 1);  // TMEM P, MN-major V
 
 struct __align__(8) FaBarriers {
   uint64_t q_full[TWFA_MAX_TILES], q_empty[TWFA_MAX_TILES];
   uint64_t k_full[kMaxRing], k_empty[kMaxRing];
   uint64_t v_full[kMaxRing], v_empty[kMaxRing];
-  uint64_t s_full[TWFA_MAX_TILES], s_half[TWFA_MAX_TILES], p_full[TWFA_MAX_TILES], p_half[TWFA_MAX_TILES];
-  uint64_t o_ready[TWFA_MAX_TILES], o_done[TWFA_MAX_TILES];
+  // per S buffer (ring depth <= 2): a phase-parity barrier may only run one
+  // phase ahead of its waiters, which the per-buffer split guarantees
+  uint64_t s_full[TWFA_MAX_TILES][2], p_full[TWFA_MAX_TILES][2], p_half[TWFA_MAX_TILES][2];
+  uint64_t o_ready[TWFA_MAX_TILES][2], o_done[TWFA_MAX_TILES][2];
   uint64_t st_full[TWFA_MAX_TILES][2], st_empty[TWFA_MAX_TILES][2];
   uint64_t l_full[TWFA_MAX_TILES], l_empty[TWFA_MAX_TILES];
   uint32_t tmem_base;
@@ -126,56 +130,32 @@ __device__ __forceinline__ void trace_mark(uint32_t* e, int field) {
 }
 
 // ---------------------------------------------------------------- softmax pieces
-// all 128 scores of this thread's TMEM lane, one wait
-__device__ __forceinline__ void load_row(uint32_t taddr, uint32_t (&s)[128]) {
-  tmem_ld32(taddr + 0, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
-  tmem_ld32(taddr + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
-  tmem_ld32(taddr + 64, *reinterpret_cast<uint32_t(*)[32]>(&s[64]));
-  tmem_ld32(taddr + 96, *reinterpret_cast<uint32_t(*)[32]>(&s[96]));
+// all N scores of this thread's TMEM lane, one wait
+template <int N>
+__device__ __forceinline__ void load_row(uint32_t taddr, uint32_t (&s)[N]) {
+#pragma unroll
+  for (int c = 0; c < N / 32; ++c) tmem_ld32(taddr + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&s[c * 32]));
   tmem_ld_wait();
 }
 
-__device__ __forceinline__ void mask_row(uint32_t (&s)[128], int limit) {
+template <int N>
+__device__ __forceinline__ void mask_row(uint32_t (&s)[N], int limit) {
 #pragma unroll
-  for (int i = 0; i < 128; ++i)
+  for (int i = 0; i < N; ++i)
     if (i >= limit) s[i] = __float_as_uint(-INFINITY);
 }
 
-// one 64-column half of the row (columns c0 .. c0 + 63)
-__device__ __forceinline__ void load_half(uint32_t taddr, uint32_t (&s)[128], int c0) {
-  tmem_ld32(taddr + c0, *reinterpret_cast<uint32_t(*)[32]>(&s[c0]));
-  tmem_ld32(taddr + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[c0 + 32]));
-  tmem_ld_wait();
-}
-__device__ __forceinline__ void mask_half(uint32_t (&s)[128], int limit, int c0) {
-#pragma unroll
-  for (int i = 0; i < 64; ++i)
-    if (c0 + i >= limit) s[c0 + i] = __float_as_uint(-INFINITY);
-}
-__device__ __forceinline__ float half_max(const uint32_t (&s)[128], int c0) {
-  float a[4] = {__uint_as_float(s[c0]), __uint_as_float(s[c0 + 1]), __uint_as_float(s[c0 + 2]),
-                __uint_as_float(s[c0 + 3])};
-#pragma unroll
-  for (int i = 4; i < 60; i += 8) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-      a[j] = fmax3(a[j], __uint_as_float(s[c0 + i + 2 * j]), __uint_as_float(s[c0 + i + 2 * j + 1]));
-  }
-  a[0] = fmax3(a[0], __uint_as_float(s[c0 + 60]), __uint_as_float(s[c0 + 61]));
-  a[1] = fmax3(a[1], __uint_as_float(s[c0 + 62]), __uint_as_float(s[c0 + 63]));
-  return fmax3(a[0], a[1], fmaxf(a[2], a[3]));
-}
-
 // FMNMX3: three-operand max (sm_100), four independent chains
-__device__ __forceinline__ float row_max(const uint32_t (&s)[128]) {
+template <int N>
+__device__ __forceinline__ float row_max(const uint32_t (&s)[N]) {
   float a[4] = {__uint_as_float(s[0]), __uint_as_float(s[1]), __uint_as_float(s[2]), __uint_as_float(s[3])};
 #pragma unroll
-  for (int i = 4; i < 124; i += 8) {
+  for (int i = 4; i < N - 4; i += 8) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) a[j] = fmax3(a[j], __uint_as_float(s[i + 2 * j]), __uint_as_float(s[i + 2 * j + 1]));
   }
-  a[0] = fmax3(a[0], __uint_as_float(s[124]), __uint_as_float(s[125]));
-  a[1] = fmax3(a[1], __uint_as_float(s[126]), __uint_as_float(s[127]));
+  a[0] = fmax3(a[0], __uint_as_float(s[N - 4]), __uint_as_float(s[N - 3]));
+  a[1] = fmax3(a[1], __uint_as_float(s[N - 2]), __uint_as_float(s[N - 1]));
   return fmax3(a[0], a[1], fmaxf(a[2], a[3]));
 }
 
@@ -185,14 +165,14 @@ __device__ __forceinline__ float row_max(const uint32_t (&s)[128]) {
 // over the first 64 columns of the S tile. The first half of P (keys 0-63)
 // is released to PV_k on `half_bar` before the second half is computed.
 // Returns the row sum.
-template <bool kMask>
-__device__ __forceinline__ float exp_store_row(const uint32_t (&s)[128], uint32_t taddr, float sl, float m,
+template <int N, bool kMask>
+__device__ __forceinline__ float exp_store_row(const uint32_t (&s)[N], uint32_t taddr, float sl, float m,
                                                uint64_t* half_bar) {
   const float2 sl2 = make_float2(sl, sl);
   const float2 nm2 = make_float2(-m, -m);
   float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
+  for (int c = 0; c < N / 32; ++c) {
     uint32_t pk[16];
 #pragma unroll
     for (int i = 0; i < 32; i += 2) {
@@ -209,9 +189,9 @@ __device__ __forceinline__ float exp_store_row(const uint32_t (&s)[128], uint32_
       acc[(i >> 1) & 1] = fadd2(acc[(i >> 1) & 1], p);
       pk[i >> 1] = pack_bf16(p.x, p.y);
     }
-    if (c == 2) {
-      // keys 0-63 of P (chunks 0, 1) are in tensor memory: release the first
-      // half of PV. The store wait is placed after chunk 2's exponentials so
+    if (c == N / 64) {
+      // the first half of P is in tensor memory: release the first half of
+      // PV. The store wait is placed after the next chunk's exponentials so
       // the MUFU stream does not drain behind it.
       tmem_st_wait();
       tc_fence_before();
@@ -242,6 +222,7 @@ struct WorkTile {
   uint32_t tcount;  // work tiles done by this CTA (Q / LSE buffer phases)
 };
 
+template <int KV>
 __device__ __forceinline__ WorkTile work_tile(const FaCtx& c, const FaArgs& args, int work, uint32_t gbase,
                                               uint32_t tcount) {
   WorkTile t;
@@ -255,7 +236,7 @@ __device__ __forceinline__ WorkTile work_tile(const FaCtx& c, const FaArgs& args
   }
   t.q0 = qb * 2 * kBlockQ;
   const int kv_end = args.causal ? min(c.S, t.q0 + 2 * kBlockQ) : c.S;
-  t.N = (kv_end + kBlockK - 1) / kBlockK;
+  t.N = (kv_end + KV - 1) / KV;
   t.gbase = gbase;
   t.tcount = tcount;
   return t;
@@ -263,9 +244,10 @@ __device__ __forceinline__ WorkTile work_tile(const FaCtx& c, const FaArgs& args
 
 // Number of leading keys of this K/V tile that row `row` may attend to
 // (the rest are past the sequence end or above the causal diagonal).
+template <int KV>
 __device__ __forceinline__ int valid_keys(const FaArgs& a, int row, int key0) {
   const int end = a.causal ? min(a.S, row + 1) : a.S;
-  return max(0, min(kBlockK, end - key0));
+  return max(0, min(KV, end - key0));
 }
 
 // running per-warp state
@@ -297,13 +279,14 @@ struct Maps {
 // ---------------------------------------------------------------- op bodies
 // One op of the trip program on this warp, trip r. Shared by both kernels:
 // with a compile-time `op` and `rg` every branch below folds.
-template <bool kHeavy, bool kTrace>
+template <int KV, bool kHeavy, bool kTrace>
 __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const FaCtx& c, const WorkTile& t,
                                         WarpState& st, const Rings rg, const Maps& tm, const FaArgs& args) {
   FaBarriers& bar = g_sh.bar;
   const uint32_t warp = c.warp, lane = c.lane;
   const uint32_t tmem = c.tmem;
   const int N = t.N;
+  using G = Kv<KV>;
 
   if (op.kind == TWFA_OP_LDK || op.kind == TWFA_OP_LDV) {
     if constexpr (!kHeavy) {
@@ -321,14 +304,14 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
         const uint32_t s = g % depth, ph = (g / depth) & 1;
         uint64_t* full = is_k ? &bar.k_full[s] : &bar.v_full[s];
         uint64_t* empty = is_k ? &bar.k_empty[s] : &bar.v_empty[s];
-        uint8_t* dst = (is_k ? c.k_smem : c.v_smem) + s * kTileBytes;
+        uint8_t* dst = (is_k ? c.k_smem : c.v_smem) + s * G::tile;
         const CUtensorMap* map = is_k ? tm.k : tm.v;
         mbar_wait(empty, ph ^ 1);
         trace_mark<kTrace>(tr, 4);
         if (elect_one()) {
-          mbar_arrive_expect_tx(full, kTileBytes);
-          tma_load_3d(dst, map, full, 0, lit * kBlockK, t.bh, c.pol_kv);
-          tma_load_3d(dst + kHalfBytes, map, full, 64, lit * kBlockK, t.bh, c.pol_kv);
+          mbar_arrive_expect_tx(full, G::tile);
+          tma_load_3d(dst, map, full, 0, lit * KV, t.bh, c.pol_kv);
+          tma_load_3d(dst + G::half, map, full, 64, lit * KV, t.bh, c.pol_kv);
         }
         __syncwarp();
         trace_mark<kTrace>(tr, 5);
@@ -341,6 +324,7 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
   if (op.kind == TWFA_OP_EX && (op.flags & TWFA_OPF_FUSED)) return;  // done by MX_k
   const uint32_t g = t.gbase + static_cast<uint32_t>(it);
   const int k = op.tile;
+  const uint32_t b = g % G::depth, pb = (g / G::depth) & 1;  // S buffer of this iteration, its phase
   uint32_t* tr = trace_begin<kTrace>(args, warp, st.trace_n, op.node, it, r);
 
   if (op.kind == TWFA_OP_S) {
@@ -349,35 +333,21 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
     // issues the tcgen05.mma chain and the commits
     const uint32_t s = g % rg.kd;
     if (it == 0) mbar_wait(&bar.q_full[k], t.tcount & 1);
-    if (g > 0 && !(op.flags & TWFA_OPF_INORDER))  // K landed; P_k(g-1) consumed by PV_k(g-1)
-      mbar_wait_all(&bar.k_full[s], (g / rg.kd) & 1, &bar.o_done[k], (g - 1) & 1);
+    if (g >= G::depth && !(op.flags & TWFA_OPF_INORDER))  // K landed; P_k(g-depth) consumed by PV_k
+      mbar_wait_all(&bar.k_full[s], (g / rg.kd) & 1, &bar.o_done[k][b], pb ^ 1);
     else
       mbar_wait(&bar.k_full[s], (g / rg.kd) & 1);
     trace_mark<kTrace>(tr, 4);
     tc_fence_after();
     const uint32_t qa = smem_u32(c.q_smem + k * kTileBytes);
-    const uint32_t ka = smem_u32(c.k_smem + s * kTileBytes);
-    const uint32_t d_s = tmem + k * 128;
+    const uint32_t ka = smem_u32(c.k_smem + s * G::tile);
+    const uint32_t d_s = tmem + k * 128 + b * KV;
     if (elect_one()) {
-      if constexpr (kSplitS) {
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {  // keys [64h, 64h + 64): K rows 64h.. (8 SW128 atoms in)
-#pragma unroll
-          for (int kk = 0; kk < kHeadDim / 16; ++kk) {
-            const uint32_t off = (kk >> 2) * kHalfBytes + (kk & 3) * 32;
-            mma_ss(d_s + h * 64, sdesc_sw128(qa + off, 16, 1024), sdesc_sw128(ka + off + h * 8192, 16, 1024),
-                   kIdescS, kk > 0);
-          }
-          if (h == 0) mma_commit(&bar.s_half[k]);
-        }
-      } else {
-#pragma unroll
-        for (int kk = 0; kk < kHeadDim / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * kHalfBytes + (kk & 3) * 32;
-          mma_ss(d_s, sdesc_sw128(qa + off, 16, 1024), sdesc_sw128(ka + off, 16, 1024), kIdescS, kk > 0);
-        }
-      }
-      mma_commit(&bar.s_full[k]);
+      for (int kk = 0; kk < kHeadDim / 16; ++kk)  // 16 head dims per step, 4 per SW128 half
+        mma_ss(d_s, sdesc_sw128(qa + (kk >> 2) * kHalfBytes + (kk & 3) * 32, 16, 1024),
+               sdesc_sw128(ka + (kk >> 2) * G::half + (kk & 3) * 32, 16, 1024), G::idesc_s, kk > 0);
+      mma_commit(&bar.s_full[k][b]);
       mma_commit(&bar.k_empty[s]);
       if (it == N - 1) mma_commit(&bar.q_empty[k]);
     }
@@ -386,25 +356,25 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
     const uint32_t s = g % rg.vd;
     // P_k arrives in two halves (keys 0-63, 64-127): the first four
     // K-steps of PV_k overlap the exponentials of the second half
-    mbar_wait_all(&bar.v_full[s], (g / rg.vd) & 1, &bar.p_half[k], g & 1, &bar.o_ready[k], g & 1);
+    mbar_wait_all(&bar.v_full[s], (g / rg.vd) & 1, &bar.p_half[k][b], pb, &bar.o_ready[k][b], pb);
     trace_mark<kTrace>(tr, 4);
     tc_fence_after();
-    const uint32_t va = smem_u32(c.v_smem + s * kTileBytes);
-    const uint32_t d_o = tmem + 256 + k * 128, a_p = tmem + k * 128;
+    const uint32_t va = smem_u32(c.v_smem + s * G::tile);
+    const uint32_t d_o = tmem + 256 + k * 128, a_p = tmem + k * 128 + b * KV;
     const uint32_t acc0 = it > 0 ? 1u : 0u;
     if (elect_one()) {
 #pragma unroll
-      for (int kk = 0; kk < kBlockK / 32; ++kk)  // V is MN-major: 16 keys = 16 rows of 128 B
-        mma_ts(d_o, a_p + kk * 8, sdesc_sw128(va + kk * 2048, kHalfBytes, 1024), kIdescPV, kk > 0 ? 1u : acc0);
+      for (int kk = 0; kk < KV / 32; ++kk)  // V is MN-major: 16 keys = 16 rows of 128 B
+        mma_ts(d_o, a_p + kk * 8, sdesc_sw128(va + kk * 2048, G::half, 1024), kIdescPV, kk > 0 ? 1u : acc0);
     }
     __syncwarp();
-    mbar_wait(&bar.p_full[k], g & 1);
+    mbar_wait(&bar.p_full[k][b], pb);
     tc_fence_after();
     if (elect_one()) {
 #pragma unroll
-      for (int kk = kBlockK / 32; kk < kBlockK / 16; ++kk)
-        mma_ts(d_o, a_p + kk * 8, sdesc_sw128(va + kk * 2048, kHalfBytes, 1024), kIdescPV, 1u);
-      mma_commit(&bar.o_done[k]);
+      for (int kk = KV / 32; kk < KV / 16; ++kk)
+        mma_ts(d_o, a_p + kk * 8, sdesc_sw128(va + kk * 2048, G::half, 1024), kIdescPV, 1u);
+      mma_commit(&bar.o_done[k][b]);
       mma_commit(&bar.v_empty[s]);
     }
     __syncwarp();
@@ -416,7 +386,8 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
     // with the rescale threshold most iterations keep the max: then O is
     // not touched and the correction only forwards the handoff
     if (it > 0 && !__all_sync(0xffffffffu, alpha == 1.f)) {
-      mbar_wait(&bar.o_done[k], (g - 1) & 1);
+      // O is read-modified-written: PV_k(g - 1) must have completed
+      mbar_wait(&bar.o_done[k][(g - 1) % G::depth], ((g - 1) / G::depth) & 1);
       trace_mark<kTrace>(tr, 4);
       tc_fence_after();
 #pragma unroll 1
@@ -437,36 +408,21 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
       tmem_st_wait();
     }
     tc_fence_before();
-    warp_arrive(&bar.o_ready[k]);
+    warp_arrive(&bar.o_ready[k][b]);
   } else if (op.kind == TWFA_OP_MX || op.kind == TWFA_OP_EX) {
     if constexpr (kHeavy) {
-      const uint32_t taddr = tmem + c.lane_off + k * 128;
+      const uint32_t taddr = tmem + c.lane_off + k * 128 + b * KV;
       const int row = t.q0 + k * kBlockQ + c.quad * 32 + lane;
-      const int limit = valid_keys(args, row, it * kBlockK);
-      const bool mask = !__all_sync(0xffffffffu, limit >= kBlockK);
-      uint32_t srow[128];
+      const int limit = valid_keys<KV>(args, row, it * KV);
+      const bool mask = !__all_sync(0xffffffffu, limit >= KV);
+      uint32_t srow[KV];
       if (op.kind == TWFA_OP_MX) {
-        float mx;
-        if constexpr (kSplitS) {
-          mbar_wait(&bar.s_half[k], g & 1);
-          trace_mark<kTrace>(tr, 4);
-          tc_fence_after();
-          load_half(taddr, srow, 0);
-          if (mask) mask_half(srow, limit, 0);
-          const float mx0 = half_max(srow, 0);
-          mbar_wait(&bar.s_full[k], g & 1);
-          tc_fence_after();
-          load_half(taddr, srow, 64);
-          if (mask) mask_half(srow, limit, 64);
-          mx = fmaxf(mx0, half_max(srow, 64));
-        } else {
-          mbar_wait(&bar.s_full[k], g & 1);
-          trace_mark<kTrace>(tr, 4);
-          tc_fence_after();
-          load_row(taddr, srow);
-          if (mask) mask_row(srow, limit);
-          mx = row_max(srow);
-        }
+        mbar_wait(&bar.s_full[k][b], pb);
+        trace_mark<kTrace>(tr, 4);
+        tc_fence_after();
+        load_row<KV>(taddr, srow);
+        if (mask) mask_row<KV>(srow, limit);
+        const float mx = row_max<KV>(srow);
         const float m_old = rd(st.m_run, k);
         const float m_cand = fmaxf(m_old, mx * c.scale_log2);
         const float m_new = (m_cand - m_old > kRescaleLog2) ? m_cand : m_old;  // m_old = -inf -> m_cand
@@ -486,16 +442,16 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
         // unfused EX (other ops run between MX_k and EX_k on this warp):
         // re-read S; the running max and alpha of MX_k are in registers
         trace_mark<kTrace>(tr, 4);
-        load_row(taddr, srow);
-        if (mask) mask_row(srow, limit);
+        load_row<KV>(taddr, srow);
+        if (mask) mask_row<KV>(srow, limit);
       }
       const float m_run = rd(st.m_run, k);
       const float m_safe = m_run == -INFINITY ? 0.f : m_run;
-      const float sum = mask ? exp_store_row<true>(srow, taddr, c.scale_log2, m_safe, &bar.p_half[k])
-                             : exp_store_row<false>(srow, taddr, c.scale_log2, m_safe, &bar.p_half[k]);
+      const float sum = mask ? exp_store_row<KV, true>(srow, taddr, c.scale_log2, m_safe, &bar.p_half[k][b])
+                             : exp_store_row<KV, false>(srow, taddr, c.scale_log2, m_safe, &bar.p_half[k][b]);
       wr(st.l_run, k, rd(st.l_run, k) * rd(st.alpha, k) + sum);
       tc_fence_before();
-      warp_arrive(&bar.p_full[k]);
+      warp_arrive(&bar.p_full[k][b]);
       if (it == N - 1) {
         mbar_wait(&bar.l_empty[k], (t.tcount & 1) ^ 1);
         g_sh.lbuf[k][0][c.quad * 32 + lane] = m_run;
@@ -524,11 +480,12 @@ __device__ __forceinline__ void load_q(const FaCtx& c, const WorkTile& t, int ti
 
 // Epilogue of sub-tile k on its correction warpgroup: O / l -> bf16 -> global,
 // LSE (the accumulator is final after the last PV_k).
+template <int KV>
 __device__ __forceinline__ void epilogue(const FaCtx& c, const WorkTile& t, int k, const FaArgs& args) {
   FaBarriers& bar = g_sh.bar;
   const uint32_t lane = c.lane;
   const uint32_t g_last = t.gbase + static_cast<uint32_t>(t.N - 1);
-  mbar_wait(&bar.o_done[k], g_last & 1);
+  mbar_wait(&bar.o_done[k][g_last % Kv<KV>::depth], (g_last / Kv<KV>::depth) & 1);
   mbar_wait(&bar.l_full[k], t.tcount & 1);
   const float m = g_sh.lbuf[k][0][c.quad * 32 + lane];
   const float l = g_sh.lbuf[k][1][c.quad * 32 + lane];
@@ -561,12 +518,12 @@ __device__ __forceinline__ void epilogue(const FaCtx& c, const WorkTile& t, int 
 }
 
 // Work-tile loop of one warp. `trip` runs the warp's trip program for trip r.
-template <class Trip>
+template <int KV, class Trip>
 __device__ __forceinline__ void work_loop(const FaCtx& c, const FaArgs& args, const Maps& tm, int tiles, int max_stage,
                                           bool is_load_warp, const int* cr_warp, WarpState& st, Trip&& trip) {
   uint32_t gbase = 0, tcount = 0;
   for (int work = blockIdx.x; work < c.num_work; work += gridDim.x, ++tcount) {
-    const WorkTile t = work_tile(c, args, work, gbase, tcount);
+    const WorkTile t = work_tile<KV>(c, args, work, gbase, tcount);
     if (is_load_warp) load_q(c, t, tiles, tm);
 #pragma unroll
     for (int k = 0; k < TWFA_MAX_TILES; ++k) {
@@ -578,12 +535,13 @@ __device__ __forceinline__ void work_loop(const FaCtx& c, const FaArgs& args, co
     const int trips = t.N + max_stage;
     for (int r = 0; r < trips; ++r) trip(r, t);
     for (int k = 0; k < tiles; ++k)
-      if (static_cast<int>(c.warp & ~3u) == cr_warp[k]) epilogue(c, t, k, args);
+      if (static_cast<int>(c.warp & ~3u) == cr_warp[k]) epilogue<KV>(c, t, k, args);
     gbase += static_cast<uint32_t>(t.N);
   }
 }
 
 // Shared prologue of both kernels: smem carve-up, barriers, TMEM allocation.
+template <int KV>
 __device__ __forceinline__ FaCtx fa_setup(int tiles, int kd, int vd, int load_warp, const FaArgs& args,
                                           const Maps& tm, uint8_t* smem_raw) {
   // 1 KiB alignment of the tile buffers (SW128 atoms) by offset arithmetic on
@@ -592,7 +550,7 @@ __device__ __forceinline__ FaCtx fa_setup(int tiles, int kd, int vd, int load_wa
   FaCtx c;
   c.q_smem = smem;
   c.k_smem = c.q_smem + tiles * kTileBytes;
-  c.v_smem = c.k_smem + kd * kTileBytes;
+  c.v_smem = c.k_smem + kd * Kv<KV>::tile;
   FaBarriers& bar = g_sh.bar;
   c.warp = warp_id();
   c.lane = lane_id();
@@ -600,12 +558,13 @@ __device__ __forceinline__ FaCtx fa_setup(int tiles, int kd, int vd, int load_wa
     for (int k = 0; k < tiles; ++k) {
       mbar_init(&bar.q_full[k], 1);
       mbar_init(&bar.q_empty[k], 1);
-      mbar_init(&bar.s_full[k], 1);
-      mbar_init(&bar.s_half[k], 1);
-      mbar_init(&bar.p_full[k], 4);  // warp arrivals of a warpgroup
-      mbar_init(&bar.p_half[k], 4);
-      mbar_init(&bar.o_ready[k], 4);
-      mbar_init(&bar.o_done[k], 1);
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(&bar.s_full[k][b], 1);
+        mbar_init(&bar.p_full[k][b], 4);  // warp arrivals of a warpgroup
+        mbar_init(&bar.p_half[k][b], 4);
+        mbar_init(&bar.o_ready[k][b], 4);
+        mbar_init(&bar.o_done[k][b], 1);
+      }
       for (int j = 0; j < 2; ++j) {
         mbar_init(&bar.st_full[k][j], 4);
         mbar_init(&bar.st_empty[k][j], 4);
@@ -667,20 +626,21 @@ __device__ __forceinline__ void set_register_class(int heavy_wgs) {
 }
 
 // ---------------------------------------------------------------- interpreter
-template <bool kHeavy, bool kTrace>
+template <int KV, bool kHeavy, bool kTrace>
 __device__ __forceinline__ void run_interp(const FaCtx& c, const Maps& tm, const FaArgs& args, int tiles,
                                            int max_stage, int load_warp, const int* cr_warp, const Rings rg) {
   WarpState st;
   st.trace_n = 0;
   int plen = 0;
   while (plen < TWFA_MAX_NODES && g_sh.prog_len[c.warp] > plen) ++plen;
-  work_loop(c, args, tm, tiles, max_stage, !kHeavy && c.warp == static_cast<uint32_t>(load_warp), cr_warp, st,
-            [&](int r, const WorkTile& t) {
-              for (int j = 0; j < plen; ++j) exec_op<kHeavy, kTrace>(g_sh.prog[c.warp][j], r, c, t, st, rg, tm, args);
+  work_loop<KV>(c, args, tm, tiles, max_stage, !kHeavy && c.warp == static_cast<uint32_t>(load_warp), cr_warp, st,
+                [&](int r, const WorkTile& t) {
+                  for (int j = 0; j < plen; ++j)
+                    exec_op<KV, kHeavy, kTrace>(g_sh.prog[c.warp][j], r, c, t, st, rg, tm, args);
             });
 }
 
-template <bool kTrace>
+template <int KV, bool kTrace>
 __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
     fa_fwd_interp(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                   const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ TwfaDevicePlan plan,
@@ -692,16 +652,16 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
     if (j < plan.prog_len[w]) g_sh.prog[w][j] = plan.ops[plan.prog[w][j]];
     if (j == 0) g_sh.prog_len[w] = plan.prog_len[w];
   }
-  const FaCtx c = fa_setup(plan.num_tiles, plan.k_depth, plan.v_depth, plan.load_warp, args, tm, smem_raw);
+  const FaCtx c = fa_setup<KV>(plan.num_tiles, plan.k_depth, plan.v_depth, plan.load_warp, args, tm, smem_raw);
   const Rings rg{plan.k_depth, plan.v_depth, plan.k_prefetch, plan.v_prefetch};
   const bool heavy = (plan.heavy_wg_mask >> (c.warp >> 2)) & 1;
   const int heavy_wgs = __popc(plan.heavy_wg_mask);
   if (heavy) {
     set_register_class<true>(heavy_wgs);
-    run_interp<true, kTrace>(c, tm, args, plan.num_tiles, plan.max_stage, plan.load_warp, plan.cr_warp, rg);
+    run_interp<KV, true, kTrace>(c, tm, args, plan.num_tiles, plan.max_stage, plan.load_warp, plan.cr_warp, rg);
   } else {
     set_register_class<false>(heavy_wgs);
-    run_interp<false, kTrace>(c, tm, args, plan.num_tiles, plan.max_stage, plan.load_warp, plan.cr_warp, rg);
+    run_interp<KV, false, kTrace>(c, tm, args, plan.num_tiles, plan.max_stage, plan.load_warp, plan.cr_warp, rg);
   }
   fa_teardown(c);
 }
@@ -743,7 +703,7 @@ __device__ __forceinline__ void spec_trip(int r, const FaCtx& c, const WorkTile&
                                           const FaArgs& args, std::integer_sequence<int, J...>) {
   constexpr bool kHeavy = (TWFA_PLAN(I).heavy_wg_mask >> (W / 4)) & 1;
   constexpr Rings rg{TWFA_PLAN(I).k_depth, TWFA_PLAN(I).v_depth, TWFA_PLAN(I).k_prefetch, TWFA_PLAN(I).v_prefetch};
-  (exec_op<kHeavy, kTrace>(spec_op<I, W, J>(), r, c, t, st, rg, tm, args), ...);
+  (exec_op<TWFA_PLAN(I).kv_tile, kHeavy, kTrace>(spec_op<I, W, J>(), r, c, t, st, rg, tm, args), ...);
 }
 
 template <int I, int W, bool kTrace>
@@ -754,7 +714,7 @@ __device__ __forceinline__ void run_spec(const FaCtx& c, const Maps& tm, const F
   constexpr int cr_warp[TWFA_MAX_TILES] = {TWFA_PLAN(I).cr_warp[0], TWFA_PLAN(I).cr_warp[1]};
   WarpState st;
   st.trace_n = 0;
-  work_loop(c, args, tm, TWFA_PLAN(I).num_tiles, TWFA_PLAN(I).max_stage, kLoad, cr_warp, st,
+  work_loop<TWFA_PLAN(I).kv_tile>(c, args, tm, TWFA_PLAN(I).num_tiles, TWFA_PLAN(I).max_stage, kLoad, cr_warp, st,
             [&](int r, const WorkTile& t) {
               spec_trip<I, W, kTrace>(r, c, t, st, tm, args, std::make_integer_sequence<int, plen>{});
             });
@@ -784,8 +744,9 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
   for (int i = threadIdx.x; i < TWFA_MAX_WARPS * TWFA_MAX_NODES; i += blockDim.x)
     fill_progs<I>(i / TWFA_MAX_NODES, i % TWFA_MAX_NODES, std::make_integer_sequence<int, TWFA_MAX_WARPS>{});
   constexpr int cr_warp[TWFA_MAX_TILES] = {TWFA_PLAN(I).cr_warp[0], TWFA_PLAN(I).cr_warp[1]};
-  const FaCtx c = fa_setup(TWFA_PLAN(I).num_tiles, TWFA_PLAN(I).k_depth, TWFA_PLAN(I).v_depth,
-                           TWFA_PLAN(I).load_warp, args, tm, smem_raw);
+  constexpr int KV = TWFA_PLAN(I).kv_tile;
+  const FaCtx c = fa_setup<KV>(TWFA_PLAN(I).num_tiles, TWFA_PLAN(I).k_depth, TWFA_PLAN(I).v_depth,
+                               TWFA_PLAN(I).load_warp, args, tm, smem_raw);
   // the register class is per warpgroup; the warp roles of each class are
   // dispatched inside its branch so ptxas allocates them under that budget
   constexpr int mask = TWFA_PLAN(I).heavy_wg_mask;
@@ -793,7 +754,7 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
   constexpr int nw = TWFA_PLAN(I).num_warps;
   if ((mask >> (c.warp >> 2)) & 1) {
     set_register_class<true>(heavy_wgs);
-    run_interp<true, kTrace>(c, tm, args, TWFA_PLAN(I).num_tiles, TWFA_PLAN(I).max_stage, TWFA_PLAN(I).load_warp,
+    run_interp<KV, true, kTrace>(c, tm, args, TWFA_PLAN(I).num_tiles, TWFA_PLAN(I).max_stage, TWFA_PLAN(I).load_warp,
                              cr_warp, Rings{TWFA_PLAN(I).k_depth, TWFA_PLAN(I).v_depth, TWFA_PLAN(I).k_prefetch,
                                             TWFA_PLAN(I).v_prefetch});
   } else {
@@ -807,7 +768,7 @@ bool same_plan(const TwfaDevicePlan& a, const TwfaDevicePlan& b) {
   if (a.family != b.family || a.ii != b.ii || a.max_stage != b.max_stage || a.num_nodes != b.num_nodes ||
       a.num_warps != b.num_warps || a.num_tiles != b.num_tiles || a.k_depth != b.k_depth || a.v_depth != b.v_depth ||
       a.load_warp != b.load_warp || a.k_prefetch != b.k_prefetch || a.v_prefetch != b.v_prefetch ||
-      a.heavy_wg_mask != b.heavy_wg_mask)
+      a.heavy_wg_mask != b.heavy_wg_mask || a.s_depth != b.s_depth || a.kv_tile != b.kv_tile)
     return false;
   for (int k = 0; k < TWFA_MAX_TILES; ++k)
     if (a.cr_warp[k] != b.cr_warp[k] || a.sm_warp[k] != b.sm_warp[k]) return false;

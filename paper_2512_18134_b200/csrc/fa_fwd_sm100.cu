@@ -9,7 +9,8 @@ namespace twfa {
 
 size_t fa_fwd_smem_bytes(const TwfaDevicePlan& plan) {
   // dynamic part only: tile buffers (+ alignment slack); FaShared is static
-  return 1024 + static_cast<size_t>(plan.num_tiles + plan.k_depth + plan.v_depth) * kTileBytes;
+  const size_t kv_bytes = static_cast<size_t>(plan.kv_tile) * kHeadDim * 2;
+  return 1024 + static_cast<size_t>(plan.num_tiles) * kTileBytes + (plan.k_depth + plan.v_depth) * kv_bytes;
 }
 
 const char* fa_fwd_kernel_name(const TwfaDevicePlan& plan) {
@@ -32,8 +33,11 @@ cudaError_t fa_fwd_launch(const CUtensorMap& tq, const CUtensorMap& tk, const CU
     TWFA_SPECIALIZED_PLANS(TWFA_LAUNCH)
 #undef TWFA_LAUNCH
   }
-  return trace ? launch(fa_fwd_interp<true>, smem, grid, threads, stream, tq, tk, tv, plan, args)
-               : launch(fa_fwd_interp<false>, smem, grid, threads, stream, tq, tk, tv, plan, args);
+  if (plan.kv_tile == 64)
+    return trace ? launch(fa_fwd_interp<64, true>, smem, grid, threads, stream, tq, tk, tv, plan, args)
+                 : launch(fa_fwd_interp<64, false>, smem, grid, threads, stream, tq, tk, tv, plan, args);
+  return trace ? launch(fa_fwd_interp<128, true>, smem, grid, threads, stream, tq, tk, tv, plan, args)
+               : launch(fa_fwd_interp<128, false>, smem, grid, threads, stream, tq, tk, tv, plan, args);
 }
 
 }  // namespace twfa

@@ -391,8 +391,23 @@ void derive(LoweredSchedule& s) {
       for (size_t i = 0; i < ex.size(); ++i) p.ex_ring[i] = p.ops[ex[i]].tile;
     }
   }
-  // smem: Q (tiles x 32 KiB) + K ring + V ring of 32 KiB slots
-  const int64_t smem = 32768LL * (tiles + p.k_depth + p.v_depth);
+  // S ring in tensor memory: the delta of PV_k -> S_k (S_k(i + delta)
+  // overwrites the P_k(i) aliased over S_k(i)); 1 = one 128-key S tile per
+  // sub-tile, 2 = two 64-key tiles in the same 128 columns
+  p.s_depth = 0;
+  for (const LEdge& e : s.edges)
+    for (int k = 0; k < tiles; ++k)
+      if (e.src == node_id("PV" + std::to_string(k)) && e.dst == node_id("S" + std::to_string(k))) {
+        if (p.s_depth != 0 && p.s_depth != e.delta) throw DomainError("sub-tiles disagree on the S ring depth");
+        p.s_depth = e.delta;
+      }
+  if (p.s_depth != 1 && p.s_depth != 2)
+    throw DomainError("PV_k -> S_k must carry delta 1 or 2 (S ring depth in tensor memory)");
+  p.kv_tile = 128 / p.s_depth;
+  // smem: Q (tiles x 32 KiB) + K ring + V ring of kv_tile-key slots
+  const int64_t kv_bytes = static_cast<int64_t>(p.kv_tile) * 256;
+  const int64_t smem = 32768LL * tiles + kv_bytes * (p.k_depth + p.v_depth);
+  if (p.k_depth > 4 || p.v_depth > 4) throw DomainError("ring depth above 4");
   if (smem > 200 * 1024) throw DomainError("ring depths exceed shared memory");
 }
 
@@ -438,6 +453,8 @@ std::string describe(const LoweredSchedule& s) {
   json rings = json::object();
   if (p.family == TWFA_FAMILY_FA_FWD) {
     rings["K"] = p.k_depth;
+    rings["S"] = p.s_depth;
+    j["kv_tile"] = p.kv_tile;
     rings["V"] = p.v_depth;
     j["prefetch"] = {{"LDK", p.k_prefetch}, {"LDV", p.v_prefetch}};
     j["num_tiles"] = p.num_tiles;

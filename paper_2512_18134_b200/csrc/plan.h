@@ -78,6 +78,11 @@ struct TwfaDevicePlan {
   // waits on a slot its own warp frees later.
   int32_t k_prefetch;
   int32_t v_prefetch;
+  // S ring depth in tensor memory (delta of the PV_k -> S_k edge, 1 or 2) and
+  // the K/V tile it implies: the 128 S/P columns of a sub-tile hold s_depth
+  // tiles of kv_tile = 128 / s_depth keys.
+  int32_t s_depth;
+  int32_t kv_tile;
   int32_t cr_warp[TWFA_MAX_TILES];  // warpgroup start running CR_k (+ epilogue of tile k)
   int32_t sm_warp[TWFA_MAX_TILES];  // warpgroup start running MX_k / EX_k
   int32_t mma_warp;                 // GEMM: warp issuing MMA

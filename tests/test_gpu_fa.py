@@ -147,3 +147,12 @@ def test_specialized_kernel_matches_interpreter(twfa, plan, causal, monkeypatch)
     torch.cuda.synchronize()
     assert torch.equal(o_spec, o_int)
     assert torch.equal(l_spec, l_int)
+
+
+@pytest.mark.parametrize("S,causal", [(512, False), (640, True), (300, False), (64, False), (100, True)])
+def test_double_buffered_s_schedule_matches_oracle(twfa, S, causal):
+    """The fa_fwd_ring2 schedule (PV_k -> S_k with delta 2: two 64-key S tiles
+    per sub-tile in tensor memory, 4-deep K/V rings) through the same kernels."""
+    p = twfa.Plan(*twfa.load_schedule("fa_fwd_ring2"))
+    assert p.describe()["kv_tile"] == 64
+    _check(twfa, p, 1, 2, S, causal, 12)

@@ -87,7 +87,7 @@ def test_gemm_stream_depth_sets_ring(twfa, ws):
 def test_fa_ring_depth_follows_solution(twfa):
     prob, sol = twfa.load_schedule("fa_fwd")
     s = json.loads(sol)
-    assert twfa.Plan(prob, sol).describe()["rings"] == {"K": 2, "V": 2}
+    assert twfa.Plan(prob, sol).describe()["rings"] == {"K": 2, "V": 2, "S": 1}
     # two 32 KiB Q tiles + 2 + 2 ring slots fill the 227 KiB of shared memory;
     # a deeper ring than the solution's is not realizable and must say so
     s["streaming_depths"] = {"LDK": 3, "LDV": 2}
@@ -137,3 +137,18 @@ def test_malformed_problem_is_rejected(twfa):
         twfa.Plan("{not json", sol)
     with pytest.raises(ValueError, match="unknown key"):
         twfa.Plan(json.dumps({"machine": {}, "graph": {}, "extra": 1}), sol)
+
+
+def test_s_ring_depth_from_pv_s_edge(twfa):
+    """The double-buffered-S problem (PV_k -> S_k with delta 2) lowers to a
+    2-deep S ring of 64-key tiles with the 4-deep K/V rings its solution
+    streams; any other delta cannot be realized in 512 TMEM columns."""
+    prob, sol = twfa.load_schedule("fa_fwd_ring2")
+    d = twfa.Plan(prob, sol).describe()
+    assert d["rings"] == {"K": 4, "V": 4, "S": 2} and d["kv_tile"] == 64
+    p = json.loads(prob)
+    for e in p["graph"]["edges"]:
+        if e["src"] in ("PV0", "PV1") and e["dst"] == "S" + e["src"][2]:
+            e["delta"] = 3
+    with pytest.raises(ValueError, match="delta 1 or 2"):
+        twfa.Plan(json.dumps(p), sol)

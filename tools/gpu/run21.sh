@@ -1,0 +1,2 @@
+REPS=2 SCHEDS=fa_fwd,fa_fwd_ring2,fa_fwd_ring2:experiments/R2_sep,fa_fwd:experiments/E1_fa4 timeout 900 python tools/variants.py paper_2512_18134_b200/libtwfa.so 2>&1
+timeout 300 python tools/trace_stats.py 4 32 8192 fa_fwd_ring2:experiments/R2_sep > gpurun_out/trace_r2.txt 2>&1

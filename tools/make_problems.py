@@ -48,7 +48,7 @@ def edge(src, dst, d, delta=0, blocking=False):
     return e
 
 
-def fa_forward_problem(tc_variable_latency=False, calibrated=False):
+def fa_forward_problem(tc_variable_latency=False, calibrated=False, s_ring=1):
     """FA-forward loop body on sm_100a: two 128-row Q sub-tiles (k = 0, 1)
     share one 128-key K/V tile per iteration.
 
@@ -64,6 +64,13 @@ def fa_forward_problem(tc_variable_latency=False, calibrated=False):
     Blocking edges are the mbarrier waits of the realized kernel: TMA landed
     (LD -> GEMM), MMA committed (S -> MX, PV -> CR), P stored (EX -> PV),
     O rescaled (CR -> PV).
+
+    s_ring = 2 double-buffers S in tensor memory instead: the S/P columns of
+    each sub-tile (128) hold two 64-key S tiles, so the K/V tile is 64 keys,
+    every per-iteration cost halves, and S_k(i+1) no longer waits for
+    PV_k(i): the edge PV_k -> S_k carries delta = 2 (S_k(i+2) overwrites the
+    P_k(i) that PV_k(i) reads). The executor derives the ring depth (and the
+    64-key tile) from that delta.
     """
     T = 256  # raw clk per unit (see module docstring)
     # per-op durations in units of T: datasheet throughput (default) or the
@@ -71,6 +78,8 @@ def fa_forward_problem(tc_variable_latency=False, calibrated=False):
     # MX ~500 clk (TMEM load of the S row + max + handoff), EX ~1500 clk
     # (MUFU-bound exp of a 128x128 tile + bf16 pack + TMEM store)
     cost = dict(S=2, PV=2, MX=1, EX=4, CR=1) if not calibrated else dict(S=2, PV=2, MX=2, EX=6, CR=1)
+    if s_ring == 2:  # 64-key iterations: GEMMs 256 clk, 8192 exp2 = 512 clk
+        cost = dict(S=1, PV=1, MX=1, EX=2, CR=1)
     machine = {
         "units": [{"name": "TC", "capacity": 1}, {"name": "TMA", "capacity": 1},
                   {"name": "MUFU", "capacity": 1}, {"name": "ALU", "capacity": 1},
@@ -80,16 +89,17 @@ def fa_forward_problem(tc_variable_latency=False, calibrated=False):
         "reg_limit": 224,
         "vl_warp": 15,
     }
+    kv = 128 // s_ring  # keys per K/V tile
     nodes = [
-        node("LDK", "TMA", 2 * T // T, variable_latency=True),
-        node("LDV", "TMA", 2 * T // T, variable_latency=True),
+        node("LDK", "TMA", 2 // s_ring, variable_latency=True),
+        node("LDV", "TMA", 2 // s_ring, variable_latency=True),
     ]
     edges = []
     for k in (0, 1):
         nodes += [
-            node(f"S{k}", "TC", cost["S"], footprint={"tmem": 128}),
-            node(f"MX{k}", "ALU", cost["MX"], regs=128, spill_cost=1, warps_required=4),
-            node(f"EX{k}", "MUFU", cost["EX"], regs=64, warps_required=4),
+            node(f"S{k}", "TC", cost["S"], footprint={"tmem": kv}),
+            node(f"MX{k}", "ALU", cost["MX"], regs=kv, spill_cost=1, warps_required=4),
+            node(f"EX{k}", "MUFU", cost["EX"], regs=kv // 2, warps_required=4),
             node(f"CR{k}", "FMA", cost["CR"], regs=64, warps_required=4),
             node(f"PV{k}", "TC", cost["PV"], footprint={"tmem": 128}),
         ]
@@ -107,7 +117,7 @@ def fa_forward_problem(tc_variable_latency=False, calibrated=False):
             edge(f"PV{k}", f"PV{k}", cost["PV"], delta=1),
             # S_k(i+1) overwrites the TMEM columns P_k(i) is read from: the
             # calibrated model waits for PV_k's completion (cross-warp commit)
-            edge(f"PV{k}", f"S{k}", cost["PV"] if calibrated else 0, delta=1),
+            edge(f"PV{k}", f"S{k}", cost["PV"] if calibrated else 0, delta=s_ring),
         ]
     if tc_variable_latency:
         # tcgen05.mma is asynchronous: its completion is only observed through
@@ -212,6 +222,8 @@ def main():
         # comparison: MMAs as fixed-latency ops (the solver scatters them over warps)
         "fa_fwd_fixedtc": (fa_forward_problem(), 2),
         "fa_fwd_cal": (fa_forward_problem(calibrated=True), 2),
+        # double-buffered S (64-key K/V tiles): S_k(i+1) independent of PV_k(i)
+        "fa_fwd_ring2": (fa_forward_problem(tc_variable_latency=True, s_ring=2), 4),
     }
     for name, (raw, depth) in probs.items():
         if args.only and name != args.only:

@@ -51,3 +51,17 @@ print(f"\ntrip {mid}..{mid+1} of work tile 0: warp op it issue ready done")
 for r in sorted(recs, key=lambda r: r[4]):
     if r[3] in (mid, mid + 1) and d(start, r[4]) < 20000 and (r[0] % 4 == 0 or r[0] >= 12 or r[1][0] in "SP"):
         print(f"w{r[0]:2d} {r[1]:4s} it={r[2]:3d} trip={r[3]:3d} issue={d(start, r[4]):6d} ready={d(start, r[5]) if r[5] else -1:6d} done={d(start, r[6]):6d}")
+
+# tile boundaries: time from the last steady issue of each op to its first
+# issue in the next work tile, in units of the median trip
+print("\nwork-tile boundary cost (CTA 0), per op: median gap across a tile boundary / median trip")
+for op in ids:
+    for w in sorted({r[0] for r in recs if r[1] == op})[:1]:
+        rs = [r for r in recs if r[1] == op and r[0] == w]
+        if len(rs) < 8: continue
+        steady, bound = [], []
+        for a, b in zip(rs, rs[1:]):
+            (bound if b[2] < a[2] else steady).append(d(a[4], b[4]))
+        if steady and bound:
+            print(f"{op:4s} w{w:2d} trip {np.median(steady):7.0f}  boundary {np.median(bound):8.0f} "
+                  f"({np.median(bound) / np.median(steady):.2f} trips)  n={len(bound)}")
