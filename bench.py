@@ -239,6 +239,47 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
+def realized_schedule(twfa, plan, q, k, v, causal):
+    """Steady-state cycles per trip of the realized schedule (one traced launch
+    of the same workload, outside the timed region) against the solver's
+    prediction I x (raw clk per normalized unit, schedules/fa_fwd.meta.json).
+    Measured = median clock64 distance between consecutive issues of S1 on
+    its warp in CTA 0 (one trip = 256 query rows x one K/V tile)."""
+    import numpy as np
+    import torch
+    desc = plan.describe()
+    meta = json.load(open(os.path.join(twfa.schedule_dir(), "fa_fwd.meta.json")))
+    unit = min(int(raw) // norm for raw, norm in meta["cost_map"].items())
+    nw, cap = desc["num_warps"], 8192
+    tr = torch.zeros(nw * cap * 8, dtype=torch.int32, device=q.device)
+    twfa.fa_fwd(plan, q, k, v, causal=causal, trace=tr, trace_cap=cap)
+    torch.cuda.synchronize()
+    t = tr.cpu().numpy().view(np.uint32).reshape(nw, cap, 8).astype(np.int64)
+    prob = json.loads(twfa.load_schedule("fa_fwd")[0])
+    s1 = [n["id"] for n in prob["graph"]["nodes"]].index("S1")
+    w = desc["nodes"]["S1"]["warp_start"]
+    n = int(t[w, 0, 0])
+    recs = t[w, 1:1 + n]
+    clk = recs[recs[:, 0] == s1][:, 3]
+    trips = recs[recs[:, 0] == s1][:, 2]
+    d = np.diff(clk) % (1 << 32)
+    d = d[np.diff(trips) == 1]  # consecutive trips of one work tile
+    return {"I": desc["I"], "unit_clk": unit, "predicted_clk_per_trip": desc["I"] * unit,
+            "measured_clk_per_trip": float(np.median(d)) if len(d) else None,
+            "trip": f"256 query rows x {desc.get('kv_tile', 128)} keys", "kernel": desc.get("kernel"),
+            "how": "traced launch, CTA 0, median S1 issue-to-issue; tracing adds ~10%"}
+
+
+def ncu_tensor_util(workload):
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    e = json.load(open(p)).get(workload)
+    return None if not e else {"tensor_pipe_active_pct": e.get("tensor_pipe_active_pct"),
+                               "xu_pipe_inst_pct": e.get("xu_pipe_inst_pct"),
+                               "source": "profiles/ncu_summary.json (ncu --set full, one launch)"}
+
+
 def run_ours(args, world, rank, local):
     import torch
     import paper_2512_18134_b200 as twfa
@@ -333,6 +374,8 @@ def run_ours(args, world, rank, local):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "steps": e2e_steps, "path": "pinned host -> device copies + twfa fa_fwd + device -> host O"},
         "gpu_launches": args.steps,
+        "tensor_pipe": ncu_tensor_util(workload),
+        "schedule_realized": realized_schedule(twfa, plan, q, k, v, causal),
     }
     if world == 1 and not args.no_cpu_baseline:
         tfl, secs, sample, threads = cpu_attention_sample()
