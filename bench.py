@@ -361,7 +361,9 @@ def run_ours(args, world, rank, local):
         "data": "synthetic N(0,1) bf16 Q/K/V generated on device (seed 2026 + rank)",
         "config": {"workload": desc, "B_per_gpu": B, "B_total": B * world, "H": H, "S": S, "d": D,
                    "causal": causal, "parallelism": f"bh-shard x{world}, no collective",
-                   "schedule": "fa_fwd.solution.json (z3 -in, I=9)",
+                   "schedule": "fa_fwd.solution.json (%s, I=%d)" % (
+                       json.load(open(os.path.join(twfa.schedule_dir(), "fa_fwd.meta.json")))["backend"],
+                       plan.describe()["I"]),
                    "l2": "inputs 3x%d MiB per rank > 126 MB L2; no flush" % (q.numel() * 2 >> 20)},
         "per_gpu_tflops": value / world,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",

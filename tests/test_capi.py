@@ -54,7 +54,7 @@ def test_plan_survives_threads(twfa):
     ts = [threading.Thread(target=work) for _ in range(8)]
     [t.start() for t in ts]
     [t.join() for t in ts]
-    assert out == [9] * 8
+    assert out == [json.loads(sol)["I"]] * 8
 
 
 def _host_tool(twfa):

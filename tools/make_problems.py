@@ -215,21 +215,27 @@ def main():
     ap.add_argument("--solver", default="")
     ap.add_argument("--only", default="")
     args = ap.parse_args()
+    # name: (raw problem, stream depth, normalization resolution U or None = --resolution)
     probs = {
-        "gemm_mainloop": (gemm_problem(), 4),
-        # production: tcgen05.mma modeled as variable latency (see fa_forward_problem)
-        "fa_fwd": (fa_forward_problem(tc_variable_latency=True), 2),
+        "gemm_mainloop": (gemm_problem(), 4, None),
+        # production: tcgen05.mma modeled as variable latency (see
+        # fa_forward_problem) with the B200-calibrated costs (EX 6, MX 2
+        # units of 256 clk, measured by the in-kernel trace); U = 9 normalizes
+        # {256, 512, 1536} exactly (F = 0)
+        "fa_fwd": (fa_forward_problem(tc_variable_latency=True, calibrated=True), 2, 9),
+        # variable latency with the datasheet costs (EX 4, MX 1)
+        "fa_fwd_vl": (fa_forward_problem(tc_variable_latency=True), 2, None),
         # comparison: MMAs as fixed-latency ops (the solver scatters them over warps)
-        "fa_fwd_fixedtc": (fa_forward_problem(), 2),
-        "fa_fwd_cal": (fa_forward_problem(calibrated=True), 2),
+        "fa_fwd_fixedtc": (fa_forward_problem(), 2, None),
+        "fa_fwd_cal": (fa_forward_problem(calibrated=True), 2, None),
         # double-buffered S (64-key K/V tiles): S_k(i+1) independent of PV_k(i)
-        "fa_fwd_ring2": (fa_forward_problem(tc_variable_latency=True, s_ring=2), 4),
+        "fa_fwd_ring2": (fa_forward_problem(tc_variable_latency=True, s_ring=2), 4, None),
     }
-    for name, (raw, depth) in probs.items():
+    for name, (raw, depth, res) in probs.items():
         if args.only and name != args.only:
             continue
         if args.solve:
-            solve(name, raw, args.resolution, depth, args.solver)
+            solve(name, raw, res or args.resolution, depth, args.solver)
         else:
             print(json.dumps(raw, indent=2))
 
