@@ -77,7 +77,17 @@ def fa_forward_problem(tc_variable_latency=False, calibrated=False, s_ring=1):
     # values measured on B200 by the in-kernel trace (tools/timeline.py):
     # MX ~500 clk (TMEM load of the S row + max + handoff), EX ~1500 clk
     # (MUFU-bound exp of a 128x128 tile + bf16 pack + TMEM store)
-    cost = dict(S=2, PV=2, MX=1, EX=4, CR=1) if not calibrated else dict(S=2, PV=2, MX=2, EX=6, CR=1)
+    cost = dict(S=2, PV=2, MX=1, EX=4, CR=1)
+    spill = 1
+    if calibrated:
+        # measured on B200 (tools/calibrate.py -> schedules/calibration.json),
+        # rounded to units of T = 256 clk (the normalizer then maps them
+        # exactly, F = 0; the reference's ILP on the unrounded cycles, with
+        # five distinct costs, distorts ratios by F >= 512 at U <= 16)
+        cal = json.load(open(os.path.join(OUT, "calibration.json")))
+        assert cal["T"] == T
+        cost = {k: v for k, v in cal["units"].items() if k != "spill"}
+        spill = cal["units"]["spill_row"]  # MX's value is the S row: re-read + handoff
     if s_ring == 2:  # 64-key iterations: GEMMs 256 clk, 8192 exp2 = 512 clk
         cost = dict(S=1, PV=1, MX=1, EX=2, CR=1)
     machine = {
@@ -90,15 +100,16 @@ def fa_forward_problem(tc_variable_latency=False, calibrated=False, s_ring=1):
         "vl_warp": 15,
     }
     kv = 128 // s_ring  # keys per K/V tile
+    ld = 2 // s_ring  # streamed: zero cycles after the rewrite
     nodes = [
-        node("LDK", "TMA", 2 // s_ring, variable_latency=True),
-        node("LDV", "TMA", 2 // s_ring, variable_latency=True),
+        node("LDK", "TMA", ld, variable_latency=True),
+        node("LDV", "TMA", ld, variable_latency=True),
     ]
     edges = []
     for k in (0, 1):
         nodes += [
             node(f"S{k}", "TC", cost["S"], footprint={"tmem": kv}),
-            node(f"MX{k}", "ALU", cost["MX"], regs=kv, spill_cost=1, warps_required=4),
+            node(f"MX{k}", "ALU", cost["MX"], regs=kv, spill_cost=spill, warps_required=4),
             node(f"EX{k}", "MUFU", cost["EX"], regs=kv // 2, warps_required=4),
             node(f"CR{k}", "FMA", cost["CR"], regs=64, warps_required=4),
             node(f"PV{k}", "TC", cost["PV"], footprint={"tmem": 128}),
@@ -227,7 +238,7 @@ def main():
         "fa_fwd_vl": (fa_forward_problem(tc_variable_latency=True), 2, None),
         # comparison: MMAs as fixed-latency ops (the solver scatters them over warps)
         "fa_fwd_fixedtc": (fa_forward_problem(), 2, None),
-        "fa_fwd_cal": (fa_forward_problem(calibrated=True), 2, None),
+        "fa_fwd_cal": (fa_forward_problem(calibrated=True), 2, 9),
         # double-buffered S (64-key K/V tiles): S_k(i+1) independent of PV_k(i)
         "fa_fwd_ring2": (fa_forward_problem(tc_variable_latency=True, s_ring=2), 4, None),
     }
