@@ -532,8 +532,11 @@ __device__ __forceinline__ void work_loop(const FaCtx& c, const FaArgs& args, co
       st.alpha[k] = 1.f;
     }
     st.k_next = st.v_next = 0;
+    // trip -1 only tops up the streamed-load rings (every timed op has
+    // iteration < 0 there): a consumer that precedes its load in the trip
+    // program finds iteration 0 already in flight
     const int trips = t.N + max_stage;
-    for (int r = 0; r < trips; ++r) trip(r, t);
+    for (int r = -1; r < trips; ++r) trip(r, t);
     for (int k = 0; k < tiles; ++k)
       if (static_cast<int>(c.warp & ~3u) == cr_warp[k]) epilogue<KV>(c, t, k, args);
     gbase += static_cast<uint32_t>(t.N);

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cstring>
 #include <set>
+#include <tuple>
 
 #include "json.hpp"
 
@@ -227,17 +228,24 @@ void derive(LoweredSchedule& s) {
   p.max_stage = max_stage;
 
   // per-warp trip programs: ops covering the warp, ordered by their cycle in
-  // the trip and then by declaration order -- the same key the reference's
-  // program synthesis sorts a region by (codegen.cpp:179-183)
+  // the trip and then by declaration order -- the key the reference's
+  // program synthesis sorts a region by (codegen.cpp:179-183) -- except that
+  // streamed loads (zero cycles and no unit reservation after the streaming
+  // rewrite, jointsolve.cpp:511-524) issue after the timed ops of their
+  // cycle: a zero-duration op occupies no part of the cycle, so either side
+  // realizes the same modulo schedule, and the ring prefetch (prefetch_of)
+  // already serves its consumers from an earlier trip.
+  auto streamed = [&](int v) { return s.nodes[static_cast<size_t>(v)].cycles == 0; };
+  auto order_key = [&](int v) {
+    return std::make_tuple(s.slot[static_cast<size_t>(v)], streamed(v) ? 1 : 0, v);
+  };
   s.warp_prog.assign(static_cast<size_t>(s.num_warps), {});
   for (int w = 0; w < s.num_warps; ++w) {
     std::vector<int>& prog = s.warp_prog[static_cast<size_t>(w)];
     for (size_t v = 0; v < n; ++v)
       if (p.ops[v].warp_start <= w && w < p.ops[v].warp_start + p.ops[v].warp_count)
         prog.push_back(static_cast<int>(v));
-    std::stable_sort(prog.begin(), prog.end(), [&](int x, int y) {
-      return std::make_pair(s.slot[static_cast<size_t>(x)], x) < std::make_pair(s.slot[static_cast<size_t>(y)], y);
-    });
+    std::stable_sort(prog.begin(), prog.end(), [&](int x, int y) { return order_key(x) < order_key(y); });
     p.prog_len[w] = static_cast<uint8_t>(prog.size());
     for (size_t i = 0; i < prog.size(); ++i) {
       p.prog[w][i] = static_cast<uint8_t>(prog[i]);
@@ -255,7 +263,7 @@ void derive(LoweredSchedule& s) {
     if (gap < e.d)
       throw DomainError("schedule violates dependence " + s.nodes[e.src].id + " -> " + s.nodes[e.dst].id);
     const bool share = u.warp_start < v.warp_start + v.warp_count && v.warp_start < u.warp_start + u.warp_count;
-    if (gap == 0 && share && e.dst < e.src)
+    if (gap == 0 && share && !streamed(e.src) && order_key(e.dst) < order_key(e.src))
       throw DomainError("same-cycle dependence " + s.nodes[e.src].id + " -> " + s.nodes[e.dst].id +
                         " is ordered consumer-first on a shared warp");
   }
@@ -287,8 +295,7 @@ void derive(LoweredSchedule& s) {
                           " is shallower than its consumer lag");
       const bool share = L.warp_start < C.warp_start + C.warp_count && C.warp_start < L.warp_start + L.warp_count;
       if (!share) continue;
-      const bool before = std::make_pair(s.slot[static_cast<size_t>(e.dst)], e.dst) <
-                          std::make_pair(s.slot[static_cast<size_t>(ld)], ld);
+      const bool before = order_key(e.dst) < order_key(ld);
       pf = std::min<int64_t>(pf, depth - lag - (before ? 0 : 1));
     }
     if (pf < 0)

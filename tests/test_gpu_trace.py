@@ -45,7 +45,9 @@ def realized_schedule(twfa, plan, B=1, H=1, S=2048, causal=False, cap=512):
     for w in range(nw):
         n = int(t[w, 0, 0])
         # (node, iteration, trip, t_issue, t_ready, t_done)
+        # trip is signed: streamed loads prime their ring in trip -1
         per_warp[w] = [tuple(int(x) for x in t[w, 1 + i, :6]) for i in range(n)]
+        per_warp[w] = [(r[0], r[1], r[2] - (1 << 32) if r[2] >= 1 << 31 else r[2]) + r[3:] for r in per_warp[w]]
     return desc, per_warp
 
 

@@ -32,13 +32,20 @@ def steady_programs_from_reference(ws, prob, sol):
     prog = json.loads(ws.codegen(prob, sol, "json"))
     copies = prog["copies"]
     per_warp, stage, warp = {}, {}, {}
+    streamed = set(json.loads(sol).get("streaming_depths", {}))
+    cycle = {}
     for ins in prog["steady_state"]:
         if ins["kind"] != "op":
             continue
         stage[ins["node"]] = copies - 1 - ins["copy"]
         warp[ins["node"]] = (ins["warp_start"], ins["warp_count"])
+        cycle[ins["node"]] = ins["cycle"]
         for w in range(ins["warp_start"], ins["warp_start"] + ins["warp_count"]):
             per_warp.setdefault(w, []).append(ins["node"])
+    # the executor issues streamed (zero-cycle) loads after the timed ops of
+    # their cycle (lowering.cpp); otherwise the reference's region order
+    for w, ops in per_warp.items():
+        ops.sort(key=lambda v: (cycle[v], v in streamed))
     return prog, per_warp, stage, warp
 
 

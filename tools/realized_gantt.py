@@ -80,7 +80,8 @@ def main():
     for w in range(nw):
         for i in range(int(t[w, 0, 0])):
             e = t[w, 1 + i]
-            recs.append((w, int(e[0]), int(e[1]), int(e[2]), int(e[3]), int(e[4]), int(e[5])))
+            trip = int(e[2]) - (1 << 32) if int(e[2]) >= 1 << 31 else int(e[2])  # trip -1 primes rings
+            recs.append((w, int(e[0]), int(e[1]), trip, int(e[3]), int(e[4]), int(e[5])))
     I = solution["I"]
     prefetch = desc.get("prefetch", {})
     stage, warps = {}, {}

@@ -32,7 +32,8 @@ recs = []
 for w in range(nw):
     for i in range(int(t[w, 0, 0])):
         e = t[w, 1 + i]
-        recs.append((w, ids[e[0]], int(e[1]), int(e[2]), int(e[3]), int(e[4]), int(e[5])))
+        trip = int(e[2]) - (1 << 32) if int(e[2]) >= 1 << 31 else int(e[2])  # trip -1 primes rings
+        recs.append((w, ids[e[0]], int(e[1]), trip, int(e[3]), int(e[4]), int(e[5])))
 def d(a, b):
     return (b - a) % (1 << 32)
 print(f"{'op':4s} {'warp':>4s} {'n':>6s} {'wait_med':>9s} {'work_med':>9s} {'wait_mean':>9s} {'work_mean':>9s} {'issue2issue':>11s}")
