@@ -522,7 +522,13 @@ template <int KV, class Trip>
 __device__ __forceinline__ void work_loop(const FaCtx& c, const FaArgs& args, const Maps& tm, int tiles, int max_stage,
                                           bool is_load_warp, const int* cr_warp, WarpState& st, Trip&& trip) {
   uint32_t gbase = 0, tcount = 0;
-  for (int work = blockIdx.x; work < c.num_work; work += gridDim.x, ++tcount) {
+  for (int round = 0;; ++round, ++tcount) {
+    // causal tiles are ordered longest first; alternating the direction of
+    // each round over the persistent CTAs ("snake") balances their totals
+    const int work = round * static_cast<int>(gridDim.x) +
+                     ((args.causal && (round & 1)) ? static_cast<int>(gridDim.x - 1 - blockIdx.x)
+                                                   : static_cast<int>(blockIdx.x));
+    if (work >= c.num_work) break;
     const WorkTile t = work_tile<KV>(c, args, work, gbase, tcount);
     if (is_load_warp) load_q(c, t, tiles, tm);
 #pragma unroll
