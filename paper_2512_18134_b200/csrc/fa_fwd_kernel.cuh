@@ -77,6 +77,9 @@ constexpr int kPolyEvery = TWFA_POLY_EVERY;  // 1 in kPolyEvery exp2 pairs on th
 // iterations need no O correction. The final O / l is unchanged in exact
 // arithmetic (m cancels); bf16 P and fp32 l stay far from overflow.
 constexpr float kRescaleLog2 = 8.0f;
+#ifndef TWFA_SOFTMAX_TOKEN
+#define TWFA_SOFTMAX_TOKEN 0  // measured: serializing MX+EX of the two tiles is 12% slower (C3)
+#endif
 constexpr uint32_t kIdescPV = idesc_bf16_f32(128, kHeadDim, 1);  // TMEM P, MN-major V
 
 struct __align__(8) FaBarriers {
@@ -89,6 +92,7 @@ struct __align__(8) FaBarriers {
   uint64_t o_ready[TWFA_MAX_TILES][2], o_done[TWFA_MAX_TILES][2];
   uint64_t st_full[TWFA_MAX_TILES][2], st_empty[TWFA_MAX_TILES][2];
   uint64_t l_full[TWFA_MAX_TILES], l_empty[TWFA_MAX_TILES];
+  uint64_t sm_tok[TWFA_MAX_TILES];  // softmax order token (TWFA_SOFTMAX_TOKEN)
   uint32_t tmem_base;
 };
 
@@ -268,6 +272,10 @@ __device__ __forceinline__ void wr(float (&a)[TWFA_MAX_TILES], int k, float x) {
 // (compile-time constants in the specialized kernels).
 struct Rings {
   int kd, vd, kpf, vpf;
+  // softmax order token (TWFA_SOFTMAX_TOKEN): the EX ops share the MUFU unit
+  // and the schedule orders them inside the trip (ex_ring, slot order); the
+  // softmax warpgroups then run MX_k + EX_k one after the other in that order
+  int ring_len, ring0, ring1;
 };
 
 struct Maps {
@@ -416,7 +424,9 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
       const int limit = valid_keys<KV>(args, row, it * KV);
       const bool mask = !__all_sync(0xffffffffu, limit >= KV);
       uint32_t srow[KV];
+      const bool tok = TWFA_SOFTMAX_TOKEN && rg.ring_len == 2 && (op.flags & TWFA_OPF_FUSE_NEXT);
       if (op.kind == TWFA_OP_MX) {
+        if (tok) mbar_wait(&bar.sm_tok[k], (g & 1) ^ (k == rg.ring0 ? 1u : 0u));
         mbar_wait(&bar.s_full[k][b], pb);
         trace_mark<kTrace>(tr, 4);
         tc_fence_after();
@@ -452,6 +462,7 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
       wr(st.l_run, k, rd(st.l_run, k) * rd(st.alpha, k) + sum);
       tc_fence_before();
       warp_arrive(&bar.p_full[k][b]);
+      if (tok) warp_arrive(&bar.sm_tok[k == rg.ring0 ? rg.ring1 : rg.ring0]);
       if (it == N - 1) {
         mbar_wait(&bar.l_empty[k], (t.tcount & 1) ^ 1);
         g_sh.lbuf[k][0][c.quad * 32 + lane] = m_run;
@@ -578,6 +589,7 @@ __device__ __forceinline__ FaCtx fa_setup(int tiles, int kd, int vd, int load_wa
         mbar_init(&bar.st_full[k][j], 4);
         mbar_init(&bar.st_empty[k][j], 4);
       }
+      mbar_init(&bar.sm_tok[k], 4);
       mbar_init(&bar.l_full[k], 4);
       mbar_init(&bar.l_empty[k], 4);
     }
@@ -662,7 +674,8 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
     if (j == 0) g_sh.prog_len[w] = plan.prog_len[w];
   }
   const FaCtx c = fa_setup<KV>(plan.num_tiles, plan.k_depth, plan.v_depth, plan.load_warp, args, tm, smem_raw);
-  const Rings rg{plan.k_depth, plan.v_depth, plan.k_prefetch, plan.v_prefetch};
+  const Rings rg{plan.k_depth, plan.v_depth, plan.k_prefetch, plan.v_prefetch, plan.ex_ring_len, plan.ex_ring[0],
+                 plan.ex_ring[1]};
   const bool heavy = (plan.heavy_wg_mask >> (c.warp >> 2)) & 1;
   const int heavy_wgs = __popc(plan.heavy_wg_mask);
   if (heavy) {
@@ -711,7 +724,9 @@ template <int I, int W, bool kTrace, int... J>
 __device__ __forceinline__ void spec_trip(int r, const FaCtx& c, const WorkTile& t, WarpState& st, const Maps& tm,
                                           const FaArgs& args, std::integer_sequence<int, J...>) {
   constexpr bool kHeavy = (TWFA_PLAN(I).heavy_wg_mask >> (W / 4)) & 1;
-  constexpr Rings rg{TWFA_PLAN(I).k_depth, TWFA_PLAN(I).v_depth, TWFA_PLAN(I).k_prefetch, TWFA_PLAN(I).v_prefetch};
+  constexpr Rings rg{TWFA_PLAN(I).k_depth,    TWFA_PLAN(I).v_depth,    TWFA_PLAN(I).k_prefetch,
+                     TWFA_PLAN(I).v_prefetch, TWFA_PLAN(I).ex_ring_len, TWFA_PLAN(I).ex_ring[0],
+                     TWFA_PLAN(I).ex_ring[1]};
   (exec_op<TWFA_PLAN(I).kv_tile, kHeavy, kTrace>(spec_op<I, W, J>(), r, c, t, st, rg, tm, args), ...);
 }
 
@@ -765,7 +780,8 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
     set_register_class<true>(heavy_wgs);
     run_interp<KV, true, kTrace>(c, tm, args, TWFA_PLAN(I).num_tiles, TWFA_PLAN(I).max_stage, TWFA_PLAN(I).load_warp,
                              cr_warp, Rings{TWFA_PLAN(I).k_depth, TWFA_PLAN(I).v_depth, TWFA_PLAN(I).k_prefetch,
-                                            TWFA_PLAN(I).v_prefetch});
+                                            TWFA_PLAN(I).v_prefetch, TWFA_PLAN(I).ex_ring_len,
+                                            TWFA_PLAN(I).ex_ring[0], TWFA_PLAN(I).ex_ring[1]});
   } else {
     set_register_class<false>(heavy_wgs);
     spec_dispatch_light<I, kTrace>(c, tm, args, std::make_integer_sequence<int, nw>{});
