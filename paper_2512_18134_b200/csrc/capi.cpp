@@ -126,7 +126,9 @@ int fa_fwd_impl(const twfa_plan* plan, const void* q, const void* k, const void*
   const CUtensorMap tq = make_map(q, 3, dims, strides, box_q);
   const CUtensorMap tk = make_map(k, 3, dims, strides, box_kv);
   const CUtensorMap tv = make_map(v, 3, dims, strides, box_kv);
+  const CUtensorMap to = make_map(o, 3, dims, strides, box_q);
   twfa::FaArgs a{};
+  a.tm_o = to;
   a.o = static_cast<__nv_bfloat16*>(o);
   a.lse = lse;
   a.trace = trace;

@@ -11,6 +11,10 @@
 namespace twfa {
 
 struct FaArgs {
+  // O as a TMA map (d, S, B*H), 64x128 boxes, SWIZZLE_128B: the epilogue
+  // stages each 128x64 half-tile in shared memory and stores it with one
+  // bulk tensor copy (kernel parameter space keeps the 64-byte alignment)
+  alignas(64) CUtensorMap tm_o;
   __nv_bfloat16* o;    // [B, H, S, 128]
   float* lse;          // [B, H, S] natural log-sum-exp, or nullptr
   uint32_t* trace;     // per-warp issue records of CTA 0 (debug), or nullptr

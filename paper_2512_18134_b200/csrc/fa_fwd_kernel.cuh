@@ -77,6 +77,9 @@ constexpr int kPolyEvery = TWFA_POLY_EVERY;  // 1 in kPolyEvery exp2 pairs on th
 // iterations need no O correction. The final O / l is unchanged in exact
 // arithmetic (m cancels); bf16 P and fp32 l stay far from overflow.
 constexpr float kRescaleLog2 = 8.0f;
+#ifndef TWFA_TMA_EPILOGUE
+#define TWFA_TMA_EPILOGUE 1
+#endif
 #ifndef TWFA_SOFTMAX_TOKEN
 #define TWFA_SOFTMAX_TOKEN 0  // measured: serializing MX+EX of the two tiles is 12% slower (C3)
 #endif
@@ -212,6 +215,7 @@ struct FaCtx {
   uint8_t* q_smem;
   uint8_t* k_smem;
   uint8_t* v_smem;
+  uint8_t* o_smem;  // 16 KiB epilogue staging (one 128 x 64 bf16 half-tile, SW128)
   uint32_t tmem;
   uint32_t warp, lane, quad, lane_off;
   int S, BH, q_blocks, num_work;
@@ -504,6 +508,40 @@ __device__ __forceinline__ void epilogue(const FaCtx& c, const WorkTile& t, int 
   tc_fence_after();
   const int row = t.q0 + k * kBlockQ + c.quad * 32 + lane;
   const float inv = l > 0.f ? 1.f / l : 0.f;
+#if TWFA_TMA_EPILOGUE
+  // two 128 x 64 halves through the swizzled staging buffer and a bulk
+  // tensor store each (rows past S are clipped by the tensor map): the
+  // epilogue issues 16 shared stores per thread instead of 16 scattered
+  // global ones, which otherwise flood the MIO queue the TMA / MMA warp
+  // shares at the work-tile boundary
+  const uint32_t wg_bar = 1 + (c.warp >> 2);  // named barrier of this warpgroup
+  const bool leader = (c.warp & 3u) == 0 && lane == 0;
+  const uint32_t r = c.quad * 32 + lane;  // row inside the sub-tile
+#pragma unroll 1
+  for (int h = 0; h < 2; ++h) {
+    uint32_t v[64];
+    tmem_ld32(c.tmem + c.lane_off + 256 + k * 128 + h * 64, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+    tmem_ld32(c.tmem + c.lane_off + 256 + k * 128 + h * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+    tmem_ld_wait();
+    const uint32_t rbase = smem_u32(c.o_smem) + r * 128;
+#pragma unroll
+    for (int ch = 0; ch < 8; ++ch) {  // 16-byte chunk ch of the row, SW128: chunk ^ (row % 8)
+      st_shared_v4(rbase + ((ch ^ (r & 7)) << 4),
+                   pack_bf16(__uint_as_float(v[8 * ch + 0]) * inv, __uint_as_float(v[8 * ch + 1]) * inv),
+                   pack_bf16(__uint_as_float(v[8 * ch + 2]) * inv, __uint_as_float(v[8 * ch + 3]) * inv),
+                   pack_bf16(__uint_as_float(v[8 * ch + 4]) * inv, __uint_as_float(v[8 * ch + 5]) * inv),
+                   pack_bf16(__uint_as_float(v[8 * ch + 6]) * inv, __uint_as_float(v[8 * ch + 7]) * inv));
+    }
+    fence_proxy_async_shared();
+    named_bar_sync(wg_bar, 128);
+    if (leader) {
+      tma_store_3d(&args.tm_o, c.o_smem, h * 64, t.q0 + k * kBlockQ, t.bh);
+      bulk_commit();
+      bulk_wait_read();  // the staging buffer is reusable
+    }
+    named_bar_sync(wg_bar, 128);
+  }
+#else
   __nv_bfloat16* orow = args.o + (static_cast<int64_t>(t.bh) * c.S + row) * kHeadDim;
 #pragma unroll 1
   for (int cc = 0; cc < 4; ++cc) {
@@ -523,6 +561,7 @@ __device__ __forceinline__ void epilogue(const FaCtx& c, const WorkTile& t, int 
       }
     }
   }
+#endif
   if (args.lse != nullptr && row < c.S)
     args.lse[static_cast<int64_t>(t.bh) * c.S + row] = (m + __log2f(l)) * 0.69314718055994531f;
   tc_fence_before();
@@ -571,6 +610,7 @@ __device__ __forceinline__ FaCtx fa_setup(int tiles, int kd, int vd, int load_wa
   c.q_smem = smem;
   c.k_smem = c.q_smem + tiles * kTileBytes;
   c.v_smem = c.k_smem + kd * Kv<KV>::tile;
+  c.o_smem = c.v_smem + vd * Kv<KV>::tile;
   FaBarriers& bar = g_sh.bar;
   c.warp = warp_id();
   c.lane = lane_id();
@@ -629,6 +669,7 @@ __device__ __forceinline__ FaCtx fa_setup(int tiles, int kd, int vd, int load_wa
 }
 
 __device__ __forceinline__ void fa_teardown(const FaCtx& c) {
+  if (c.lane == 0) bulk_wait_all();  // epilogue bulk stores of this warp (if any) are complete
   tc_fence_before();
   __syncthreads();
   if (c.warp == 0) {

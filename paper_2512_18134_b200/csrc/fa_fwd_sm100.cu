@@ -10,7 +10,8 @@ namespace twfa {
 size_t fa_fwd_smem_bytes(const TwfaDevicePlan& plan) {
   // dynamic part only: tile buffers (+ alignment slack); FaShared is static
   const size_t kv_bytes = static_cast<size_t>(plan.kv_tile) * kHeadDim * 2;
-  return 1024 + static_cast<size_t>(plan.num_tiles) * kTileBytes + (plan.k_depth + plan.v_depth) * kv_bytes;
+  // + 16 KiB epilogue staging (one 128 x 64 bf16 SW128 half-tile)
+  return 1024 + static_cast<size_t>(plan.num_tiles) * kTileBytes + (plan.k_depth + plan.v_depth) * kv_bytes + 16384;
 }
 
 const char* fa_fwd_kernel_name(const TwfaDevicePlan& plan) {

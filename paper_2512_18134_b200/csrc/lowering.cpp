@@ -413,9 +413,16 @@ void derive(LoweredSchedule& s) {
   p.kv_tile = 128 / p.s_depth;
   // smem: Q (tiles x 32 KiB) + K ring + V ring of kv_tile-key slots
   const int64_t kv_bytes = static_cast<int64_t>(p.kv_tile) * 256;
-  const int64_t smem = 32768LL * tiles + kv_bytes * (p.k_depth + p.v_depth);
+  // + 16 KiB epilogue staging; 227 KiB per CTA minus the static state
+  // (barriers, row statistics, trip programs ~10 KiB) and alignment slack
+  const int64_t smem = 32768LL * tiles + kv_bytes * (p.k_depth + p.v_depth) + 16384;
   if (p.k_depth > 4 || p.v_depth > 4) throw DomainError("ring depth above 4");
-  if (smem > 200 * 1024) throw DomainError("ring depths exceed shared memory");
+  if (smem > 216 * 1024) throw DomainError("ring depths exceed shared memory");
+  // one epilogue staging buffer: the sub-tiles' corrections (and with them
+  // the epilogues) must run on one warpgroup
+  for (int k = 1; k < tiles; ++k)
+    if (p.cr_warp[k] != p.cr_warp[0])
+      throw DomainError("CR ops of all Q sub-tiles must share a warpgroup (one epilogue staging buffer)");
 }
 
 }  // namespace
