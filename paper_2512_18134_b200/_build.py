@@ -107,7 +107,8 @@ def stale():
         return True
     t = os.path.getmtime(LIB)
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f != "gen"] + [
-        os.path.join(ROOT, "include", "twfa.h"), os.path.join(PKG, "host", "twfa_run.cpp")]
+        os.path.join(ROOT, "include", "twfa.h"), os.path.join(PKG, "host", "twfa_run.cpp"),
+        os.path.join(PKG, "host", "twfa_pybind.cpp")]
     deps += [p for _, a, b in specializations() for p in (a, b)]
     if not os.path.exists(HOST_TOOL):
         return True
@@ -151,9 +152,24 @@ def build(force=False, verbose=False, ptxas_info=False, defines=(), out=None):
     shutil.move(tmp, lib)
     if out is None and not defines:
         build_host_tool(verbose)
+        build_pybind(verbose)
     if ptxas_info:
         print(log)
     return lib
+
+
+def build_pybind(verbose=False):
+    """_twfa: the pybind11 module over the C ABI (host/twfa_pybind.cpp), the
+    counterpart of the reference's _weftsched; rpath $ORIGIN to libtwfa.so."""
+    import sysconfig
+    import pybind11
+    ext = sysconfig.get_config_var("EXT_SUFFIX")
+    out = os.path.join(PKG, "_twfa" + ext)
+    cmd = [host_cxx(), "-std=c++17", "-O2", "-Wall", "-shared", "-fPIC", os.path.join(PKG, "host", "twfa_pybind.cpp"),
+           "-I" + os.path.join(ROOT, "include"), "-I" + sysconfig.get_paths()["include"], "-I" + pybind11.get_include(),
+           "-L" + PKG, "-ltwfa", "-Wl,-rpath,$ORIGIN", "-o", out]
+    run(cmd, verbose)
+    return out
 
 
 def build_host_tool(verbose=False):

@@ -80,3 +80,30 @@ def test_host_tool_exit_codes(twfa):
     r = subprocess.run([tool, "describe", prob, sol], capture_output=True, text=True)
     assert r.returncode == 0
     assert json.loads(r.stdout)["I"] == json.loads(open(sol).read())["I"]
+
+
+def _pybind(twfa):
+    import importlib
+    import sys
+    from paper_2512_18134_b200 import _build
+    pkg = os.path.dirname(_build.LIB)
+    if not any(f.startswith("_twfa") for f in os.listdir(pkg)):
+        _build.build_pybind()
+    if pkg not in sys.path:
+        sys.path.insert(0, pkg)
+    return importlib.import_module("_twfa")
+
+
+def test_pybind_module_mirrors_reference_conventions(twfa):
+    """_twfa (pybind11 over the C ABI) is JSON in / dict out like the
+    reference's _weftsched (module.cpp:219-249); bad documents raise
+    ValueError (test_smoke.py:80-82)."""
+    import pytest
+    m = _pybind(twfa)
+    prob, sol = twfa.load_schedule("fa_fwd")
+    d = m.describe(prob, sol)
+    assert d["I"] == json.loads(sol)["I"] and d == twfa.Plan(prob, sol).describe()
+    with pytest.raises(ValueError, match="machine"):
+        m.Plan("{}", "{}")
+    with pytest.raises(ValueError, match="unknown key"):
+        m.Plan(prob, json.dumps(dict(json.loads(sol), bogus=1)))

@@ -156,3 +156,23 @@ def test_double_buffered_s_schedule_matches_oracle(twfa, S, causal):
     p = twfa.Plan(*twfa.load_schedule("fa_fwd_ring2"))
     assert p.describe()["kv_tile"] == 64
     _check(twfa, p, 1, 2, S, causal, 12)
+
+
+def test_pybind_module_runs_the_same_kernel(twfa, plan):
+    """The pybind layer (_twfa) and the ctypes layer call the same C ABI:
+    bit-identical O on the same inputs."""
+    import sys
+    import os
+    from paper_2512_18134_b200 import _build
+    pkg = os.path.dirname(_build.LIB)
+    if pkg not in sys.path:
+        sys.path.insert(0, pkg)
+    import _twfa
+    q, k, v = (x.cuda() for x in _inputs(1, 2, 640, 128, 13))
+    p = _twfa.Plan(*twfa.load_schedule("fa_fwd"))
+    o = torch.empty_like(q)
+    p.fa_fwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), B=1, H=2, S=640, scale=128 ** -0.5,
+             stream=torch.cuda.current_stream().cuda_stream)
+    ref = twfa.fa_fwd(plan, q, k, v)
+    torch.cuda.synchronize()
+    assert torch.equal(o, ref)
