@@ -84,6 +84,7 @@ constexpr float kRescaleLog2 = 8.0f;
 #define TWFA_SOFTMAX_TOKEN 0  // measured: serializing MX+EX of the two tiles is 12% slower (C3)
 #endif
 constexpr uint32_t kIdescPV = idesc_bf16_f32(128, kHeadDim, 1);  // TMEM P, MN-major V
+constexpr uint32_t kIdescS64 = idesc_bf16_f32(128, 64, 0);       // split S: one 64-key half
 
 struct __align__(8) FaBarriers {
   uint64_t q_full[TWFA_MAX_TILES], q_empty[TWFA_MAX_TILES];
@@ -96,6 +97,8 @@ struct __align__(8) FaBarriers {
   uint64_t st_full[TWFA_MAX_TILES][2], st_empty[TWFA_MAX_TILES][2];
   uint64_t l_full[TWFA_MAX_TILES], l_empty[TWFA_MAX_TILES];
   uint64_t sm_tok[TWFA_MAX_TILES];  // softmax order token (TWFA_SOFTMAX_TOKEN)
+  uint64_t s_half[TWFA_MAX_TILES];  // split S: SA_k committed
+  uint64_t s_read[TWFA_MAX_TILES];  // split S: MX_k has the S row in registers
   uint32_t tmem_base;
 };
 
@@ -280,6 +283,7 @@ struct Rings {
   // and the schedule orders them inside the trip (ex_ring, slot order); the
   // softmax warpgroups then run MX_k + EX_k one after the other in that order
   int ring_len, ring0, ring1;
+  int split;  // S_k issued as SA_k + SB_k; P_k at S columns 64-127
 };
 
 struct Maps {
@@ -339,7 +343,35 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
   const uint32_t b = g % G::depth, pb = (g / G::depth) & 1;  // S buffer of this iteration, its phase
   uint32_t* tr = trace_begin<kTrace>(args, warp, st.trace_n, op.node, it, r);
 
-  if (op.kind == TWFA_OP_S) {
+  if (op.kind == TWFA_OP_SA || op.kind == TWFA_OP_SB) {
+    // split S_k (single 128-key S tile): SA_k = keys 0-63 into columns 0-63,
+    // issued once MX_k(g-1) holds its row in registers; SB_k = keys 64-127
+    // into columns 64-127, where P_k(g-1) lives, after PV_k(g-1)
+    const bool a = op.kind == TWFA_OP_SA;
+    const uint32_t s = g % rg.kd;
+    if (it == 0) mbar_wait(&bar.q_full[k], t.tcount & 1);
+    if (a && g >= 1)
+      mbar_wait_all(&bar.k_full[s], (g / rg.kd) & 1, &bar.s_read[k], (g - 1) & 1);
+    else if (!a && g >= 1 && !(op.flags & TWFA_OPF_INORDER))
+      mbar_wait_all(&bar.k_full[s], (g / rg.kd) & 1, &bar.o_done[k][0], (g - 1) & 1);
+    else
+      mbar_wait(&bar.k_full[s], (g / rg.kd) & 1);
+    trace_mark<kTrace>(tr, 4);
+    tc_fence_after();
+    const uint32_t qa = smem_u32(c.q_smem + k * kTileBytes);
+    const uint32_t ka = smem_u32(c.k_smem + s * G::tile) + (a ? 0u : 64u * 128u);  // K rows 64.. (8 SW128 atoms)
+    const uint32_t d_s = tmem + k * 128 + (a ? 0u : 64u);
+    if (elect_one()) {
+#pragma unroll
+      for (int kk = 0; kk < kHeadDim / 16; ++kk)
+        mma_ss(d_s, sdesc_sw128(qa + (kk >> 2) * kHalfBytes + (kk & 3) * 32, 16, 1024),
+               sdesc_sw128(ka + (kk >> 2) * G::half + (kk & 3) * 32, 16, 1024), kIdescS64, kk > 0);
+      mma_commit(a ? &bar.s_half[k] : &bar.s_full[k][0]);
+      mma_commit(&bar.k_empty[s]);
+      if (it == N - 1) mma_commit(&bar.q_empty[k]);
+    }
+    __syncwarp();
+  } else if (op.kind == TWFA_OP_S) {
     // MMA issue: every lane waits and computes the (warp-uniform)
     // descriptors, so they live in uniform registers; one elected lane
     // issues the tcgen05.mma chain and the commits
@@ -372,7 +404,7 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
     trace_mark<kTrace>(tr, 4);
     tc_fence_after();
     const uint32_t va = smem_u32(c.v_smem + s * G::tile);
-    const uint32_t d_o = tmem + 256 + k * 128, a_p = tmem + k * 128 + b * KV;
+    const uint32_t d_o = tmem + 256 + k * 128, a_p = tmem + k * 128 + b * KV + (rg.split ? 64u : 0u);
     const uint32_t acc0 = it > 0 ? 1u : 0u;
     if (elect_one()) {
 #pragma unroll
@@ -431,10 +463,17 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
       const bool tok = TWFA_SOFTMAX_TOKEN && rg.ring_len == 2 && (op.flags & TWFA_OPF_FUSE_NEXT);
       if (op.kind == TWFA_OP_MX) {
         if (tok) mbar_wait(&bar.sm_tok[k], (g & 1) ^ (k == rg.ring0 ? 1u : 0u));
-        mbar_wait(&bar.s_full[k][b], pb);
+        if (rg.split)
+          mbar_wait_all(&bar.s_half[k], g & 1, &bar.s_full[k][b], pb);
+        else
+          mbar_wait(&bar.s_full[k][b], pb);
         trace_mark<kTrace>(tr, 4);
         tc_fence_after();
         load_row<KV>(taddr, srow);
+        if (rg.split) {  // the row is in registers: SA_k(g+1) may overwrite columns 0-63
+          tc_fence_before();
+          warp_arrive(&bar.s_read[k]);
+        }
         if (mask) mask_row<KV>(srow, limit);
         const float mx = row_max<KV>(srow);
         const float m_old = rd(st.m_run, k);
@@ -461,8 +500,9 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
       }
       const float m_run = rd(st.m_run, k);
       const float m_safe = m_run == -INFINITY ? 0.f : m_run;
-      const float sum = mask ? exp_store_row<KV, true>(srow, taddr, c.scale_log2, m_safe, &bar.p_half[k][b])
-                             : exp_store_row<KV, false>(srow, taddr, c.scale_log2, m_safe, &bar.p_half[k][b]);
+      const uint32_t paddr = taddr + (rg.split ? 64u : 0u);  // P_k columns
+      const float sum = mask ? exp_store_row<KV, true>(srow, paddr, c.scale_log2, m_safe, &bar.p_half[k][b])
+                             : exp_store_row<KV, false>(srow, paddr, c.scale_log2, m_safe, &bar.p_half[k][b]);
       wr(st.l_run, k, rd(st.l_run, k) * rd(st.alpha, k) + sum);
       tc_fence_before();
       warp_arrive(&bar.p_full[k][b]);
@@ -601,7 +641,7 @@ __device__ __forceinline__ void work_loop(const FaCtx& c, const FaArgs& args, co
 
 // Shared prologue of both kernels: smem carve-up, barriers, TMEM allocation.
 template <int KV>
-__device__ __forceinline__ FaCtx fa_setup(int tiles, int kd, int vd, int load_warp, const FaArgs& args,
+__device__ __forceinline__ FaCtx fa_setup(int tiles, int kd, int vd, int load_warp, int split, const FaArgs& args,
                                           const Maps& tm, uint8_t* smem_raw) {
   // 1 KiB alignment of the tile buffers (SW128 atoms) by offset arithmetic on
   // the shared window address, keeping the pointer in the shared space
@@ -617,7 +657,7 @@ __device__ __forceinline__ FaCtx fa_setup(int tiles, int kd, int vd, int load_wa
   if (threadIdx.x == 0) {
     for (int k = 0; k < tiles; ++k) {
       mbar_init(&bar.q_full[k], 1);
-      mbar_init(&bar.q_empty[k], 1);
+      mbar_init(&bar.q_empty[k], split ? 2 : 1);  // the last S GEMM(s) of the tile read Q_k
       for (int b = 0; b < 2; ++b) {
         mbar_init(&bar.s_full[k][b], 1);
         mbar_init(&bar.p_full[k][b], 4);  // warp arrivals of a warpgroup
@@ -630,12 +670,14 @@ __device__ __forceinline__ FaCtx fa_setup(int tiles, int kd, int vd, int load_wa
         mbar_init(&bar.st_empty[k][j], 4);
       }
       mbar_init(&bar.sm_tok[k], 4);
+      mbar_init(&bar.s_half[k], 1);
+      mbar_init(&bar.s_read[k], 4);
       mbar_init(&bar.l_full[k], 4);
       mbar_init(&bar.l_empty[k], 4);
     }
     for (int s = 0; s < kd; ++s) {
       mbar_init(&bar.k_full[s], 1);
-      mbar_init(&bar.k_empty[s], tiles);
+      mbar_init(&bar.k_empty[s], tiles * (split ? 2 : 1));
     }
     for (int s = 0; s < vd; ++s) {
       mbar_init(&bar.v_full[s], 1);
@@ -714,9 +756,10 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
     if (j < plan.prog_len[w]) g_sh.prog[w][j] = plan.ops[plan.prog[w][j]];
     if (j == 0) g_sh.prog_len[w] = plan.prog_len[w];
   }
-  const FaCtx c = fa_setup<KV>(plan.num_tiles, plan.k_depth, plan.v_depth, plan.load_warp, args, tm, smem_raw);
-  const Rings rg{plan.k_depth, plan.v_depth, plan.k_prefetch, plan.v_prefetch, plan.ex_ring_len, plan.ex_ring[0],
-                 plan.ex_ring[1]};
+  const FaCtx c =
+      fa_setup<KV>(plan.num_tiles, plan.k_depth, plan.v_depth, plan.load_warp, plan.s_split, args, tm, smem_raw);
+  const Rings rg{plan.k_depth,   plan.v_depth,    plan.k_prefetch, plan.v_prefetch,
+                 plan.ex_ring_len, plan.ex_ring[0], plan.ex_ring[1], plan.s_split};
   const bool heavy = (plan.heavy_wg_mask >> (c.warp >> 2)) & 1;
   const int heavy_wgs = __popc(plan.heavy_wg_mask);
   if (heavy) {
@@ -767,7 +810,7 @@ __device__ __forceinline__ void spec_trip(int r, const FaCtx& c, const WorkTile&
   constexpr bool kHeavy = (TWFA_PLAN(I).heavy_wg_mask >> (W / 4)) & 1;
   constexpr Rings rg{TWFA_PLAN(I).k_depth,    TWFA_PLAN(I).v_depth,    TWFA_PLAN(I).k_prefetch,
                      TWFA_PLAN(I).v_prefetch, TWFA_PLAN(I).ex_ring_len, TWFA_PLAN(I).ex_ring[0],
-                     TWFA_PLAN(I).ex_ring[1]};
+                     TWFA_PLAN(I).ex_ring[1], TWFA_PLAN(I).s_split};
   (exec_op<TWFA_PLAN(I).kv_tile, kHeavy, kTrace>(spec_op<I, W, J>(), r, c, t, st, rg, tm, args), ...);
 }
 
@@ -811,7 +854,7 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
   constexpr int cr_warp[TWFA_MAX_TILES] = {TWFA_PLAN(I).cr_warp[0], TWFA_PLAN(I).cr_warp[1]};
   constexpr int KV = TWFA_PLAN(I).kv_tile;
   const FaCtx c = fa_setup<KV>(TWFA_PLAN(I).num_tiles, TWFA_PLAN(I).k_depth, TWFA_PLAN(I).v_depth,
-                               TWFA_PLAN(I).load_warp, args, tm, smem_raw);
+                               TWFA_PLAN(I).load_warp, TWFA_PLAN(I).s_split, args, tm, smem_raw);
   // the register class is per warpgroup; the warp roles of each class are
   // dispatched inside its branch so ptxas allocates them under that budget
   constexpr int mask = TWFA_PLAN(I).heavy_wg_mask;
@@ -822,7 +865,8 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
     run_interp<KV, true, kTrace>(c, tm, args, TWFA_PLAN(I).num_tiles, TWFA_PLAN(I).max_stage, TWFA_PLAN(I).load_warp,
                              cr_warp, Rings{TWFA_PLAN(I).k_depth, TWFA_PLAN(I).v_depth, TWFA_PLAN(I).k_prefetch,
                                             TWFA_PLAN(I).v_prefetch, TWFA_PLAN(I).ex_ring_len,
-                                            TWFA_PLAN(I).ex_ring[0], TWFA_PLAN(I).ex_ring[1]});
+                                            TWFA_PLAN(I).ex_ring[0], TWFA_PLAN(I).ex_ring[1],
+                                            TWFA_PLAN(I).s_split});
   } else {
     set_register_class<false>(heavy_wgs);
     spec_dispatch_light<I, kTrace>(c, tm, args, std::make_integer_sequence<int, nw>{});
@@ -834,7 +878,8 @@ bool same_plan(const TwfaDevicePlan& a, const TwfaDevicePlan& b) {
   if (a.family != b.family || a.ii != b.ii || a.max_stage != b.max_stage || a.num_nodes != b.num_nodes ||
       a.num_warps != b.num_warps || a.num_tiles != b.num_tiles || a.k_depth != b.k_depth || a.v_depth != b.v_depth ||
       a.load_warp != b.load_warp || a.k_prefetch != b.k_prefetch || a.v_prefetch != b.v_prefetch ||
-      a.heavy_wg_mask != b.heavy_wg_mask || a.s_depth != b.s_depth || a.kv_tile != b.kv_tile)
+      a.heavy_wg_mask != b.heavy_wg_mask || a.s_depth != b.s_depth || a.kv_tile != b.kv_tile ||
+      a.s_split != b.s_split)
     return false;
   for (int k = 0; k < TWFA_MAX_TILES; ++k)
     if (a.cr_warp[k] != b.cr_warp[k] || a.sm_warp[k] != b.sm_warp[k]) return false;

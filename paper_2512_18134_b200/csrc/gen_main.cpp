@@ -52,7 +52,7 @@ std::string emit(int id, const std::string& name, const twfa::LoweredSchedule& s
   o << "    .num_warps = " << p.num_warps << ", .num_tiles = " << p.num_tiles << ", .k_depth = " << p.k_depth
     << ", .v_depth = " << p.v_depth << ", .load_warp = " << p.load_warp << ",\n";
   o << "    .k_prefetch = " << p.k_prefetch << ", .v_prefetch = " << p.v_prefetch << ", .s_depth = " << p.s_depth
-    << ", .kv_tile = " << p.kv_tile
+    << ", .kv_tile = " << p.kv_tile << ", .s_split = " << p.s_split
     << ", .cr_warp = " << ints(p.cr_warp, TWFA_MAX_TILES) << ", .sm_warp = " << ints(p.sm_warp, TWFA_MAX_TILES)
     << ", .mma_warp = " << p.mma_warp << ",\n";
   o << "    .heavy_wg_mask = " << p.heavy_wg_mask << ", .ex_ring_len = " << p.ex_ring_len

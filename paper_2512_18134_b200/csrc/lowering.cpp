@@ -179,8 +179,8 @@ bool classify(const std::string& id, uint8_t& kind, uint8_t& tile) {
                               {"LDB", TWFA_OP_LDB}, {"MMA", TWFA_OP_MMA}};
   for (const Pfx& f : fixed)
     if (id == f.p) { kind = f.k; tile = 0; return true; }
-  static const Pfx tiled[] = {{"MX", TWFA_OP_MX}, {"EX", TWFA_OP_EX}, {"CR", TWFA_OP_CR},
-                              {"PV", TWFA_OP_PV}, {"S", TWFA_OP_S}};
+  static const Pfx tiled[] = {{"MX", TWFA_OP_MX}, {"EX", TWFA_OP_EX}, {"CR", TWFA_OP_CR}, {"PV", TWFA_OP_PV},
+                              {"SA", TWFA_OP_SA}, {"SB", TWFA_OP_SB}, {"S", TWFA_OP_S}};
   for (const Pfx& f : tiled) {
     const size_t l = std::strlen(f.p);
     if (id.size() == l + 1 && id.compare(0, l, f.p) == 0 && id[l] >= '0' && id[l] < '0' + TWFA_MAX_TILES) {
@@ -304,7 +304,8 @@ void derive(LoweredSchedule& s) {
     return static_cast<int32_t>(pf);
   };
 
-  const bool is_fa = kinds.count(TWFA_OP_S) && kinds.count(TWFA_OP_PV);
+  const bool is_fa = (kinds.count(TWFA_OP_S) || (kinds.count(TWFA_OP_SA) && kinds.count(TWFA_OP_SB))) &&
+                     kinds.count(TWFA_OP_PV);
   const bool is_gemm = kinds.count(TWFA_OP_MMA) && kinds.count(TWFA_OP_LDA) && kinds.count(TWFA_OP_LDB);
   if (is_fa == is_gemm) throw DomainError("graph is neither the FA-forward nor the GEMM loop");
   if (is_gemm) {
@@ -329,17 +330,22 @@ void derive(LoweredSchedule& s) {
   }
 
   p.family = TWFA_FAMILY_FA_FWD;
+  // S_k as one GEMM, or split into SA_k + SB_k
+  const bool split = node_id("SA0") >= 0;
+  const char* s_last = split ? "SB" : "S";  // the GEMM that overwrites P_k's columns
+  p.s_split = split ? 1 : 0;
   int tiles = 0;
-  while (tiles < TWFA_MAX_TILES && node_id("S" + std::to_string(tiles)) >= 0) ++tiles;
-  if (tiles < 1) throw DomainError("FA loop needs S0");
+  while (tiles < TWFA_MAX_TILES && node_id((split ? "SA" : "S") + std::to_string(tiles)) >= 0) ++tiles;
+  if (tiles < 1) throw DomainError("FA loop needs S0 (or SA0, SB0)");
   p.num_tiles = tiles;
   const int ldk = node_id("LDK"), ldv = node_id("LDV");
   if (ldk < 0 || ldv < 0) throw DomainError("FA loop needs LDK and LDV");
   for (int k = 0; k < tiles; ++k)
-    for (const char* pre : {"S", "MX", "EX", "CR", "PV"})
-      if (node_id(pre + std::to_string(k)) < 0)
+    for (const char* pre : {"S", "SA", "SB", "MX", "EX", "CR", "PV"})
+      if ((split ? std::string(pre) != "S" : (std::string(pre) != "SA" && std::string(pre) != "SB")) &&
+          node_id(pre + std::to_string(k)) < 0)
         throw DomainError(std::string("FA loop is missing ") + pre + std::to_string(k));
-  if (static_cast<int>(n) != 2 + 5 * tiles) throw DomainError("FA loop has unexpected extra nodes");
+  if (static_cast<int>(n) != 2 + (split ? 6 : 5) * tiles) throw DomainError("FA loop has unexpected extra nodes");
   if (p.ops[ldk].warp_start != p.ops[ldv].warp_start || p.ops[ldk].warp_count != 1)
     throw DomainError("LDK and LDV must be issued by one TMA warp");
   p.load_warp = p.ops[ldk].warp_start;
@@ -351,7 +357,9 @@ void derive(LoweredSchedule& s) {
     const TwfaPlanOp& mx = p.ops[node_id("MX" + std::to_string(k))];
     const TwfaPlanOp& ex = p.ops[node_id("EX" + std::to_string(k))];
     const TwfaPlanOp& cr = p.ops[node_id("CR" + std::to_string(k))];
-    const TwfaPlanOp& sk = p.ops[node_id("S" + std::to_string(k))];
+    const TwfaPlanOp& sk = p.ops[node_id(s_last + std::to_string(k))];
+    if (split && p.ops[node_id("SA" + std::to_string(k))].warp_count != 1)
+      throw DomainError("MMA issue ops are single-warp");
     const TwfaPlanOp& pv = p.ops[node_id("PV" + std::to_string(k))];
     // TMEM lane quadrants: a 128-row tile is touched by 4 warps, one per
     // quadrant (warp % 4), so row-wise ops need an aligned warpgroup.
@@ -376,10 +384,15 @@ void derive(LoweredSchedule& s) {
     if (adjacent) {
       p.ops[mxi].flags |= TWFA_OPF_FUSE_NEXT;
       p.ops[exi].flags |= TWFA_OPF_FUSED;
+    } else if (split) {
+      // SA_k(i+1) may overwrite S columns 0-63 once MX_k(i) has read them:
+      // only a register-resident row (fused MX_k; EX_k) never re-reads S
+      throw DomainError("split S needs MX" + std::to_string(k) + " and EX" + std::to_string(k) +
+                        " back to back on their warpgroup");
     }
     // same issuing warp for S_k and PV_k: the realizability check above
     // guarantees PV_k(i-1) precedes S_k(i) in that warp's program order
-    if (sk.warp_start == pv.warp_start) p.ops[node_id("S" + std::to_string(k))].flags |= TWFA_OPF_INORDER;
+    if (sk.warp_start == pv.warp_start) p.ops[node_id(s_last + std::to_string(k))].flags |= TWFA_OPF_INORDER;
   }
   if (__builtin_popcount(static_cast<unsigned>(p.heavy_wg_mask)) > 2)
     throw DomainError("softmax of more than two warpgroups exceeds the register file");
@@ -404,13 +417,14 @@ void derive(LoweredSchedule& s) {
   p.s_depth = 0;
   for (const LEdge& e : s.edges)
     for (int k = 0; k < tiles; ++k)
-      if (e.src == node_id("PV" + std::to_string(k)) && e.dst == node_id("S" + std::to_string(k))) {
+      if (e.src == node_id("PV" + std::to_string(k)) && e.dst == node_id(s_last + std::to_string(k))) {
         if (p.s_depth != 0 && p.s_depth != e.delta) throw DomainError("sub-tiles disagree on the S ring depth");
         p.s_depth = e.delta;
       }
   if (p.s_depth != 1 && p.s_depth != 2)
     throw DomainError("PV_k -> S_k must carry delta 1 or 2 (S ring depth in tensor memory)");
   p.kv_tile = 128 / p.s_depth;
+  if (split && p.s_depth != 1) throw DomainError("split S is realized with a single 128-key S tile (delta 1)");
   // smem: Q (tiles x 32 KiB) + K ring + V ring of kv_tile-key slots
   const int64_t kv_bytes = static_cast<int64_t>(p.kv_tile) * 256;
   // + 16 KiB epilogue staging; 227 KiB per CTA minus the static state
@@ -469,6 +483,7 @@ std::string describe(const LoweredSchedule& s) {
     rings["K"] = p.k_depth;
     rings["S"] = p.s_depth;
     j["kv_tile"] = p.kv_tile;
+    j["s_split"] = p.s_split;
     rings["V"] = p.v_depth;
     j["prefetch"] = {{"LDK", p.k_prefetch}, {"LDV", p.v_prefetch}};
     j["num_tiles"] = p.num_tiles;

@@ -28,7 +28,12 @@ enum TwfaOpKind : uint8_t {
   TWFA_OP_LDA = 7,  // GEMM: TMA load of the A k-block
   TWFA_OP_LDB = 8,  // GEMM: TMA load of the B k-block
   TWFA_OP_MMA = 9,  // GEMM: D += A B^T over one k-block
-  TWFA_OP_COUNT = 10
+  // S_k as two N = 64 GEMMs: SA_k (keys 0-63 -> columns 0-63) overwrites only
+  // S columns MX_k has already read, SB_k (keys 64-127 -> columns 64-127)
+  // the columns P_k (bf16) is aliased over; see fa_forward_problem(split_s)
+  TWFA_OP_SA = 10,
+  TWFA_OP_SB = 11,
+  TWFA_OP_COUNT = 12
 };
 
 struct alignas(16) TwfaPlanOp {  // 16 bytes: one vector load on the device
@@ -83,6 +88,7 @@ struct TwfaDevicePlan {
   // tiles of kv_tile = 128 / s_depth keys.
   int32_t s_depth;
   int32_t kv_tile;
+  int32_t s_split;  // S_k is SA_k + SB_k (P_k at columns 64-127)
   int32_t cr_warp[TWFA_MAX_TILES];  // warpgroup start running CR_k (+ epilogue of tile k)
   int32_t sm_warp[TWFA_MAX_TILES];  // warpgroup start running MX_k / EX_k
   int32_t mma_warp;                 // GEMM: warp issuing MMA

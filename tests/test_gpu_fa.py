@@ -176,3 +176,13 @@ def test_pybind_module_runs_the_same_kernel(twfa, plan):
     ref = twfa.fa_fwd(plan, q, k, v)
     torch.cuda.synchronize()
     assert torch.equal(o, ref)
+
+
+@pytest.mark.parametrize("S,causal", [(512, False), (640, True), (300, False), (100, True)])
+def test_split_s_schedule_matches_oracle(twfa, S, causal):
+    """fa_fwd_split: S_k issued as SA_k (keys 0-63, after MX_k read the row)
+    and SB_k (keys 64-127, over P_k's columns, after PV_k); P_k at columns
+    64-127."""
+    p = twfa.Plan(*twfa.load_schedule("fa_fwd_split"))
+    assert p.describe()["s_split"] == 1
+    _check(twfa, p, 1, 2, S, causal, 14)

@@ -48,7 +48,7 @@ def edge(src, dst, d, delta=0, blocking=False):
     return e
 
 
-def fa_forward_problem(tc_variable_latency=False, calibrated=False, s_ring=1):
+def fa_forward_problem(tc_variable_latency=False, calibrated=False, s_ring=1, split_s=False):
     """FA-forward loop body on sm_100a: two 128-row Q sub-tiles (k = 0, 1)
     share one 128-key K/V tile per iteration.
 
@@ -71,6 +71,12 @@ def fa_forward_problem(tc_variable_latency=False, calibrated=False, s_ring=1):
     PV_k(i): the edge PV_k -> S_k carries delta = 2 (S_k(i+2) overwrites the
     P_k(i) that PV_k(i) reads). The executor derives the ring depth (and the
     64-key tile) from that delta.
+
+    split_s issues each S_k as two N = 64 GEMMs. SA_k computes keys 0-63
+    into S columns 0-63; it only waits for MX_k(i-1) to hold its row in
+    registers (edge MX_k -> SA_k, delta 1). SB_k computes keys 64-127 into
+    columns 64-127, where P_k (bf16) is aliased; it follows PV_k(i-1)
+    (edge PV_k -> SB_k, delta 1). Half of the next S then overlaps EX_k.
     """
     T = 256  # raw clk per unit (see module docstring)
     # per-op durations in units of T: datasheet throughput (default) or the
@@ -107,16 +113,32 @@ def fa_forward_problem(tc_variable_latency=False, calibrated=False, s_ring=1):
     ]
     edges = []
     for k in (0, 1):
+        if split_s:
+            half = max(1, cost["S"] // 2)
+            nodes += [node(f"SA{k}", "TC", half, footprint={"tmem": kv // 2}),
+                      node(f"SB{k}", "TC", half, footprint={"tmem": kv // 2})]
+            edges += [edge("LDK", f"SA{k}", 0, blocking=True), edge("LDK", f"SB{k}", 0, blocking=True),
+                      edge(f"SA{k}", f"MX{k}", half, blocking=True), edge(f"SB{k}", f"MX{k}", half, blocking=True),
+                      edge(f"MX{k}", f"SA{k}", cost["MX"], delta=1),
+                      edge(f"PV{k}", f"SB{k}", 0, delta=1)]
+        else:
+            nodes += [node(f"S{k}", "TC", cost["S"], footprint={"tmem": kv})]
+            edges += [edge("LDK", f"S{k}", 0, blocking=True), edge(f"S{k}", f"MX{k}", cost["S"], blocking=True),
+                      # S_k(i+1) overwrites the TMEM columns P_k(i) is read from: the
+                      # calibrated model waits for PV_k's completion (cross-warp commit)
+                      edge(f"PV{k}", f"S{k}", cost["PV"] if calibrated else 0, delta=s_ring)]
         nodes += [
-            node(f"S{k}", "TC", cost["S"], footprint={"tmem": kv}),
-            node(f"MX{k}", "ALU", cost["MX"], regs=kv, spill_cost=spill, warps_required=4),
+            # split S: SA_k(i+1) overwrites S columns right after MX_k(i) read them,
+            # so the S row (MX_k's value) cannot be re-read by a consumer on another
+            # warp: a spill cost of a whole EX (reusing an existing cost, so the
+            # normalization is unchanged) keeps EX_k with MX_k
+            node(f"MX{k}", "ALU", cost["MX"], regs=kv, spill_cost=cost["EX"] if split_s else spill,
+                 warps_required=4),
             node(f"EX{k}", "MUFU", cost["EX"], regs=kv // 2, warps_required=4),
             node(f"CR{k}", "FMA", cost["CR"], regs=64, warps_required=4),
             node(f"PV{k}", "TC", cost["PV"], footprint={"tmem": 128}),
         ]
         edges += [
-            edge("LDK", f"S{k}", 0, blocking=True),
-            edge(f"S{k}", f"MX{k}", cost["S"], blocking=True),
             edge(f"MX{k}", f"EX{k}", cost["MX"]),
             edge(f"MX{k}", f"MX{k}", cost["MX"], delta=1),
             edge(f"EX{k}", f"EX{k}", cost["EX"], delta=1),
@@ -126,9 +148,6 @@ def fa_forward_problem(tc_variable_latency=False, calibrated=False, s_ring=1):
             edge(f"CR{k}", f"PV{k}", cost["CR"], blocking=True),
             edge(f"PV{k}", f"CR{k}", cost["PV"], delta=1, blocking=True),
             edge(f"PV{k}", f"PV{k}", cost["PV"], delta=1),
-            # S_k(i+1) overwrites the TMEM columns P_k(i) is read from: the
-            # calibrated model waits for PV_k's completion (cross-warp commit)
-            edge(f"PV{k}", f"S{k}", cost["PV"] if calibrated else 0, delta=s_ring),
         ]
     if tc_variable_latency:
         # tcgen05.mma is asynchronous: its completion is only observed through
@@ -239,6 +258,8 @@ def main():
         # comparison: MMAs as fixed-latency ops (the solver scatters them over warps)
         "fa_fwd_fixedtc": (fa_forward_problem(), 2, None),
         "fa_fwd_cal": (fa_forward_problem(calibrated=True), 2, 9),
+        # production model with S_k split into SA_k + SB_k (half of S(i+1) overlaps EX(i))
+        "fa_fwd_split": (fa_forward_problem(tc_variable_latency=True, calibrated=True, split_s=True), 2, 9),
         # double-buffered S (64-key K/V tiles): S_k(i+1) independent of PV_k(i)
         "fa_fwd_ring2": (fa_forward_problem(tc_variable_latency=True, s_ring=2), 4, None),
     }
