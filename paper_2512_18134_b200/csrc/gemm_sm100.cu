@@ -82,48 +82,53 @@ __global__ void __launch_bounds__(256, 1)
   const int kblocks = args.K / kBK;
 
   if (warp == static_cast<uint32_t>(plan.load_warp)) {
-    // LDA, LDB: streamed loads into the ring (depth = streaming depth)
-    if (lane == 0) {
-      const uint64_t pol_a = policy_evict_last();
-      const uint64_t pol_b = policy_evict_last();
-      uint32_t g = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        int tm, tn;
-        tile_coords(t, tiles_m, tiles_n, tm, tn);
-        for (int kb = 0; kb < kblocks; ++kb, ++g) {
-          const uint32_t s = g % stages, ph = (g / stages) & 1;
-          mbar_wait(&bar->empty[s], ph ^ 1);
+    // LDA, LDB: streamed loads into the ring (depth = streaming depth).
+    // Warp-uniform arithmetic, one elected lane issues (uniform registers).
+    const uint64_t pol_a = policy_evict_last();
+    const uint64_t pol_b = policy_evict_last();
+    uint32_t g = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      int tm, tn;
+      tile_coords(t, tiles_m, tiles_n, tm, tn);
+      for (int kb = 0; kb < kblocks; ++kb, ++g) {
+        const uint32_t s = g % stages, ph = (g / stages) & 1;
+        mbar_wait(&bar->empty[s], ph ^ 1);
+        uint8_t* sa = smem + s * kStageBytes;
+        if (elect_one()) {
           mbar_arrive_expect_tx(&bar->full[s], kStageBytes);
-          uint8_t* sa = smem + s * kStageBytes;
           tma_load_2d(sa, &tm_a, &bar->full[s], kb * kBK, tm * kBM, pol_a);
           tma_load_2d(sa + kABytes, &tm_b, &bar->full[s], kb * kBK, tn * kBN, pol_b);
         }
+        __syncwarp();
       }
     }
   } else if (warp == static_cast<uint32_t>(plan.mma_warp)) {
-    // MMA: D += A B^T, one 128x256x16 instruction per 16-wide k slice
-    if (lane == 0) {
-      uint32_t g = 0, lt = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
-        const uint32_t acc = lt & 1, acc_ph = (lt >> 1) & 1;
-        mbar_wait(&bar->acc_empty[acc], acc_ph ^ 1);
+    // MMA: D += A B^T, one 128x256x16 instruction per 16-wide k slice.
+    // Every lane waits and computes the (uniform) descriptors; one elected
+    // lane issues, so the operands stay in uniform registers.
+    uint32_t g = 0, lt = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
+      const uint32_t acc = lt & 1, acc_ph = (lt >> 1) & 1;
+      mbar_wait(&bar->acc_empty[acc], acc_ph ^ 1);
+      tc_fence_after();
+      for (int kb = 0; kb < kblocks; ++kb, ++g) {
+        const uint32_t s = g % stages, ph = (g / stages) & 1;
+        mbar_wait(&bar->full[s], ph);
         tc_fence_after();
-        for (int kb = 0; kb < kblocks; ++kb, ++g) {
-          const uint32_t s = g % stages, ph = (g / stages) & 1;
-          mbar_wait(&bar->full[s], ph);
-          tc_fence_after();
-          const uint32_t sa = smem_u32(smem + s * kStageBytes);
-          const uint32_t sb = sa + kABytes;
+        const uint32_t sa = smem_u32(smem + s * kStageBytes);
+        const uint32_t sb = sa + kABytes;
+        if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < kBK / 16; ++kk)
-            mma_ss(tmem + acc * kBN, sdesc_sw128(sa + kk * 32, 16, 1024), sdesc_sw128(sb + kk * 32, 16, 1024), kIdesc,
-                   (kb | kk) != 0);
+            mma_ss(tmem + acc * kBN, sdesc_sw128(sa + kk * 32, 16, 1024), sdesc_sw128(sb + kk * 32, 16, 1024),
+                   kIdesc, (kb | kk) != 0);
           mma_commit(&bar->empty[s]);
         }
-        mma_commit(&bar->acc_full[acc]);
+        __syncwarp();
       }
+      if (elect_one()) mma_commit(&bar->acc_full[acc]);
+      __syncwarp();
     }
-    __syncwarp();
   } else if (warp >= first_epi && warp < first_epi + 4) {
     const uint32_t quad = warp & 3u;
     const uint32_t lane_off = (quad * 32u) << 16;
