@@ -209,7 +209,9 @@ def run_reference(args, world, rank):
     import numpy as np
     from tests import oracle_lib
     threads = os.cpu_count()
-    rows, Hs, Sk, D = 128, 1, S, 128
+    # one step: 1024 query rows of two (b, h) pairs against all S keys
+    # (~8.6 GFLOP at S = 8192: a bounded, representative sample)
+    rows, Hs, Sk, D = 1024, 2, S, 128
     rng = np.random.default_rng(11)
     q = oracle_lib.round_bf16(rng.standard_normal((1, Hs, rows, D), dtype=np.float32))
     k = oracle_lib.round_bf16(rng.standard_normal((1, Hs, Sk, D), dtype=np.float32))
@@ -224,7 +226,7 @@ def run_reference(args, world, rank):
     tflops = flops * args.steps / secs / 1e12
     solver = solver_time()
     sample = (f"per step: fp32 online-softmax host attention (oracle restatement; the reference has no "
-              f"attention numerics) for {rows} query rows x {Sk} keys x d={D} of one (b,h) pair")
+              f"attention numerics) for {rows} query rows x {Sk} keys x d={D} of {Hs} (b,h) pairs")
     line = {
         "impl": "reference", "metric": METRIC, "value": tflops, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
