@@ -80,11 +80,27 @@ constexpr float kRescaleLog2 = 8.0f;
 #ifndef TWFA_TMA_EPILOGUE
 #define TWFA_TMA_EPILOGUE 1
 #endif
+// What-if knobs for sensitivity experiments (timing only; results are WRONG
+// when set): 1 = half the exponentials on MUFU (the rest reuse them),
+// 3 = MX reads half the row
+#ifndef TWFA_WHATIF
+#define TWFA_WHATIF 0
+#endif
+// P_k is handed to PV_k in kPParts parts of 128 / kPParts keys: part j is
+// released once its tcgen05.st completed (checked after the exponentials of
+// part j + 1, so MUFU does not drain), and PV_k issues its K-steps over those
+// keys. Finer parts start PV earlier and leave a shorter tail after EX.
+#ifndef TWFA_P_PARTS
+#define TWFA_P_PARTS 4  // measured: 4 parts >= halves >= 8 parts (C3, C4)
+#endif
+constexpr int kPParts = TWFA_P_PARTS;
+static_assert(kPParts == 2 || kPParts == 4 || kPParts == 8, "P parts");
 #ifndef TWFA_SOFTMAX_TOKEN
 #define TWFA_SOFTMAX_TOKEN 0  // measured: serializing MX+EX of the two tiles is 12% slower (C3)
 #endif
 constexpr uint32_t kIdescPV = idesc_bf16_f32(128, kHeadDim, 1);  // TMEM P, MN-major V
 constexpr uint32_t kIdescS64 = idesc_bf16_f32(128, 64, 0);       // split S: one 64-key half
+constexpr uint32_t kSdescHi = sdesc_hi(1024);                     // SW128, 8-row groups 1 KiB apart
 
 struct __align__(8) FaBarriers {
   uint64_t q_full[TWFA_MAX_TILES], q_empty[TWFA_MAX_TILES];
@@ -92,7 +108,8 @@ struct __align__(8) FaBarriers {
   uint64_t v_full[kMaxRing], v_empty[kMaxRing];
   // per S buffer (ring depth <= 2): a phase-parity barrier may only run one
   // phase ahead of its waiters, which the per-buffer split guarantees
-  uint64_t s_full[TWFA_MAX_TILES][2], p_full[TWFA_MAX_TILES][2], p_half[TWFA_MAX_TILES][2];
+  uint64_t s_full[TWFA_MAX_TILES][2];
+  uint64_t p_part[TWFA_MAX_TILES][2][kPParts];  // P_k keys [j*128/kPParts, ...) in tensor memory
   uint64_t o_ready[TWFA_MAX_TILES][2], o_done[TWFA_MAX_TILES][2];
   uint64_t st_full[TWFA_MAX_TILES][2], st_empty[TWFA_MAX_TILES][2];
   uint64_t l_full[TWFA_MAX_TILES], l_empty[TWFA_MAX_TILES];
@@ -169,28 +186,33 @@ __device__ __forceinline__ float row_max(const uint32_t (&s)[N]) {
   return fmax3(a[0], a[1], fmaxf(a[2], a[3]));
 }
 
-// P = exp2(S*sl - m) for the 128 resident scores: FFMA2 for the argument,
-// MUFU ex2 or the FMA-pipe polynomial (1 in kPolyEvery pairs) for the exp,
-// FADD2 for the row sum, F2FP to bf16 pairs, stored as the TS-MMA A operand
-// over the first 64 columns of the S tile. The first half of P (keys 0-63)
-// is released to PV_k on `half_bar` before the second half is computed.
-// Returns the row sum.
+// P = exp2(S*sl - m) for the resident scores: FFMA2 for the argument, MUFU
+// ex2 or the FMA-pipe polynomial (1 in kPolyEvery pairs) for the exp, FADD2
+// for the row sum, F2FP to bf16 pairs, stored as the TS-MMA A operand over
+// the first N/2 columns of the S tile. Part j of P is released to PV_k on
+// part_bar[j] (see kPParts). Returns the row sum.
 template <int N, bool kMask>
 __device__ __forceinline__ float exp_store_row(const uint32_t (&s)[N], uint32_t taddr, float sl, float m,
-                                               uint64_t* half_bar) {
+                                               uint64_t* part_bar) {
+  constexpr int kParts = N == 128 ? kPParts : 2;  // 64-key tiles keep halves
+  constexpr int kPartKeys = N / kParts;
+  constexpr int kKeys = kPartKeys < 32 ? kPartKeys : 32;  // keys per tcgen05.st chunk
+  constexpr int kRegs = kKeys / 2;
   const float2 sl2 = make_float2(sl, sl);
   const float2 nm2 = make_float2(-m, -m);
   float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-  for (int c = 0; c < N / 32; ++c) {
-    uint32_t pk[16];
+  for (int c = 0; c < N / kKeys; ++c) {
+    uint32_t pk[kRegs];
 #pragma unroll
-    for (int i = 0; i < 32; i += 2) {
-      const float2 x =
-          ffma2(make_float2(__uint_as_float(s[c * 32 + i]), __uint_as_float(s[c * 32 + i + 1])), sl2, nm2);
+    for (int i = 0; i < kKeys; i += 2) {
+      const int e = c * kKeys + i;
+      const float2 x = ffma2(make_float2(__uint_as_float(s[e]), __uint_as_float(s[e + 1])), sl2, nm2);
       float2 p;
-      // masked tiles (diagonal / sequence tail) hold -inf: MUFU maps it to 0
-      if (!kMask && ((i >> 1) % kPolyEvery) == kPolyEvery - 1) {
+      if (TWFA_WHATIF == 1 && e >= N / 2) {
+        p = x;
+      } else if (!kMask && ((e >> 1) % kPolyEvery) == kPolyEvery - 1) {
+        // masked tiles (diagonal / sequence tail) hold -inf: MUFU maps it to 0
         p = poly_exp2x2(x);
       } else {
         p.x = fast_exp2(x.x);
@@ -199,15 +221,14 @@ __device__ __forceinline__ float exp_store_row(const uint32_t (&s)[N], uint32_t 
       acc[(i >> 1) & 1] = fadd2(acc[(i >> 1) & 1], p);
       pk[i >> 1] = pack_bf16(p.x, p.y);
     }
-    if (c == N / 64) {
-      // the first half of P is in tensor memory: release the first half of
-      // PV. The store wait is placed after the next chunk's exponentials so
-      // the MUFU stream does not drain behind it.
+    if (c > 0 && (c * kKeys) % kPartKeys == 0) {
+      // the part that ended with chunk c - 1 was stored one chunk of MUFU
+      // work ago: release it
       tmem_st_wait();
       tc_fence_before();
-      warp_arrive(half_bar);
+      warp_arrive(&part_bar[c * kKeys / kPartKeys - 1]);
     }
-    tmem_st16(taddr + c * 16, pk);
+    tmem_st<kRegs>(taddr + c * kRegs, pk);
   }
   tmem_st_wait();
   return (acc[0].x + acc[0].y) + (acc[1].x + acc[1].y);
@@ -358,14 +379,15 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
       mbar_wait(&bar.k_full[s], (g / rg.kd) & 1);
     trace_mark<kTrace>(tr, 4);
     tc_fence_after();
-    const uint32_t qa = smem_u32(c.q_smem + k * kTileBytes);
-    const uint32_t ka = smem_u32(c.k_smem + s * G::tile) + (a ? 0u : 64u * 128u);  // K rows 64.. (8 SW128 atoms)
+    const uint32_t qd = sdesc_lo(smem_u32(c.q_smem + k * kTileBytes), 16);
+    // K rows 64.. (8 SW128 atoms)
+    const uint32_t kd = sdesc_lo(smem_u32(c.k_smem + s * G::tile) + (a ? 0u : 64u * 128u), 16);
     const uint32_t d_s = tmem + k * 128 + (a ? 0u : 64u);
     if (elect_one()) {
 #pragma unroll
       for (int kk = 0; kk < kHeadDim / 16; ++kk)
-        mma_ss(d_s, sdesc_sw128(qa + (kk >> 2) * kHalfBytes + (kk & 3) * 32, 16, 1024),
-               sdesc_sw128(ka + (kk >> 2) * G::half + (kk & 3) * 32, 16, 1024), kIdescS64, kk > 0);
+        mma_ss(d_s, sdesc_join(qd + ((kk >> 2) * kHalfBytes + (kk & 3) * 32) / 16, kSdescHi),
+               sdesc_join(kd + ((kk >> 2) * G::half + (kk & 3) * 32) / 16, kSdescHi), kIdescS64, kk > 0);
       mma_commit(a ? &bar.s_half[k] : &bar.s_full[k][0]);
       mma_commit(&bar.k_empty[s]);
       if (it == N - 1) mma_commit(&bar.q_empty[k]);
@@ -383,14 +405,14 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
       mbar_wait(&bar.k_full[s], (g / rg.kd) & 1);
     trace_mark<kTrace>(tr, 4);
     tc_fence_after();
-    const uint32_t qa = smem_u32(c.q_smem + k * kTileBytes);
-    const uint32_t ka = smem_u32(c.k_smem + s * G::tile);
+    const uint32_t qd = sdesc_lo(smem_u32(c.q_smem + k * kTileBytes), 16);
+    const uint32_t kd = sdesc_lo(smem_u32(c.k_smem + s * G::tile), 16);
     const uint32_t d_s = tmem + k * 128 + b * KV;
     if (elect_one()) {
 #pragma unroll
       for (int kk = 0; kk < kHeadDim / 16; ++kk)  // 16 head dims per step, 4 per SW128 half
-        mma_ss(d_s, sdesc_sw128(qa + (kk >> 2) * kHalfBytes + (kk & 3) * 32, 16, 1024),
-               sdesc_sw128(ka + (kk >> 2) * G::half + (kk & 3) * 32, 16, 1024), G::idesc_s, kk > 0);
+        mma_ss(d_s, sdesc_join(qd + ((kk >> 2) * kHalfBytes + (kk & 3) * 32) / 16, kSdescHi),
+               sdesc_join(kd + ((kk >> 2) * G::half + (kk & 3) * 32) / 16, kSdescHi), G::idesc_s, kk > 0);
       mma_commit(&bar.s_full[k][b]);
       mma_commit(&bar.k_empty[s]);
       if (it == N - 1) mma_commit(&bar.q_empty[k]);
@@ -400,28 +422,31 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
     const uint32_t s = g % rg.vd;
     // P_k arrives in two halves (keys 0-63, 64-127): the first four
     // K-steps of PV_k overlap the exponentials of the second half
-    mbar_wait_all(&bar.v_full[s], (g / rg.vd) & 1, &bar.p_half[k][b], pb, &bar.o_ready[k][b], pb);
+    constexpr int kParts = KV == 128 ? kPParts : 2;
+    constexpr int kSteps = KV / 16 / kParts;  // K-steps (16 keys) per part
+    mbar_wait_all(&bar.v_full[s], (g / rg.vd) & 1, &bar.p_part[k][b][0], pb, &bar.o_ready[k][b], pb);
     trace_mark<kTrace>(tr, 4);
     tc_fence_after();
-    const uint32_t va = smem_u32(c.v_smem + s * G::tile);
+    const uint32_t vd = sdesc_lo(smem_u32(c.v_smem + s * G::tile), G::half);
     const uint32_t d_o = tmem + 256 + k * 128, a_p = tmem + k * 128 + b * KV + (rg.split ? 64u : 0u);
     const uint32_t acc0 = it > 0 ? 1u : 0u;
-    if (elect_one()) {
 #pragma unroll
-      for (int kk = 0; kk < KV / 32; ++kk)  // V is MN-major: 16 keys = 16 rows of 128 B
-        mma_ts(d_o, a_p + kk * 8, sdesc_sw128(va + kk * 2048, G::half, 1024), kIdescPV, kk > 0 ? 1u : acc0);
-    }
-    __syncwarp();
-    mbar_wait(&bar.p_full[k][b], pb);
-    tc_fence_after();
-    if (elect_one()) {
+    for (int j = 0; j < kParts; ++j) {
+      if (j > 0) {
+        mbar_wait(&bar.p_part[k][b][j], pb);
+        tc_fence_after();
+      }
+      if (elect_one()) {
 #pragma unroll
-      for (int kk = KV / 32; kk < KV / 16; ++kk)
-        mma_ts(d_o, a_p + kk * 8, sdesc_sw128(va + kk * 2048, G::half, 1024), kIdescPV, 1u);
-      mma_commit(&bar.o_done[k][b]);
-      mma_commit(&bar.v_empty[s]);
+        for (int kk = j * kSteps; kk < (j + 1) * kSteps; ++kk)  // V is MN-major: 16 keys = 16 rows of 128 B
+          mma_ts(d_o, a_p + kk * 8, sdesc_join(vd + kk * 2048 / 16, kSdescHi), kIdescPV, kk > 0 ? 1u : acc0);
+        if (j == kParts - 1) {
+          mma_commit(&bar.o_done[k][b]);
+          mma_commit(&bar.v_empty[s]);
+        }
+      }
+      __syncwarp();
     }
-    __syncwarp();
   } else if (op.kind == TWFA_OP_CR) {
     const uint32_t sb = g & 1;
     mbar_wait(&bar.st_full[k][sb], (g >> 1) & 1);
@@ -469,7 +494,16 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
           mbar_wait(&bar.s_full[k][b], pb);
         trace_mark<kTrace>(tr, 4);
         tc_fence_after();
-        load_row<KV>(taddr, srow);
+        if (TWFA_WHATIF == 3) {
+#pragma unroll
+          for (int c2 = 0; c2 < KV / 64; ++c2)
+            tmem_ld32(taddr + c2 * 32, *reinterpret_cast<uint32_t(*)[32]>(&srow[c2 * 32]));
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = KV / 2; i < KV; ++i) srow[i] = srow[i - KV / 2];
+        } else {
+          load_row<KV>(taddr, srow);
+        }
         if (rg.split) {  // the row is in registers: SA_k(g+1) may overwrite columns 0-63
           tc_fence_before();
           warp_arrive(&bar.s_read[k]);
@@ -501,11 +535,11 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
       const float m_run = rd(st.m_run, k);
       const float m_safe = m_run == -INFINITY ? 0.f : m_run;
       const uint32_t paddr = taddr + (rg.split ? 64u : 0u);  // P_k columns
-      const float sum = mask ? exp_store_row<KV, true>(srow, paddr, c.scale_log2, m_safe, &bar.p_half[k][b])
-                             : exp_store_row<KV, false>(srow, paddr, c.scale_log2, m_safe, &bar.p_half[k][b]);
+      const float sum = mask ? exp_store_row<KV, true>(srow, paddr, c.scale_log2, m_safe, bar.p_part[k][b])
+                             : exp_store_row<KV, false>(srow, paddr, c.scale_log2, m_safe, bar.p_part[k][b]);
       wr(st.l_run, k, rd(st.l_run, k) * rd(st.alpha, k) + sum);
       tc_fence_before();
-      warp_arrive(&bar.p_full[k][b]);
+      warp_arrive(&bar.p_part[k][b][(KV == 128 ? kPParts : 2) - 1]);
       if (tok) warp_arrive(&bar.sm_tok[k == rg.ring0 ? rg.ring1 : rg.ring0]);
       if (it == N - 1) {
         mbar_wait(&bar.l_empty[k], (t.tcount & 1) ^ 1);
@@ -660,8 +694,7 @@ __device__ __forceinline__ FaCtx fa_setup(int tiles, int kd, int vd, int load_wa
       mbar_init(&bar.q_empty[k], split ? 2 : 1);  // the last S GEMM(s) of the tile read Q_k
       for (int b = 0; b < 2; ++b) {
         mbar_init(&bar.s_full[k][b], 1);
-        mbar_init(&bar.p_full[k][b], 4);  // warp arrivals of a warpgroup
-        mbar_init(&bar.p_half[k][b], 4);
+        for (int j = 0; j < kPParts; ++j) mbar_init(&bar.p_part[k][b][j], 4);  // warp arrivals of a warpgroup
         mbar_init(&bar.o_ready[k][b], 4);
         mbar_init(&bar.o_done[k][b], 1);
       }
