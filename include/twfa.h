@@ -87,6 +87,21 @@ int twfa_fa_fwd_traced(const twfa_plan* plan, const void* q, const void* k, cons
 int twfa_fa_fwd_host(const twfa_plan* plan, const uint16_t* q, const uint16_t* k, const uint16_t* v,
                      uint16_t* o, float* lse, int B, int H, int S, int D, int causal, float softmax_scale);
 
+/* FA backward (the paper's second workload), bf16, head
+ * dim 128, from an FA-backward plan (problem fa_backward_problem, solved by
+ * the reference scheduler):
+ *   dQ = scale dS K,  dK = scale dS^T Q,  dV = P^T dO,
+ *   P = exp(scale Q K^T - lse),  dS = P (dO V^T - rowsum(dO O)).
+ * q, k, v, o, dout, dq, dk, dv: [B, H, S, 128] contiguous bf16 device
+ * buffers; lse: [B, H, S] fp32 from the forward (natural log). workspace: a
+ * device buffer of at least twfa_fa_bwd_workspace_size(B, H, S, D) bytes
+ * (fp32 dQ accumulator and rowsum(dO O)); contents are overwritten. */
+int twfa_fa_bwd_workspace_size(int B, int H, int S, int D, size_t* bytes);
+int twfa_fa_bwd(const twfa_plan* plan, const void* q, const void* k, const void* v, const void* o,
+                const void* dout, const float* lse, void* dq, void* dk, void* dv, void* workspace,
+                size_t workspace_bytes, int B, int H, int S, int D, int causal, float softmax_scale,
+                void* stream);
+
 /* GEMM mainloop plan: C[M,N] = A[M,K] * B[N,K]^T, bf16 in/out, fp32 accumulate.
  * M % 128 == 0, N % 256 == 0, K % 64 == 0. */
 int twfa_gemm(const twfa_plan* plan, const void* a, const void* b, void* c, int M, int N, int K,

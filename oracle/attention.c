@@ -129,6 +129,57 @@ void oracle_attention_online(const float* q, const float* k, const float* v,
   }
 }
 
+void oracle_attention_bwd(const float* q, const float* k, const float* v,
+                          const float* o, const float* dout, const float* lse,
+                          float* dq, float* dk, float* dv, int B, int H, int S,
+                          int D, int causal, float scale, int threads) {
+  set_threads(threads);
+  const int BH = B * H;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int bh = 0; bh < BH; ++bh) {
+    const int64_t base = (int64_t)bh * S * D;
+    const float *qb = q + base, *kb = k + base, *vb = v + base, *ob = o + base, *gb = dout + base;
+    const float* lb = lse + (int64_t)bh * S;
+    double* dqa = (double*)calloc((size_t)S * D, sizeof(double));
+    double* dka = (double*)calloc((size_t)S * D, sizeof(double));
+    double* dva = (double*)calloc((size_t)S * D, sizeof(double));
+    for (int i = 0; i < S; ++i) {
+      const float* qi = qb + (int64_t)i * D;
+      const float* gi = gb + (int64_t)i * D;
+      double Di = 0.0;
+      for (int c = 0; c < D; ++c) Di += (double)gi[c] * (double)ob[(int64_t)i * D + c];
+      const int nkeys = causal ? (i + 1 < S ? i + 1 : S) : S;
+      for (int j = 0; j < nkeys; ++j) {
+        const float* kj = kb + (int64_t)j * D;
+        const float* vj = vb + (int64_t)j * D;
+        double s = 0.0, dp = 0.0;
+        for (int c = 0; c < D; ++c) {
+          s += (double)qi[c] * (double)kj[c];
+          dp += (double)gi[c] * (double)vj[c];
+        }
+        const double p = exp(s * (double)scale - (double)lb[i]);
+        const double ds = p * (dp - Di);
+        double* dvj = dva + (int64_t)j * D;
+        double* dkj = dka + (int64_t)j * D;
+        double* dqi = dqa + (int64_t)i * D;
+        for (int c = 0; c < D; ++c) {
+          dvj[c] += p * (double)gi[c];
+          dkj[c] += ds * (double)qi[c];
+          dqi[c] += ds * (double)kj[c];
+        }
+      }
+    }
+    for (int64_t e = 0; e < (int64_t)S * D; ++e) {
+      dq[base + e] = (float)(dqa[e] * (double)scale);
+      dk[base + e] = (float)(dka[e] * (double)scale);
+      dv[base + e] = (float)dva[e];
+    }
+    free(dqa);
+    free(dka);
+    free(dva);
+  }
+}
+
 void oracle_round_bf16(float* x, int64_t n) {
   for (int64_t i = 0; i < n; ++i) {
     uint32_t u;

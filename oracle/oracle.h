@@ -41,6 +41,20 @@ void oracle_attention_online(const float* q, const float* k, const float* v,
 
 /* C[M,N] = A[M,K] * B[N,K]^T (both operands K-contiguous), fp32 with double
  * accumulation. */
+/* Attention backward (the paper's second workload: the
+ * single-pass algorithm of FA3), restated from the forward's definition
+ * O = softmax(scale Q K^T) V with the recorded lse:
+ *   P_ij  = exp(scale q_i.k_j - lse_i)        D_i = sum_c dO_ic O_ic
+ *   dV_j  = sum_i P_ij dO_i                   dP_ij = dO_i . v_j
+ *   dS_ij = P_ij (dP_ij - D_i)
+ *   dQ_i  = scale sum_j dS_ij k_j             dK_j = scale sum_i dS_ij q_i
+ * Layouts as oracle_attention (Sq = Sk = S); double accumulation. Parity is
+ * unpinned like the forward (no reference numerics). */
+void oracle_attention_bwd(const float* q, const float* k, const float* v,
+                          const float* o, const float* dout, const float* lse,
+                          float* dq, float* dk, float* dv, int B, int H, int S,
+                          int D, int causal, float scale, int threads);
+
 void oracle_gemm_tn(const float* a, const float* b, float* c, int M, int N,
                     int K, int threads);
 

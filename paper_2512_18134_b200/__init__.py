@@ -61,8 +61,11 @@ def lib():
         L.twfa_fa_fwd_host.argtypes = [vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, i32, f32]
         L.twfa_gemm.argtypes = [vp, vp, vp, vp, i32, i32, i32, vp]
         L.twfa_grid_size.argtypes = [ctypes.POINTER(i32)]
+        L.twfa_fa_bwd_workspace_size.argtypes = [i32, i32, i32, i32, ctypes.POINTER(sz)]
+        L.twfa_fa_bwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, i32, i32, i32, i32, i32, f32, vp]
         for name in ("twfa_plan_create", "twfa_plan_describe", "twfa_plan_raw", "twfa_fa_fwd",
-                     "twfa_fa_fwd_traced", "twfa_fa_fwd_host", "twfa_gemm", "twfa_grid_size"):
+                     "twfa_fa_fwd_traced", "twfa_fa_fwd_host", "twfa_gemm", "twfa_grid_size",
+                     "twfa_fa_bwd_workspace_size", "twfa_fa_bwd"):
             getattr(L, name).restype = i32
         _lib = L
     return _lib
@@ -170,6 +173,37 @@ def fa_fwd_host(plan, q, k, v, causal=False, softmax_scale=None, return_lse=Fals
     _check(lib().twfa_fa_fwd_host(plan.handle, p(q), p(k), p(v), p(o), p(lse) if lse is not None else None,
                                   B, H, S, D, int(bool(causal)), scale))
     return (o, lse) if return_lse else o
+
+
+def fa_bwd(plan, q, k, v, o, dout, lse, causal=False, softmax_scale=None, workspace=None):
+    """FA backward on the current CUDA stream (plan from an FA-backward
+    schedule, e.g. load_schedule("fa_bwd")). q, k, v, o, dout: [B, H, S, 128]
+    bf16 CUDA tensors; lse: [B, H, S] fp32 from fa_fwd(..., return_lse=True).
+    Returns (dq, dk, dv) bf16."""
+    import torch
+    ts = (q, k, v, o, dout)
+    if any(t.dtype != torch.bfloat16 for t in ts):
+        raise ValueError("q, k, v, o, dout must be bf16")
+    if any(not t.is_cuda for t in ts) or not lse.is_cuda:
+        raise ValueError("inputs must be CUDA tensors")
+    if any(t.shape != q.shape for t in ts) or q.dim() != 4:
+        raise ValueError("q, k, v, o, dout must share shape [B, H, S, D]")
+    q, k, v, o, dout = (t.contiguous() for t in ts)
+    B, H, S, D = q.shape
+    if lse.dtype != torch.float32 or tuple(lse.shape) != (B, H, S):
+        raise ValueError("lse must be fp32 [B, H, S]")
+    lse = lse.contiguous()
+    scale = float(softmax_scale) if softmax_scale is not None else 1.0 / math.sqrt(D)
+    need = ctypes.c_size_t()
+    _check(lib().twfa_fa_bwd_workspace_size(B, H, S, D, ctypes.byref(need)))
+    if workspace is None or workspace.numel() * workspace.element_size() < need.value:
+        workspace = torch.empty(need.value, device=q.device, dtype=torch.uint8)
+    dq, dk, dv = (torch.empty_like(q) for _ in range(3))
+    ptr = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    _check(lib().twfa_fa_bwd(plan.handle, ptr(q), ptr(k), ptr(v), ptr(o), ptr(dout), ptr(lse), ptr(dq), ptr(dk),
+                             ptr(dv), ptr(workspace), need.value, B, H, S, D, int(bool(causal)), scale,
+                             _stream_ptr(q)))
+    return dq, dk, dv
 
 
 def gemm(plan, a, b, out=None):

@@ -10,6 +10,7 @@
 #include <string>
 
 #include "../../include/twfa.h"
+#include "fa_bwd.h"
 #include "fa_fwd.h"
 #include "lowering.h"
 
@@ -73,12 +74,12 @@ EncodeFn encode_fn() {
   return fn;
 }
 
-// bf16 tensor of `rank` dims (innermost first), 128-byte swizzled boxes
+// bf16 (or fp32) tensor of `rank` dims (innermost first), 128-byte swizzled boxes
 CUtensorMap make_map(const void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides_bytes,
-                     const cuuint32_t* box) {
+                     const cuuint32_t* box, CUtensorMapDataType dtype = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16) {
   CUtensorMap m;
   cuuint32_t elem[3] = {1, 1, 1};
-  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, static_cast<cuuint32_t>(rank),
+  CUresult r = encode_fn()(&m, dtype, static_cast<cuuint32_t>(rank),
                            const_cast<void*>(base), dims, strides_bytes, box, elem,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -142,6 +143,53 @@ int fa_fwd_impl(const twfa_plan* plan, const void* q, const void* k, const void*
   const int grid = static_cast<int>(std::min<long long>(work, sm_count()));
   check(twfa::fa_fwd_launch(tq, tk, tv, p, a, grid, static_cast<cudaStream_t>(stream), allow_specialized()),
         "fa_fwd launch");
+  return TWFA_OK;
+}
+
+int fa_bwd_impl(const twfa_plan* plan, const void* q, const void* k, const void* v, const void* o,
+                const void* dout, const float* lse, void* dq, void* dk, void* dv, void* ws, size_t ws_bytes, int B,
+                int H, int S, int D, int causal, float scale, void* stream) {
+  if (!plan) throw twfa::UsageError("plan is NULL");
+  const TwfaDevicePlan& p = plan->sched.plan;
+  if (p.family != TWFA_FAMILY_FA_BWD) throw twfa::UsageError("plan is not an FA-backward plan");
+  if (D != 128) throw twfa::UsageError("head dim must be 128");
+  if (B < 1 || H < 1 || S < 1) throw twfa::UsageError("B, H, S must be positive");
+  if (!(scale > 0.f) || !std::isfinite(scale)) throw twfa::UsageError("softmax_scale must be positive");
+  for (auto [ptr, name] : {std::pair<const void*, const char*>{q, "q"}, {k, "k"}, {v, "v"}, {o, "o"},
+                           {dout, "dout"}, {lse, "lse"}, {dq, "dq"}, {dk, "dk"}, {dv, "dv"}, {ws, "workspace"}})
+    require_aligned(ptr, name);
+  if (ws_bytes < twfa::fa_bwd_workspace_bytes(B, H, S)) throw twfa::UsageError("workspace too small");
+  const cuuint64_t bh = static_cast<cuuint64_t>(B) * H;
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(S), bh};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 2, static_cast<cuuint64_t>(S) * D * 2};
+  const cuuint64_t strides32[2] = {static_cast<cuuint64_t>(D) * 4, static_cast<cuuint64_t>(S) * D * 4};
+  const cuuint32_t box[3] = {64, 128, 1};
+  const cuuint32_t box32[3] = {32, 128, 1};
+  const size_t rows = static_cast<size_t>(bh) * S;
+  float* dq_acc = static_cast<float*>(ws);
+  float* dvec = dq_acc + rows * 128;
+  twfa::FaBwdArgs a{};
+  a.tm_q = make_map(q, 3, dims, strides, box);
+  a.tm_k = make_map(k, 3, dims, strides, box);
+  a.tm_v = make_map(v, 3, dims, strides, box);
+  a.tm_do = make_map(dout, 3, dims, strides, box);
+  a.tm_dq = make_map(dq_acc, 3, dims, strides32, box32, CU_TENSOR_MAP_DATA_TYPE_FLOAT32);
+  a.lse = lse;
+  a.dvec = dvec;
+  a.dq_acc = dq_acc;
+  a.dk = static_cast<__nv_bfloat16*>(dk);
+  a.dv = static_cast<__nv_bfloat16*>(dv);
+  a.B = B;
+  a.H = H;
+  a.S = S;
+  a.causal = causal ? 1 : 0;
+  a.scale = scale;
+  a.scale_log2 = scale * 1.4426950408889634f;
+  const long long work = static_cast<long long>(bh) * ((S + 127) / 128);
+  const int grid = static_cast<int>(std::min<long long>(work, sm_count()));
+  check(twfa::fa_bwd_launch(p, a, static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(dout),
+                            static_cast<__nv_bfloat16*>(dq), grid, static_cast<cudaStream_t>(stream)),
+        "fa_bwd launch");
   return TWFA_OK;
 }
 
@@ -252,6 +300,24 @@ int twfa_fa_fwd_host(const twfa_plan* plan, const uint16_t* q, const uint16_t* k
     check(cudaMemcpy(o, dout, tb, cudaMemcpyDeviceToHost), "D2H o");
     if (lse) check(cudaMemcpy(lse, dl, lb, cudaMemcpyDeviceToHost), "D2H lse");
     return TWFA_OK;
+  });
+}
+
+int twfa_fa_bwd_workspace_size(int B, int H, int S, int D, size_t* bytes) {
+  return guarded([&] {
+    if (!bytes) throw twfa::UsageError("NULL argument");
+    if (B < 1 || H < 1 || S < 1 || D != 128) throw twfa::UsageError("unsupported shape");
+    *bytes = twfa::fa_bwd_workspace_bytes(B, H, S);
+    return TWFA_OK;
+  });
+}
+
+int twfa_fa_bwd(const twfa_plan* plan, const void* q, const void* k, const void* v, const void* o, const void* dout,
+                const float* lse, void* dq, void* dk, void* dv, void* workspace, size_t workspace_bytes, int B, int H,
+                int S, int D, int causal, float softmax_scale, void* stream) {
+  return guarded([&] {
+    return fa_bwd_impl(plan, q, k, v, o, dout, lse, dq, dk, dv, workspace, workspace_bytes, B, H, S, D, causal,
+                       softmax_scale, stream);
   });
 }
 

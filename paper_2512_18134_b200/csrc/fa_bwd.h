@@ -1,0 +1,38 @@
+// Launch interface of the sm_100a FA-backward kernel (internal to libtwfa).
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "plan.h"
+
+namespace twfa {
+
+struct FaBwdArgs {
+  // bf16 [B*H][S][128] maps with 64 x 128 SW128 boxes (Q, K, V, dO) and the
+  // fp32 dQ accumulator map with 32 x 128 SW128 boxes (TMA reduce-add)
+  alignas(64) CUtensorMap tm_q;
+  alignas(64) CUtensorMap tm_k;
+  alignas(64) CUtensorMap tm_v;
+  alignas(64) CUtensorMap tm_do;
+  alignas(64) CUtensorMap tm_dq;
+  const float* lse;   // [B, H, S] natural-log sum-exp of the forward
+  float* dvec;        // [B, H, S] workspace: rowsum(dO * O)
+  float* dq_acc;      // [B, H, S, 128] workspace: fp32 dQ accumulator
+  __nv_bfloat16* dk;  // [B, H, S, 128]
+  __nv_bfloat16* dv;
+  int B, H, S;
+  int causal;
+  float scale;        // softmax scale
+  float scale_log2;   // scale * log2(e)
+};
+
+size_t fa_bwd_smem_bytes(const TwfaDevicePlan& plan);
+size_t fa_bwd_workspace_bytes(int B, int H, int S);
+// pre-pass (D), zeroing of the accumulator, the main kernel, post-pass (dQ)
+cudaError_t fa_bwd_launch(const TwfaDevicePlan& plan, const FaBwdArgs& args, const __nv_bfloat16* o,
+                          const __nv_bfloat16* dout, __nv_bfloat16* dq, int grid, cudaStream_t stream);
+
+}  // namespace twfa

@@ -1,0 +1,598 @@
+// FA-backward on sm_100a, realized from a Twill joint schedule.
+//
+// The paper's second workload: the single-pass backward
+// of FA3 -- five GEMMs, one exponential, and an atomic reduction of dQ into
+// global memory. The loop graph is tools/make_problems.py:fa_backward_problem;
+// its solution (schedules/fa_bwd.solution.json, z3) gives the warp roles and
+// the issue order that the lowering (lowering.cpp:derive_bwd) turns into the
+// per-warp trip programs this kernel walks.
+//
+// One CTA owns a 128-key K/V tile of one (b, h) -- K and V stay in shared
+// memory, dK and dV accumulate in tensor memory -- and iterates over the
+// 128-row Q tiles i (causal: the tiles on and below the diagonal):
+//   LDQ, LDO  Q_i, dO_i -> smem rings (TMA)
+//   ST        S^T  = K Q_i^T            TMEM cols 256.. (keys on lanes)
+//   EXB       P^T  = exp2(S^T * scale*log2e - LSE_i*log2e) -> bf16 over S^T
+//   DP        dP^T = V dO_i^T           TMEM cols 384..
+//   DS        dS^T = P^T (dP^T - D_i)   -> bf16 over dP^T, and into smem
+//             (MN-major, the A operand of DQ); P^T stays in registers
+//   DV        dV  += P^T dO_i           TS, TMEM cols 128..
+//   DK        dK  += dS^T Q_i           TS, TMEM cols 0..
+//   DQ        dQ_i = dS K               SS (A MN-major) -> TMEM cols 256..
+//   RD        dQ_i (fp32) -> smem -> TMA reduce-add into the global dQ
+//             accumulator
+// after the last tile: dK * scale, dV -> bf16 -> global (RD warpgroup).
+// A pre-pass computes D_i = rowsum(dO_i * O_i); a post-pass scales dQ.
+//
+// Every cross-warp edge of the loop graph is an mbarrier; the aliasing edges
+// (DV -> DQ, DK -> DP) are realized by tcgen05 in-order execution on the
+// single issuing thread, which the lowering checks.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "fa_bwd.h"
+#include "sm100.cuh"
+
+namespace twfa {
+
+namespace {
+
+constexpr int kT = 128;                 // keys per K/V tile = rows per Q tile
+constexpr uint32_t kTile = 32768;       // 128 x 128 bf16: two 64-column SW128 halves
+constexpr uint32_t kHalf = 16384;
+constexpr uint32_t kColDK = 0, kColDV = 128, kColS = 256, kColP = 384;  // TMEM columns
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr uint32_t kIdescKK = idesc_bf16_f32(128, 128, 0);  // A, B K-major
+constexpr uint32_t kIdescKM = idesc_bf16_f32(128, 128, 1);  // A K-major (or TMEM), B MN-major
+constexpr uint32_t kIdescMM = idesc_bf16_f32(128, 128, 1) | (1u << 15);  // A and B MN-major
+constexpr uint32_t kSdHi = sdesc_hi(1024);
+constexpr uint32_t kRdBar = 2;  // named barrier of the RD warpgroup
+
+struct __align__(8) BwdBarriers {
+  uint64_t kv_full, kv_empty;
+  uint64_t q_full[2], q_empty[2], o_full[2], o_empty[2];
+  uint64_t s_full, dp_full, dq_full;  // tcgen05.commit
+  uint64_t p_full, ds_full;           // EXB / DS warpgroup (4 warp arrivals)
+  uint64_t s_free;                    // RD warpgroup read dQ_i out of TMEM (4)
+  uint64_t ds_free;                   // RD is done with the dS buffer as staging (1)
+  uint64_t acc_full;                  // dK, dV final for the work item (commit)
+  uint64_t acc_free;                  // RD warpgroup read dK, dV (4)
+  uint32_t tmem_base;
+};
+__shared__ BwdBarriers g_bb;
+
+struct BwdCtx {
+  uint8_t* k;
+  uint8_t* v;
+  uint8_t* q;   // ring of Q tiles
+  uint8_t* o;   // ring of dO tiles
+  uint8_t* ds;  // dS (A operand of DQ), then the dQ staging of RD
+  uint32_t warp, lane, quad, lane_off;
+  int S, BH, nq, num_work;
+  uint64_t pol;
+};
+
+struct BwdItem {
+  int bh, kv0, q_first, N;  // N = Q tiles of this work item
+  uint32_t gbase;           // global iteration index of its iteration 0
+  uint32_t icount;          // work items done by this CTA
+};
+
+__device__ __forceinline__ BwdItem bwd_item(const BwdCtx& c, const FaBwdArgs& a, int work, uint32_t gbase,
+                                            uint32_t icount) {
+  BwdItem t;
+  int j;
+  if (a.causal) {  // K/V tile j sees Q tiles j..nq-1: longest first
+    j = work / c.BH;
+    t.bh = work % c.BH;
+  } else {
+    t.bh = work / c.nq;
+    j = work % c.nq;
+  }
+  t.kv0 = j * kT;
+  t.q_first = a.causal ? j : 0;
+  t.N = c.nq - t.q_first;
+  t.gbase = gbase;
+  t.icount = icount;
+  return t;
+}
+
+struct BwdState {
+  int q_next, o_next;  // next Q / dO iteration to load (TMA warp)
+};
+
+__device__ __forceinline__ uint32_t sd_lo(const void* p, uint32_t lbo) { return sdesc_lo(smem_u32(p), lbo); }
+
+// P^T row of this thread (key kv0 + r) for Q tile q0: 128 fp32 registers
+// carried from EXB into the fused DS.
+template <bool kTrace>
+__device__ __forceinline__ void exb_ds(const BwdCtx& c, const FaBwdArgs& a, const BwdItem& t, int it,
+                                       uint32_t g) {
+  BwdBarriers& bar = g_bb;
+  const int q0 = (t.q_first + it) * kT;
+  const uint32_t r = c.quad * 32 + c.lane;
+  const int key = t.kv0 + static_cast<int>(r);
+  const int64_t row0 = static_cast<int64_t>(t.bh) * c.S + q0;
+  const bool full = q0 + kT <= c.S;
+  uint32_t p[kT];
+  mbar_wait(&bar.s_full, g & 1);
+  tc_fence_after();
+#pragma unroll
+  for (int cc = 0; cc < 4; ++cc)
+    tmem_ld32(c.lane_off + kColS + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(&p[cc * 32]));
+  tmem_ld_wait();
+  // P^T[key][q] = exp2(S^T * scale*log2e - LSE_q * log2e); LSE is broadcast
+  // (every thread reads the same 128 values: L1 broadcast loads)
+  const float sl = a.scale_log2;
+  const bool diag = a.causal && it == 0;  // the diagonal tile (q0 == kv0)
+#pragma unroll
+  for (int j4 = 0; j4 < kT / 4; ++j4) {
+    float4 l;
+    if (full) {
+      l = __ldg(reinterpret_cast<const float4*>(a.lse + row0) + j4);
+    } else {
+      const float* lp = a.lse + row0 + 4 * j4;
+      const int rem = c.S - q0 - 4 * j4;
+      l.x = rem > 0 ? lp[0] : INFINITY;
+      l.y = rem > 1 ? lp[1] : INFINITY;
+      l.z = rem > 2 ? lp[2] : INFINITY;
+      l.w = rem > 3 ? lp[3] : INFINITY;
+    }
+    const float lv[4] = {l.x, l.y, l.z, l.w};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = 4 * j4 + u;
+      float e = fast_exp2(fmaf(__uint_as_float(p[j]), sl, -lv[u] * kLog2e));
+      if (diag && key > q0 + j) e = 0.f;
+      p[j] = __float_as_uint(e);
+    }
+  }
+#pragma unroll
+  for (int cc = 0; cc < 4; ++cc) {
+    uint32_t pk[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(__uint_as_float(p[cc * 32 + 2 * i]), __uint_as_float(p[cc * 32 + 2 * i + 1]));
+    tmem_st16(c.lane_off + kColS + cc * 16, pk);
+  }
+  tmem_st_wait();
+  tc_fence_before();
+  warp_arrive(&bar.p_full);
+
+  // DS: dS^T = P^T (dP^T - D_q), chunk by chunk over the dP^T columns; the
+  // bf16 chunk goes to TMEM (over dP^T columns already read) for DK and to
+  // the smem A operand of DQ (MN-major: row = key, 64 queries per SW128 half)
+  if (g > 0) mbar_wait(&bar.ds_free, (g - 1) & 1);
+  mbar_wait(&bar.dp_full, g & 1);
+  tc_fence_after();
+  const uint32_t ds_base = smem_u32(c.ds) + r * 128;
+#pragma unroll
+  for (int cc = 0; cc < 4; ++cc) {
+    uint32_t dp[32];
+    tmem_ld32(c.lane_off + kColP + cc * 32, dp);
+    tmem_ld_wait();
+    uint32_t pk[16];
+#pragma unroll
+    for (int j4 = 0; j4 < 8; ++j4) {
+      float4 d;
+      const int j = cc * 32 + 4 * j4;
+      if (full) {
+        d = __ldg(reinterpret_cast<const float4*>(a.dvec + row0 + j));
+      } else {
+        const float* dpp = a.dvec + row0 + j;
+        const int rem = c.S - q0 - j;
+        d.x = rem > 0 ? dpp[0] : 0.f;
+        d.y = rem > 1 ? dpp[1] : 0.f;
+        d.z = rem > 2 ? dpp[2] : 0.f;
+        d.w = rem > 3 ? dpp[3] : 0.f;
+      }
+      const float s0 = __uint_as_float(p[j + 0]) * (__uint_as_float(dp[4 * j4 + 0]) - d.x);
+      const float s1 = __uint_as_float(p[j + 1]) * (__uint_as_float(dp[4 * j4 + 1]) - d.y);
+      const float s2 = __uint_as_float(p[j + 2]) * (__uint_as_float(dp[4 * j4 + 2]) - d.z);
+      const float s3 = __uint_as_float(p[j + 3]) * (__uint_as_float(dp[4 * j4 + 3]) - d.w);
+      pk[2 * j4] = pack_bf16(s0, s1);
+      pk[2 * j4 + 1] = pack_bf16(s2, s3);
+    }
+    tmem_st16(c.lane_off + kColP + cc * 16, pk);
+    // queries 32cc .. 32cc+31: SW128 half cc/2, 16-byte chunks 4(cc%2) .. +3
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const uint32_t ch = (cc & 1) * 4 + m;
+      st_shared_v4(ds_base + (cc >> 1) * kHalf + ((ch ^ (r & 7)) << 4), pk[4 * m], pk[4 * m + 1], pk[4 * m + 2],
+                   pk[4 * m + 3]);
+    }
+  }
+  tmem_st_wait();
+  tc_fence_before();
+  fence_proxy_async_shared();
+  warp_arrive(&bar.ds_full);
+}
+
+// RD: dQ_i from TMEM (row = query) -> smem staging (fp32, SW128 boxes of
+// 128 rows x 32 columns) -> cp.reduce.async.bulk add into the fp32 dQ
+// accumulator (the atomic reduction of the paper's backward loop).
+__device__ __forceinline__ void rd_op(const BwdCtx& c, const FaBwdArgs& a, const BwdItem& t, int it, uint32_t g) {
+  BwdBarriers& bar = g_bb;
+  const int q0 = (t.q_first + it) * kT;
+  const uint32_t r = c.quad * 32 + c.lane;
+  const bool leader = (c.warp & 3u) == 0 && c.lane == 0;
+  uint32_t v[kT];
+  mbar_wait(&bar.dq_full, g & 1);
+  tc_fence_after();
+#pragma unroll
+  for (int cc = 0; cc < 4; ++cc)
+    tmem_ld32(c.lane_off + kColS + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(&v[cc * 32]));
+  tmem_ld_wait();
+  tc_fence_before();
+  warp_arrive(&bar.s_free);  // S^T(i+1) may overwrite the columns
+  // DQ_i has completed (dq_full): the dS buffer is free for staging
+#pragma unroll
+  for (int pair = 0; pair < 2; ++pair) {
+    if (pair == 1) {
+      if (leader) bulk_wait_read();
+      named_bar_sync(kRdBar, 128);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int box = 2 * pair + h;
+      const uint32_t base = smem_u32(c.ds) + h * kHalf + r * 128;
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch)
+        st_shared_v4(base + ((ch ^ (r & 7)) << 4), v[box * 32 + 4 * ch], v[box * 32 + 4 * ch + 1],
+                     v[box * 32 + 4 * ch + 2], v[box * 32 + 4 * ch + 3]);
+    }
+    fence_proxy_async_shared();
+    named_bar_sync(kRdBar, 128);
+    if (leader) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) tma_reduce_add_3d(&a.tm_dq, c.ds + h * kHalf, 32 * (2 * pair + h), q0, t.bh);
+      bulk_commit();
+    }
+  }
+  if (leader) {
+    bulk_wait_read();
+    mbar_arrive(&bar.ds_free);
+  }
+}
+
+// dK (scaled) and dV of the work item: TMEM (row = key) -> bf16 -> global
+__device__ __forceinline__ void kv_epilogue(const BwdCtx& c, const FaBwdArgs& a, const BwdItem& t) {
+  BwdBarriers& bar = g_bb;
+  mbar_wait(&bar.acc_full, t.icount & 1);
+  tc_fence_after();
+  const int key = t.kv0 + static_cast<int>(c.quad * 32 + c.lane);
+  const int64_t off = (static_cast<int64_t>(t.bh) * c.S + key) * 128;
+#pragma unroll 1
+  for (int which = 0; which < 2; ++which) {
+    const uint32_t col = which == 0 ? kColDK : kColDV;
+    const float mul = which == 0 ? a.scale : 1.f;
+    __nv_bfloat16* dst = (which == 0 ? a.dk : a.dv) + off;
+#pragma unroll 1
+    for (int cc = 0; cc < 4; ++cc) {
+      uint32_t x[32];
+      tmem_ld32(c.lane_off + col + cc * 32, x);
+      tmem_ld_wait();
+      if (key < c.S) {
+        uint4* d4 = reinterpret_cast<uint4*>(dst + cc * 32);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          uint4 w;
+          w.x = pack_bf16(__uint_as_float(x[8 * i + 0]) * mul, __uint_as_float(x[8 * i + 1]) * mul);
+          w.y = pack_bf16(__uint_as_float(x[8 * i + 2]) * mul, __uint_as_float(x[8 * i + 3]) * mul);
+          w.z = pack_bf16(__uint_as_float(x[8 * i + 4]) * mul, __uint_as_float(x[8 * i + 5]) * mul);
+          w.w = pack_bf16(__uint_as_float(x[8 * i + 6]) * mul, __uint_as_float(x[8 * i + 7]) * mul);
+          d4[i] = w;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  warp_arrive(&bar.acc_free);
+}
+
+// Register classes (each compiled under its setmaxnreg budget): the TMA / MMA
+// warps, the RD warpgroup (RD + the dK / dV epilogue), the EXB / DS
+// warpgroup (which also runs RD when the schedule puts it there).
+enum BwdRole { kLight = 0, kReduce = 1, kHeavyRole = 2 };
+
+// One op of the trip program on this warp, trip r.
+template <int kRole>
+__device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const BwdCtx& c, const BwdItem& t,
+                                         BwdState& st, const TwfaDevicePlan& plan, const FaBwdArgs& a) {
+  BwdBarriers& bar = g_bb;
+  if (op.kind == TWFA_OP_LDQ || op.kind == TWFA_OP_LDO) {
+    if constexpr (kRole == kLight) {
+      const bool is_q = op.kind == TWFA_OP_LDQ;
+      const int target = min(t.N - 1, r - static_cast<int>(op.stage) + (is_q ? plan.k_prefetch : plan.v_prefetch));
+      int& next = is_q ? st.q_next : st.o_next;
+      const int depth = is_q ? plan.k_depth : plan.v_depth;
+      while (next <= target) {
+        const int lit = next++;
+        const uint32_t g = t.gbase + static_cast<uint32_t>(lit);
+        const uint32_t s = g % depth, ph = (g / depth) & 1;
+        uint64_t* full = is_q ? &bar.q_full[s] : &bar.o_full[s];
+        mbar_wait(is_q ? &bar.q_empty[s] : &bar.o_empty[s], ph ^ 1);
+        if (elect_one()) {
+          uint8_t* dst = (is_q ? c.q : c.o) + s * kTile;
+          const CUtensorMap* map = is_q ? &a.tm_q : &a.tm_do;
+          const int row = (t.q_first + lit) * kT;
+          mbar_arrive_expect_tx(full, kTile);
+          tma_load_3d(dst, map, full, 0, row, t.bh, c.pol);
+          tma_load_3d(dst + kHalf, map, full, 64, row, t.bh, c.pol);
+        }
+        __syncwarp();
+      }
+    }
+    return;
+  }
+  const int it = r - static_cast<int>(op.stage);
+  if (it < 0 || it >= t.N) return;
+  const uint32_t g = t.gbase + static_cast<uint32_t>(it);
+  if (op.kind == TWFA_OP_EXB || op.kind == TWFA_OP_DS) {
+    if constexpr (kRole == kHeavyRole) {
+      if (op.kind == TWFA_OP_EXB) exb_ds<false>(c, a, t, it, g);  // DS is fused (lowering guarantees)
+    }
+    return;
+  }
+  if (op.kind == TWFA_OP_RD) {
+    if constexpr (kRole != kLight) rd_op(c, a, t, it, g);
+    return;
+  }
+  if constexpr (kRole != kLight) return;
+  // tensor-core ops: warp-uniform descriptors, one elected lane issues
+  const uint32_t qs = g % plan.k_depth, os = g % plan.v_depth;
+  const bool release = op.flags & TWFA_OPF_RELEASE;
+  if (op.kind == TWFA_OP_ST) {
+    if (it == 0) mbar_wait(&bar.kv_full, t.icount & 1);
+    if (g > 0)
+      mbar_wait_all(&bar.q_full[qs], (g / plan.k_depth) & 1, &bar.s_free, (g - 1) & 1);
+    else
+      mbar_wait(&bar.q_full[qs], (g / plan.k_depth) & 1);
+    tc_fence_after();
+    const uint32_t ad = sd_lo(c.k, 16), bd = sd_lo(c.q + qs * kTile, 16);
+    if (elect_one()) {
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const uint32_t off = ((kk >> 2) * kHalf + (kk & 3) * 32) / 16;
+        mma_ss(kColS, sdesc_join(ad + off, kSdHi), sdesc_join(bd + off, kSdHi), kIdescKK, kk > 0);
+      }
+      mma_commit(&bar.s_full);
+      if (release) mma_commit(&bar.q_empty[qs]);
+    }
+    __syncwarp();
+  } else if (op.kind == TWFA_OP_DP) {
+    if (it == 0) mbar_wait(&bar.kv_full, t.icount & 1);
+    mbar_wait(&bar.o_full[os], (g / plan.v_depth) & 1);
+    tc_fence_after();
+    const uint32_t ad = sd_lo(c.v, 16), bd = sd_lo(c.o + os * kTile, 16);
+    if (elect_one()) {
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const uint32_t off = ((kk >> 2) * kHalf + (kk & 3) * 32) / 16;
+        mma_ss(kColP, sdesc_join(ad + off, kSdHi), sdesc_join(bd + off, kSdHi), kIdescKK, kk > 0);
+      }
+      mma_commit(&bar.dp_full);
+      if (release) mma_commit(&bar.o_empty[os]);
+    }
+    __syncwarp();
+  } else if (op.kind == TWFA_OP_DV || op.kind == TWFA_OP_DK) {
+    const bool dv = op.kind == TWFA_OP_DV;
+    // the accumulator is overwritten at iteration 0: the previous work
+    // item's dK / dV must have been read out
+    if (it == 0 && t.icount > 0) mbar_wait(&bar.acc_free, (t.icount - 1) & 1);
+    if (dv)
+      mbar_wait_all(&bar.p_full, g & 1, &bar.o_full[os], (g / plan.v_depth) & 1);
+    else
+      mbar_wait_all(&bar.ds_full, g & 1, &bar.q_full[qs], (g / plan.k_depth) & 1);
+    tc_fence_after();
+    // B = dO_i / Q_i as [K = query][N = d], MN-major
+    const uint32_t bd = dv ? sd_lo(c.o + os * kTile, kHalf) : sd_lo(c.q + qs * kTile, kHalf);
+    const uint32_t a_t = dv ? kColS : kColP, d_t = dv ? kColDV : kColDK;
+    if (elect_one()) {
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)  // 16 queries per K-step: 8 packed bf16 columns of P^T / dS^T
+        mma_ts(d_t, a_t + kk * 8, sdesc_join(bd + kk * 2048 / 16, kSdHi), kIdescKM, (it > 0 || kk > 0) ? 1u : 0u);
+      if (release) mma_commit(dv ? &bar.o_empty[os] : &bar.q_empty[qs]);
+    }
+    __syncwarp();
+  } else if (op.kind == TWFA_OP_DQ) {
+    mbar_wait(&bar.ds_full, g & 1);
+    tc_fence_after();
+    // A = dS as [M = query][K = key], MN-major (row = key in smem);
+    // B = K as [K = key][N = d], MN-major
+    const uint32_t ad = sd_lo(c.ds, kHalf), bd = sd_lo(c.k, kHalf);
+    if (elect_one()) {
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+        mma_ss(kColS, sdesc_join(ad + kk * 2048 / 16, kSdHi), sdesc_join(bd + kk * 2048 / 16, kSdHi), kIdescMM,
+               kk > 0);
+      mma_commit(&bar.dq_full);
+    }
+    __syncwarp();
+  }
+}
+
+template <int kRole>
+__device__ __forceinline__ void bwd_run(const BwdCtx& c, const TwfaDevicePlan& plan, const FaBwdArgs& a) {
+  BwdBarriers& bar = g_bb;
+  const int plen = plan.prog_len[c.warp];
+  const bool is_load = c.warp == static_cast<uint32_t>(plan.load_warp);
+  const bool is_mma = c.warp == static_cast<uint32_t>(plan.mma_warp);
+  const bool is_rd = static_cast<int>(c.warp & ~3u) == plan.cr_warp[0];
+  BwdState st{0, 0};
+  uint32_t gbase = 0, icount = 0;
+  for (int work = blockIdx.x; work < c.num_work; work += gridDim.x, ++icount) {
+    const BwdItem t = bwd_item(c, a, work, gbase, icount);
+    if constexpr (kRole == kLight) {
+      if (is_load) {  // K and V of the work item
+        mbar_wait(&bar.kv_empty, (icount & 1) ^ 1);
+        if (elect_one()) {
+          mbar_arrive_expect_tx(&bar.kv_full, 2 * kTile);
+          tma_load_3d(c.k, &a.tm_k, &bar.kv_full, 0, t.kv0, t.bh, c.pol);
+          tma_load_3d(c.k + kHalf, &a.tm_k, &bar.kv_full, 64, t.kv0, t.bh, c.pol);
+          tma_load_3d(c.v, &a.tm_v, &bar.kv_full, 0, t.kv0, t.bh, c.pol);
+          tma_load_3d(c.v + kHalf, &a.tm_v, &bar.kv_full, 64, t.kv0, t.bh, c.pol);
+        }
+        __syncwarp();
+      }
+    }
+    st.q_next = st.o_next = 0;
+    const int trips = t.N + plan.max_stage;
+    for (int rr = -1; rr < trips; ++rr)
+      for (int j = 0; j < plen; ++j) bwd_exec<kRole>(plan.ops[plan.prog[c.warp][j]], rr, c, t, st, plan, a);
+    if constexpr (kRole == kLight) {
+      if (is_mma) {  // every MMA of the item issued: dK, dV final; K, V free
+        if (elect_one()) {
+          mma_commit(&bar.acc_full);
+          mma_commit(&bar.kv_empty);
+        }
+        __syncwarp();
+      }
+    } else {
+      if (is_rd) kv_epilogue(c, a, t);
+    }
+    gbase += static_cast<uint32_t>(t.N);
+  }
+}
+
+__global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
+    fa_bwd_kernel(const __grid_constant__ TwfaDevicePlan plan, const __grid_constant__ FaBwdArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  BwdCtx c;
+  c.k = smem;
+  c.v = c.k + kTile;
+  c.q = c.v + kTile;
+  c.o = c.q + plan.k_depth * kTile;
+  c.ds = c.o + plan.v_depth * kTile;
+  c.warp = warp_id();
+  c.lane = lane_id();
+  c.quad = c.warp & 3u;
+  c.lane_off = (c.quad * 32u) << 16;
+  c.S = a.S;
+  c.BH = a.B * a.H;
+  c.nq = (a.S + kT - 1) / kT;
+  c.num_work = c.BH * c.nq;
+  BwdBarriers& bar = g_bb;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar.kv_full, 1);
+    mbar_init(&bar.kv_empty, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&bar.q_full[s], 1);
+      mbar_init(&bar.q_empty[s], 1);
+      mbar_init(&bar.o_full[s], 1);
+      mbar_init(&bar.o_empty[s], 1);
+    }
+    mbar_init(&bar.s_full, 1);
+    mbar_init(&bar.dp_full, 1);
+    mbar_init(&bar.dq_full, 1);
+    mbar_init(&bar.p_full, 4);
+    mbar_init(&bar.ds_full, 4);
+    mbar_init(&bar.s_free, 4);
+    mbar_init(&bar.ds_free, 1);
+    mbar_init(&bar.acc_full, 1);
+    mbar_init(&bar.acc_free, 4);
+    fence_mbar_init();
+  }
+  if (c.warp == static_cast<uint32_t>(plan.load_warp) && c.lane == 0) {
+    tma_prefetch_desc(&a.tm_q);
+    tma_prefetch_desc(&a.tm_k);
+    tma_prefetch_desc(&a.tm_v);
+    tma_prefetch_desc(&a.tm_do);
+  }
+  if (c.warp == 0) tmem_alloc<512>(&bar.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (bar.tmem_base != 0) __trap();  // one CTA per SM owns all 512 columns from 0
+  c.pol = policy_evict_last();
+  const int wg = static_cast<int>(c.warp >> 2);
+  const bool heavy = (plan.heavy_wg_mask >> wg) & 1;
+  const bool rd = wg * 4 == plan.cr_warp[0];
+  // registers: the EXB/DS warpgroup carries the 128-float P^T row, the RD
+  // warpgroup a 128-float dQ row; the TMA / MMA warps need few
+  if (heavy) {
+    setmaxnreg_inc<200>();
+    bwd_run<kHeavyRole>(c, plan, a);
+  } else if (rd) {
+    setmaxnreg_inc<168>();
+    bwd_run<kReduce>(c, plan, a);
+  } else {
+    setmaxnreg_dec<64>();
+    bwd_run<kLight>(c, plan, a);
+  }
+  if (c.lane == 0) bulk_wait_all();
+  tc_fence_before();
+  __syncthreads();
+  if (c.warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<512>(0);
+  }
+}
+
+// D = rowsum(dO * O) in fp32: 16 threads per row, 8 bf16 each
+__global__ void fa_bwd_pre(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
+                           float* __restrict__ dvec, int64_t rows) {
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 16) + threadIdx.x / 16;
+  const int part = threadIdx.x % 16;
+  float acc = 0.f;
+  if (row < rows) {
+    const uint4 x = reinterpret_cast<const uint4*>(o + row * 128)[part];
+    const uint4 y = reinterpret_cast<const uint4*>(dout + row * 128)[part];
+    const __nv_bfloat162* xa = reinterpret_cast<const __nv_bfloat162*>(&x);
+    const __nv_bfloat162* ya = reinterpret_cast<const __nv_bfloat162*>(&y);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 a = __bfloat1622float2(xa[i]), b = __bfloat1622float2(ya[i]);
+      acc = fmaf(a.x, b.x, fmaf(a.y, b.y, acc));
+    }
+  }
+#pragma unroll
+  for (int m = 8; m >= 1; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+  if (row < rows && part == 0) dvec[row] = acc;
+}
+
+// dQ = scale * accumulator -> bf16, 8 per thread
+__global__ void fa_bwd_post(const float* __restrict__ acc, __nv_bfloat16* __restrict__ dq, float scale, int64_t n8) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n8) return;
+  const float4 a = reinterpret_cast<const float4*>(acc)[2 * i];
+  const float4 b = reinterpret_cast<const float4*>(acc)[2 * i + 1];
+  uint4 w;
+  w.x = pack_bf16(a.x * scale, a.y * scale);
+  w.y = pack_bf16(a.z * scale, a.w * scale);
+  w.z = pack_bf16(b.x * scale, b.y * scale);
+  w.w = pack_bf16(b.z * scale, b.w * scale);
+  reinterpret_cast<uint4*>(dq)[i] = w;
+}
+
+}  // namespace
+
+size_t fa_bwd_smem_bytes(const TwfaDevicePlan& plan) {
+  return static_cast<size_t>(3 + plan.k_depth + plan.v_depth) * kTile + 1024;
+}
+
+size_t fa_bwd_workspace_bytes(int B, int H, int S) {
+  const size_t rows = static_cast<size_t>(B) * H * S;
+  return rows * 128 * sizeof(float) + rows * sizeof(float);
+}
+
+cudaError_t fa_bwd_launch(const TwfaDevicePlan& plan, const FaBwdArgs& args, const __nv_bfloat16* o,
+                          const __nv_bfloat16* dout, __nv_bfloat16* dq, int grid, cudaStream_t stream) {
+  const int64_t rows = static_cast<int64_t>(args.B) * args.H * args.S;
+  fa_bwd_pre<<<static_cast<unsigned>((rows + 15) / 16), 256, 0, stream>>>(o, dout, args.dvec, rows);
+  cudaError_t e = cudaMemsetAsync(args.dq_acc, 0, static_cast<size_t>(rows) * 128 * sizeof(float), stream);
+  if (e != cudaSuccess) return e;
+  const size_t smem = fa_bwd_smem_bytes(plan);
+  e = cudaFuncSetAttribute(fa_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  fa_bwd_kernel<<<grid, TWFA_MAX_WARPS * 32, smem, stream>>>(plan, args);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const int64_t n8 = rows * 16;
+  fa_bwd_post<<<static_cast<unsigned>((n8 + 255) / 256), 256, 0, stream>>>(args.dq_acc, dq, args.scale, n8);
+  return cudaGetLastError();
+}
+
+}  // namespace twfa

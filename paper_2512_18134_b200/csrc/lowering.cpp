@@ -176,7 +176,10 @@ void parse_solution(const std::string& text, LoweredSchedule& s) {
 bool classify(const std::string& id, uint8_t& kind, uint8_t& tile) {
   struct Pfx { const char* p; uint8_t k; };
   static const Pfx fixed[] = {{"LDK", TWFA_OP_LDK}, {"LDV", TWFA_OP_LDV}, {"LDA", TWFA_OP_LDA},
-                              {"LDB", TWFA_OP_LDB}, {"MMA", TWFA_OP_MMA}};
+                              {"LDB", TWFA_OP_LDB}, {"MMA", TWFA_OP_MMA}, {"LDQ", TWFA_OP_LDQ},
+                              {"LDO", TWFA_OP_LDO}, {"ST", TWFA_OP_ST},   {"DP", TWFA_OP_DP},
+                              {"EXB", TWFA_OP_EXB}, {"DS", TWFA_OP_DS},   {"DV", TWFA_OP_DV},
+                              {"DK", TWFA_OP_DK},   {"DQ", TWFA_OP_DQ},   {"RD", TWFA_OP_RD}};
   for (const Pfx& f : fixed)
     if (id == f.p) { kind = f.k; tile = 0; return true; }
   static const Pfx tiled[] = {{"MX", TWFA_OP_MX}, {"EX", TWFA_OP_EX}, {"CR", TWFA_OP_CR}, {"PV", TWFA_OP_PV},
@@ -190,6 +193,73 @@ bool classify(const std::string& id, uint8_t& kind, uint8_t& tile) {
     }
   }
   return false;
+}
+
+// FA backward (family FA_BWD): the roles of the realized kernel are the
+// solver's warp assignment. Tensor-core ops issue from one thread (their
+// in-order execution realizes the DV -> DQ and DK -> DP aliasing edges);
+// EXB and DS share a warpgroup and the DS after EXB carries P in registers;
+// RD runs on a warpgroup; LDQ / LDO stream from one TMA warp.
+template <class NodeId, class DepthOf, class PrefetchOf>
+void derive_bwd(LoweredSchedule& s, NodeId&& node_id, DepthOf&& depth_of, PrefetchOf&& prefetch_of) {
+  TwfaDevicePlan& p = s.plan;
+  p.family = TWFA_FAMILY_FA_BWD;
+  p.num_tiles = 1;
+  static const char* ids[] = {"LDQ", "LDO", "ST", "DP", "EXB", "DS", "DV", "DK", "DQ", "RD"};
+  for (const char* id : ids)
+    if (node_id(id) < 0) throw DomainError(std::string("FA-backward loop is missing ") + id);
+  if (s.nodes.size() != 10) throw DomainError("FA-backward loop has unexpected extra nodes");
+  const TwfaPlanOp &ldq = p.ops[node_id("LDQ")], &ldo = p.ops[node_id("LDO")];
+  if (ldq.warp_start != ldo.warp_start || ldq.warp_count != 1)
+    throw DomainError("LDQ and LDO must be issued by one TMA warp");
+  p.load_warp = ldq.warp_start;
+  p.k_depth = depth_of("LDQ");
+  p.v_depth = depth_of("LDO");
+  p.k_prefetch = prefetch_of(node_id("LDQ"), p.k_depth);
+  p.v_prefetch = prefetch_of(node_id("LDO"), p.v_depth);
+  if (p.k_depth > 2 || p.v_depth > 2) throw DomainError("Q / dO rings deeper than 2 exceed shared memory");
+  const int mma = p.ops[node_id("ST")].warp_start;
+  for (const char* id : {"ST", "DP", "DV", "DK", "DQ"}) {
+    const TwfaPlanOp& o = p.ops[node_id(id)];
+    if (o.warp_count != 1 || o.warp_start != mma)
+      throw DomainError("tensor-core ops of the backward loop must issue from one warp");
+  }
+  p.mma_warp = mma;
+  const TwfaPlanOp &exb = p.ops[node_id("EXB")], &ds = p.ops[node_id("DS")], &rd = p.ops[node_id("RD")];
+  for (const TwfaPlanOp* o : {&exb, &ds, &rd})
+    if (o->warp_count != 4 || o->warp_start % 4 != 0)
+      throw DomainError("EXB, DS and RD are row-wise over 128 TMEM lanes: they need a warpgroup");
+  if (exb.warp_start != ds.warp_start) throw DomainError("EXB and DS must share a warpgroup (P stays in registers)");
+  for (int w : {p.load_warp, p.mma_warp})
+    for (const TwfaPlanOp* o : {&exb, &rd})
+      if (w >= o->warp_start && w < o->warp_start + 4)
+        throw DomainError("the TMA / MMA warp cannot be inside the EXB or RD warpgroup");
+  // P^T (128 fp32 registers) lives from EXB to DS: DS must be the next op of
+  // every warp of the group, in the same iteration
+  const int exi = node_id("EXB"), dsi = node_id("DS");
+  for (int w = exb.warp_start; w < exb.warp_start + 4; ++w) {
+    const std::vector<int>& prog = s.warp_prog[static_cast<size_t>(w)];
+    auto it = std::find(prog.begin(), prog.end(), exi);
+    if (it == prog.end() || it + 1 == prog.end() || *(it + 1) != dsi ||
+        s.stage[static_cast<size_t>(exi)] != s.stage[static_cast<size_t>(dsi)])
+      throw DomainError("DS must directly follow EXB on its warpgroup (P is carried in registers)");
+  }
+  p.ops[exi].flags |= TWFA_OPF_FUSE_NEXT;
+  p.ops[dsi].flags |= TWFA_OPF_FUSED;
+  p.sm_warp[0] = exb.warp_start;
+  p.cr_warp[0] = rd.warp_start;  // RD warpgroup (also writes dK, dV)
+  p.heavy_wg_mask = 1 << (exb.warp_start / 4);
+  // the later tensor-core reader of Q_i (ST, DK) and of dO_i (DP, DV)
+  // releases the ring slot with its commit
+  auto later = [&](const char* a, const char* b) {
+    const int x = node_id(a), y = node_id(b);
+    return std::make_pair(s.m[static_cast<size_t>(x)], p.ops[x].order) >
+                   std::make_pair(s.m[static_cast<size_t>(y)], p.ops[y].order)
+               ? x
+               : y;
+  };
+  p.ops[later("ST", "DK")].flags |= TWFA_OPF_RELEASE;
+  p.ops[later("DP", "DV")].flags |= TWFA_OPF_RELEASE;
 }
 
 void derive(LoweredSchedule& s) {
@@ -307,7 +377,12 @@ void derive(LoweredSchedule& s) {
   const bool is_fa = (kinds.count(TWFA_OP_S) || (kinds.count(TWFA_OP_SA) && kinds.count(TWFA_OP_SB))) &&
                      kinds.count(TWFA_OP_PV);
   const bool is_gemm = kinds.count(TWFA_OP_MMA) && kinds.count(TWFA_OP_LDA) && kinds.count(TWFA_OP_LDB);
-  if (is_fa == is_gemm) throw DomainError("graph is neither the FA-forward nor the GEMM loop");
+  const bool is_bwd = kinds.count(TWFA_OP_ST) && kinds.count(TWFA_OP_DQ);
+  if (is_fa + is_gemm + is_bwd != 1) throw DomainError("graph is neither the FA-forward, FA-backward nor GEMM loop");
+  if (is_bwd) {
+    derive_bwd(s, node_id, depth_of, prefetch_of);
+    return;
+  }
   if (is_gemm) {
     p.family = TWFA_FAMILY_GEMM;
     const int lda = node_id("LDA"), ldb = node_id("LDB"), mma = node_id("MMA");
@@ -452,7 +527,7 @@ LoweredSchedule lower(const std::string& problem_json, const std::string& soluti
 std::string describe(const LoweredSchedule& s) {
   json j;
   const TwfaDevicePlan& p = s.plan;
-  j["family"] = p.family == TWFA_FAMILY_FA_FWD ? "fa_fwd" : "gemm";
+  j["family"] = p.family == TWFA_FAMILY_FA_FWD ? "fa_fwd" : p.family == TWFA_FAMILY_FA_BWD ? "fa_bwd" : "gemm";
   j["I"] = s.ii;
   j["L"] = s.length;
   j["copies"] = s.copies;
@@ -504,6 +579,17 @@ std::string describe(const LoweredSchedule& s) {
     json ring = json::array();
     for (int i = 0; i < p.ex_ring_len; ++i) ring.push_back("EX" + std::to_string(p.ex_ring[i]));
     j["mufu_order"] = ring;
+  } else if (p.family == TWFA_FAMILY_FA_BWD) {
+    rings["Q"] = p.k_depth;
+    rings["dO"] = p.v_depth;
+    j["prefetch"] = {{"LDQ", p.k_prefetch}, {"LDO", p.v_prefetch}};
+    j["mma_warp"] = p.mma_warp;
+    j["warpgroups"] = {{"exp_ds", p.sm_warp[0]}, {"dq_reduce", p.cr_warp[0]}};
+    json rel = json::array();
+    for (int v = 0; v < p.num_nodes; ++v)
+      if (p.ops[v].flags & TWFA_OPF_RELEASE) rel.push_back(s.nodes[static_cast<size_t>(v)].id);
+    j["ring_release"] = rel;
+    j["tmem_columns"] = {{"dK", 0}, {"dV", 128}, {"S^T/P^T/dQ", 256}, {"dP^T/dS^T", 384}};
   } else {
     rings["AB"] = p.k_depth;
     j["mma_warp"] = p.mma_warp;

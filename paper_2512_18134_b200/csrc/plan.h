@@ -33,7 +33,19 @@ enum TwfaOpKind : uint8_t {
   // the columns P_k (bf16) is aliased over; see fa_forward_problem(split_s)
   TWFA_OP_SA = 10,
   TWFA_OP_SB = 11,
-  TWFA_OP_COUNT = 12
+  // FA backward (one 128-key K/V tile per CTA, iterations over 128-row Q
+  // tiles; see fa_backward_problem in tools/make_problems.py)
+  TWFA_OP_LDQ = 12,  // TMA load of Q_i (streamed)
+  TWFA_OP_LDO = 13,  // TMA load of dO_i (streamed)
+  TWFA_OP_ST = 14,   // S^T = K Q_i^T           (tcgen05.mma SS)
+  TWFA_OP_DP = 15,   // dP^T = V dO_i^T         (tcgen05.mma SS)
+  TWFA_OP_EXB = 16,  // P^T = exp2(S^T - LSE_i) -> TMEM (bf16)
+  TWFA_OP_DS = 17,   // dS^T = P^T (dP^T - D_i) -> TMEM (bf16) and smem
+  TWFA_OP_DV = 18,   // dV += P^T dO_i          (tcgen05.mma TS)
+  TWFA_OP_DK = 19,   // dK += dS^T Q_i          (tcgen05.mma TS)
+  TWFA_OP_DQ = 20,   // dQ_i = dS K             (tcgen05.mma SS, A MN-major)
+  TWFA_OP_RD = 21,   // dQ_i -> global fp32 accumulator (TMA reduce-add)
+  TWFA_OP_COUNT = 22
 };
 
 struct alignas(16) TwfaPlanOp {  // 16 bytes: one vector load on the device
@@ -61,9 +73,12 @@ struct alignas(16) TwfaPlanOp {  // 16 bytes: one vector load on the device
 #define TWFA_OPF_INORDER 2
 // EX_k whose work is done by the fused MX_k right before it (FUSE_NEXT).
 #define TWFA_OPF_FUSED 4
+// FA backward: the last tensor-core reader of its streamed ring slot in the
+// iteration (releases Q_i / dO_i with its commit).
+#define TWFA_OPF_RELEASE 8
 
 // Kind of the workload the plan drives.
-enum TwfaPlanFamily : int32_t { TWFA_FAMILY_FA_FWD = 1, TWFA_FAMILY_GEMM = 2 };
+enum TwfaPlanFamily : int32_t { TWFA_FAMILY_FA_FWD = 1, TWFA_FAMILY_GEMM = 2, TWFA_FAMILY_FA_BWD = 3 };
 
 struct TwfaDevicePlan {
   int32_t family;      // TwfaPlanFamily

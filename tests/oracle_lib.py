@@ -29,6 +29,7 @@ def load():
         vp, i32, f32 = ctypes.c_void_p, ctypes.c_int, ctypes.c_float
         L.oracle_attention.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, i32, i32, i32, f32, i32]
         L.oracle_attention_online.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, i32, i32, i32, f32, i32, i32]
+        L.oracle_attention_bwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, i32, f32, i32]
         L.oracle_gemm_tn.argtypes = [vp, vp, vp, i32, i32, i32, i32]
         L.oracle_round_bf16.argtypes = [vp, ctypes.c_int64]
         _lib = L
@@ -55,6 +56,20 @@ def attention(q, k, v, causal=False, scale=None, online=False, tile=128, threads
     else:
         L.oracle_attention(_p(q), _p(k), _p(v), _p(o), _p(lse), B, H, Sq, Sk, D, int(causal), scale, threads)
     return o, lse
+
+
+def attention_bwd(q, k, v, o, do, lse, causal=False, scale=None, threads=0):
+    """Backward of attention: float32 [B, H, S, D] inputs, lse [B, H, S]
+    (natural log, as returned by `attention`). Returns (dq, dk, dv)."""
+    L = load()
+    q, k, v, o, do = (np.ascontiguousarray(x, dtype=np.float32) for x in (q, k, v, o, do))
+    lse = np.ascontiguousarray(lse, dtype=np.float32)
+    B, H, S, D = q.shape
+    scale = float(scale if scale is not None else 1.0 / np.sqrt(D))
+    dq, dk, dv = (np.empty_like(q) for _ in range(3))
+    L.oracle_attention_bwd(_p(q), _p(k), _p(v), _p(o), _p(do), _p(lse), _p(dq), _p(dk), _p(dv), B, H, S, D,
+                           int(causal), scale, threads)
+    return dq, dk, dv
 
 
 def gemm_tn(a, b, threads=0):

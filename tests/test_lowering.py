@@ -49,7 +49,7 @@ def steady_programs_from_reference(ws, prob, sol):
     return prog, per_warp, stage, warp
 
 
-@pytest.mark.parametrize("name", ["fa_fwd", "gemm_mainloop"])
+@pytest.mark.parametrize("name", ["fa_fwd", "gemm_mainloop", "fa_bwd"])
 def test_plan_equals_reference_program(twfa, ws, name):
     prob, sol = twfa.load_schedule(name)
     d = twfa.Plan(prob, sol).describe()
@@ -159,3 +159,34 @@ def test_s_ring_depth_from_pv_s_edge(twfa):
             e["delta"] = 3
     with pytest.raises(ValueError, match="delta 1 or 2"):
         twfa.Plan(json.dumps(p), sol)
+
+
+def test_fa_bwd_plan_roles_follow_the_solver(twfa):
+    # the backward kernel's roles are the solver's warp assignment
+    prob, sol = twfa.load_schedule("fa_bwd")
+    s = json.loads(sol)
+    d = twfa.Plan(prob, sol).describe()
+    assert d["family"] == "fa_bwd"
+    assert d["warpgroups"] == {"exp_ds": s["A"]["EXB"], "dq_reduce": s["A"]["RD"]}
+    assert d["mma_warp"] == s["A"]["ST"] and d["load_warp"] == s["A"]["LDQ"]
+    mma = d["warp_programs"][str(d["mma_warp"])]
+    tc = [v for v in mma if v in ("ST", "DP", "DV", "DK", "DQ")]
+    # issue order = slot order of the solution (all stage 0 here)
+    assert tc == sorted(tc, key=lambda v: s["M"][v])
+    # the later reader of Q_i (ST, DK) / dO_i (DP, DV) releases the ring slot
+    later = lambda a, b: a if s["M"][a] > s["M"][b] else b  # noqa: E731
+    assert sorted(d["ring_release"]) == sorted([later("ST", "DK"), later("DP", "DV")])
+
+
+@pytest.mark.parametrize("mutate,msg", [
+    (lambda s: s["A"].update(DS=4), "share a warpgroup"),
+    (lambda s: s["A"].update(DQ=14), "issue from one warp"),
+    (lambda s: s["A"].update(RD=12), "cannot be inside"),
+    (lambda s: s["M"].update(DS=13, DK=13), "violates dependence|directly follow"),
+])
+def test_fa_bwd_unrealizable_solutions_are_rejected(twfa, mutate, msg):
+    prob, sol = twfa.load_schedule("fa_bwd")
+    s = json.loads(sol)
+    mutate(s)
+    with pytest.raises(ValueError, match=msg):
+        twfa.Plan(prob, json.dumps(s))

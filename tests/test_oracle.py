@@ -78,3 +78,20 @@ def test_bf16_rounding_is_round_to_nearest_even():
     assert np.array_equal(r, t)
     bits = oracle_lib.bf16_bits(r)
     assert np.array_equal(oracle_lib.from_bf16_bits(bits), r)
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_backward_matches_float64_autograd(causal):
+    # the backward restatement against torch autograd in float64 (CPU): an
+    # independent derivation of the same gradients
+    import torch
+    rng = np.random.default_rng(3)
+    B, H, S, D = 1, 2, 80, 32
+    q, k, v, do = (rng.standard_normal((B, H, S, D)).astype(np.float32) for _ in range(4))
+    o, lse = oracle_lib.attention(q, k, v, causal=causal)
+    dq, dk, dv = oracle_lib.attention_bwd(q, k, v, o, do, lse, causal=causal)
+    tq, tk, tv = (torch.tensor(x, dtype=torch.float64, requires_grad=True) for x in (q, k, v))
+    out = torch.nn.functional.scaled_dot_product_attention(tq, tk, tv, is_causal=causal)
+    out.backward(torch.tensor(do, dtype=torch.float64))
+    for mine, t in ((dq, tq), (dk, tk), (dv, tv)):
+        assert np.abs(mine - t.grad.numpy()).max() < 1e-5

@@ -169,6 +169,81 @@ def fa_forward_problem(tc_variable_latency=False, calibrated=False, s_ring=1, sp
     return {"machine": machine, "graph": {"nodes": nodes, "edges": edges}}
 
 
+def fa_backward_problem():
+    """FA-backward loop body on sm_100a (the paper's second workload,
+    PAPER.md:1073-1148; the single-pass algorithm of FA3): one CTA owns a
+    128-key K/V tile (K, V resident in shared memory, dK and dV accumulated
+    in tensor memory) and iterates over the 128-row Q tiles of its head:
+
+      LDQ, LDO  TMA loads of Q_i and dO_i (streamed rings)
+      ST        S^T = K Q_i^T            tcgen05.mma SS -> TMEM (keys on lanes)
+      EXB       P^T = exp2(S^T - LSE_i)  MUFU; P^T (bf16) -> TMEM over S^T
+      DP        dP^T = V dO_i^T          tcgen05.mma SS -> TMEM
+      DS        dS^T = P^T (dP^T - D_i)  FMA; bf16 -> TMEM over dP^T and -> smem
+      DV        dV += P^T dO_i           tcgen05.mma TS
+      DK        dK += dS^T Q_i           tcgen05.mma TS
+      DQ        dQ_i = dS K              tcgen05.mma SS -> TMEM over S^T
+      RD        dQ_i -> global           tcgen05.ld + TMA reduce-add (fp32)
+
+    Tensor memory (512 columns): dK, dV, S^T (P^T, dQ_i), dP^T (dS^T), 128
+    each. The aliasing is carried by edges: DV -> DQ (DQ overwrites the P^T
+    DV reads; in order on the issuing thread), RD -> ST (delta 1: S^T(i+1)
+    needs dQ_i read out), DK -> DP (delta 1: dP^T(i+1) overwrites dS^T(i)),
+    RD -> DS (delta 1: dS(i+1) reuses the smem buffer RD stages dQ_i in).
+    EXB -> DS carries P in registers (spill cost: a re-read of P from tensor
+    memory in bf16 changes the numerics, so a large cost keeps them on one
+    warpgroup). The tensor-core ops are variable latency (the production
+    forward model): they go to the reserved warp with the loads.
+    Costs (datasheet, units of 256 clk): GEMMs 2, EXB 4 (16384 exp2 at
+    16/clk/SM), DS 2 (TMEM read of dP^T + FMA + two stores), RD 2 (TMEM read
+    of dQ_i + staging + bulk reduce issue)."""
+    T = 256
+    machine = {
+        "units": [{"name": "TC", "capacity": 1}, {"name": "TMA", "capacity": 1},
+                  {"name": "MUFU", "capacity": 1}, {"name": "ALU", "capacity": 1},
+                  {"name": "FMA", "capacity": 1}],
+        "memories": [{"name": "tmem", "capacity": 512}],
+        "num_warps": 16,
+        "reg_limit": 224,
+        "vl_warp": 15,
+    }
+    g = 2  # one 128x128x128 tcgen05 GEMM
+    nodes = [node("LDQ", "TMA", 2, variable_latency=True), node("LDO", "TMA", 2, variable_latency=True)]
+    for v in ("ST", "DP"):
+        nodes.append(node(v, "TC", g, footprint={"tmem": 128}, variable_latency=True))
+    nodes += [
+        node("EXB", "MUFU", 4, regs=128, spill_cost=16, warps_required=4),
+        node("DS", "FMA", 2, regs=64, warps_required=4),
+        node("DV", "TC", g, variable_latency=True),
+        node("DK", "TC", g, variable_latency=True),
+        node("DQ", "TC", g, variable_latency=True),
+        node("RD", "ALU", 2, regs=128, warps_required=4),
+    ]
+    edges = [
+        edge("LDQ", "ST", 0, blocking=True), edge("LDQ", "DK", 0, blocking=True),
+        edge("LDO", "DP", 0, blocking=True), edge("LDO", "DV", 0, blocking=True),
+        edge("ST", "EXB", g, blocking=True),
+        edge("EXB", "DV", 4, blocking=True), edge("EXB", "DS", 4),
+        edge("DP", "DS", g, blocking=True),
+        edge("DS", "DK", 2, blocking=True), edge("DS", "DQ", 2, blocking=True),
+        edge("DQ", "RD", g, blocking=True),
+        edge("DV", "DQ", 0),
+        edge("RD", "ST", 2, delta=1, blocking=True),
+        edge("DK", "DP", 0, delta=1),
+        edge("RD", "DS", 2, delta=1, blocking=True),
+        edge("DV", "DV", g, delta=1), edge("DK", "DK", g, delta=1),
+        edge("EXB", "EXB", 4, delta=1), edge("DS", "DS", 2, delta=1), edge("RD", "RD", 2, delta=1),
+    ]
+    for n in nodes:
+        n["cycles"] *= T
+        n["rrt"] = {u: [1] * n["cycles"] for u in n["rrt"]}
+        if n.get("spill_cost"):
+            n["spill_cost"] *= T
+    for e in edges:
+        e["d"] *= T
+    return {"machine": machine, "graph": {"nodes": nodes, "edges": edges}}
+
+
 def gemm_problem():
     """GEMM mainloop (BASELINE config 2): per k-block, TMA loads of the A and B
     tiles feed one 128x256x64 tcgen05 MMA chain into a TMEM accumulator.
@@ -262,6 +337,8 @@ def main():
         "fa_fwd_split": (fa_forward_problem(tc_variable_latency=True, calibrated=True, split_s=True), 2, 9),
         # double-buffered S (64-key K/V tiles): S_k(i+1) independent of PV_k(i)
         "fa_fwd_ring2": (fa_forward_problem(tc_variable_latency=True, s_ring=2), 4, None),
+        # FA backward (single pass, K/V-stationary), datasheet costs
+        "fa_bwd": (fa_backward_problem(), 2, 11),  # {512, 1024, 4096} clk exactly (F = 0)
     }
     for name, (raw, depth, res) in probs.items():
         if args.only and name != args.only:
