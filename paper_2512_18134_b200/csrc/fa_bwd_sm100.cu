@@ -32,6 +32,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdio>
+
 #include "fa_bwd.h"
 #include "sm100.cuh"
 
@@ -49,6 +51,15 @@ constexpr uint32_t kIdescKM = idesc_bf16_f32(128, 128, 1);  // A K-major (or TME
 constexpr uint32_t kIdescMM = idesc_bf16_f32(128, 128, 1) | (1u << 15);  // A and B MN-major
 constexpr uint32_t kSdHi = sdesc_hi(1024);
 constexpr uint32_t kRdBar = 2;  // named barrier of the RD warpgroup
+// timing-only experiments (results WRONG when set): 1 = RD skips the
+// reduce-add, 2 = RD skips staging and reduce
+#ifndef TWFA_BWD_WHATIF
+#define TWFA_BWD_WHATIF 0
+#endif
+// debug variant: CTA 0 prints per-op enter / exit clocks of iterations 20-21
+#ifndef TWFA_BWD_PROF
+#define TWFA_BWD_PROF 0
+#endif
 
 struct __align__(8) BwdBarriers {
   uint64_t kv_full, kv_empty;
@@ -62,6 +73,14 @@ struct __align__(8) BwdBarriers {
   uint32_t tmem_base;
 };
 __shared__ BwdBarriers g_bb;
+// LSE * log2(e) and D of the current Q tile, broadcast to the EXB / DS
+// warpgroup (thread t stages query q0 + t)
+__shared__ float g_lse2[kT], g_dvec[kT];
+constexpr uint32_t kExBar = 3;  // named barrier of the EXB / DS warpgroup
+#if TWFA_BWD_PROF
+__shared__ int g_prof_n;
+__shared__ long long g_prof[64][3];
+#endif
 
 struct BwdCtx {
   uint8_t* k;
@@ -115,36 +134,34 @@ __device__ __forceinline__ void exb_ds(const BwdCtx& c, const FaBwdArgs& a, cons
   const uint32_t r = c.quad * 32 + c.lane;
   const int key = t.kv0 + static_cast<int>(r);
   const int64_t row0 = static_cast<int64_t>(t.bh) * c.S + q0;
-  const bool full = q0 + kT <= c.S;
+  // this tile's LSE / D: one coalesced load per thread, issued before the
+  // S^T wait; staged in shared memory once every thread of the group is
+  // done with the previous tile's values
+  const int qt = q0 + static_cast<int>(r);
+  const float my_lse2 = qt < c.S ? a.lse[row0 + r] * kLog2e : INFINITY;  // rows past S: P = 0
+  const float my_d = qt < c.S ? a.dvec[row0 + r] : 0.f;
   uint32_t p[kT];
   mbar_wait(&bar.s_full, g & 1);
+  named_bar_sync(kExBar, 128);
+  g_lse2[r] = my_lse2;
+  g_dvec[r] = my_d;
+  named_bar_sync(kExBar, 128);
   tc_fence_after();
 #pragma unroll
   for (int cc = 0; cc < 4; ++cc)
     tmem_ld32(c.lane_off + kColS + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(&p[cc * 32]));
   tmem_ld_wait();
-  // P^T[key][q] = exp2(S^T * scale*log2e - LSE_q * log2e); LSE is broadcast
-  // (every thread reads the same 128 values: L1 broadcast loads)
+  // P^T[key][q] = exp2(S^T * scale*log2e - LSE_q * log2e)
   const float sl = a.scale_log2;
   const bool diag = a.causal && it == 0;  // the diagonal tile (q0 == kv0)
 #pragma unroll
   for (int j4 = 0; j4 < kT / 4; ++j4) {
-    float4 l;
-    if (full) {
-      l = __ldg(reinterpret_cast<const float4*>(a.lse + row0) + j4);
-    } else {
-      const float* lp = a.lse + row0 + 4 * j4;
-      const int rem = c.S - q0 - 4 * j4;
-      l.x = rem > 0 ? lp[0] : INFINITY;
-      l.y = rem > 1 ? lp[1] : INFINITY;
-      l.z = rem > 2 ? lp[2] : INFINITY;
-      l.w = rem > 3 ? lp[3] : INFINITY;
-    }
+    const float4 l = reinterpret_cast<const float4*>(g_lse2)[j4];
     const float lv[4] = {l.x, l.y, l.z, l.w};
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int j = 4 * j4 + u;
-      float e = fast_exp2(fmaf(__uint_as_float(p[j]), sl, -lv[u] * kLog2e));
+      float e = fast_exp2(fmaf(__uint_as_float(p[j]), sl, -lv[u]));
       if (diag && key > q0 + j) e = 0.f;
       p[j] = __float_as_uint(e);
     }
@@ -175,18 +192,8 @@ __device__ __forceinline__ void exb_ds(const BwdCtx& c, const FaBwdArgs& a, cons
     uint32_t pk[16];
 #pragma unroll
     for (int j4 = 0; j4 < 8; ++j4) {
-      float4 d;
       const int j = cc * 32 + 4 * j4;
-      if (full) {
-        d = __ldg(reinterpret_cast<const float4*>(a.dvec + row0 + j));
-      } else {
-        const float* dpp = a.dvec + row0 + j;
-        const int rem = c.S - q0 - j;
-        d.x = rem > 0 ? dpp[0] : 0.f;
-        d.y = rem > 1 ? dpp[1] : 0.f;
-        d.z = rem > 2 ? dpp[2] : 0.f;
-        d.w = rem > 3 ? dpp[3] : 0.f;
-      }
+      const float4 d = reinterpret_cast<const float4*>(g_dvec)[j / 4];
       const float s0 = __uint_as_float(p[j + 0]) * (__uint_as_float(dp[4 * j4 + 0]) - d.x);
       const float s1 = __uint_as_float(p[j + 1]) * (__uint_as_float(dp[4 * j4 + 1]) - d.y);
       const float s2 = __uint_as_float(p[j + 2]) * (__uint_as_float(dp[4 * j4 + 2]) - d.z);
@@ -226,6 +233,10 @@ __device__ __forceinline__ void rd_op(const BwdCtx& c, const FaBwdArgs& a, const
   tmem_ld_wait();
   tc_fence_before();
   warp_arrive(&bar.s_free);  // S^T(i+1) may overwrite the columns
+  if (TWFA_BWD_WHATIF == 2) {
+    if (leader) mbar_arrive(&bar.ds_free);
+    return;
+  }
   // DQ_i has completed (dq_full): the dS buffer is free for staging
 #pragma unroll
   for (int pair = 0; pair < 2; ++pair) {
@@ -244,7 +255,7 @@ __device__ __forceinline__ void rd_op(const BwdCtx& c, const FaBwdArgs& a, const
     }
     fence_proxy_async_shared();
     named_bar_sync(kRdBar, 128);
-    if (leader) {
+    if (leader && TWFA_BWD_WHATIF != 1) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) tma_reduce_add_3d(&a.tm_dq, c.ds + h * kHalf, 32 * (2 * pair + h), q0, t.bh);
       bulk_commit();
@@ -329,6 +340,18 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
   const int it = r - static_cast<int>(op.stage);
   if (it < 0 || it >= t.N) return;
   const uint32_t g = t.gbase + static_cast<uint32_t>(it);
+#if TWFA_BWD_PROF
+  const bool prof = blockIdx.x == 0 && c.lane == 0 && (c.warp & 3u) == 3 && t.icount == 0 && (it == 20 || it == 21);
+  struct Out {
+    bool on; int kind, it; long long t0;
+    __device__ ~Out() {
+      if (on) {
+        const int n = atomicAdd(&g_prof_n, 1);
+        if (n < 64) { g_prof[n][0] = (int)(threadIdx.x / 32) * 1000 + kind * 10 + (it - 20); g_prof[n][1] = t0; g_prof[n][2] = clock64(); }
+      }
+    }
+  } out_{prof, op.kind, it, clock64()};
+#endif
   if (op.kind == TWFA_OP_EXB || op.kind == TWFA_OP_DS) {
     if constexpr (kRole == kHeavyRole) {
       if (op.kind == TWFA_OP_EXB) exb_ds<false>(c, a, t, it, g);  // DS is fused (lowering guarantees)
@@ -476,6 +499,9 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
   c.num_work = c.BH * c.nq;
   BwdBarriers& bar = g_bb;
   if (threadIdx.x == 0) {
+#if TWFA_BWD_PROF
+    g_prof_n = 0;
+#endif
     mbar_init(&bar.kv_full, 1);
     mbar_init(&bar.kv_empty, 1);
     for (int s = 0; s < 2; ++s) {
@@ -525,6 +551,10 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
   if (c.lane == 0) bulk_wait_all();
   tc_fence_before();
   __syncthreads();
+#if TWFA_BWD_PROF
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    for (int i = 0; i < g_prof_n && i < 64; ++i) printf("PROF %lld %lld %lld\n", g_prof[i][0], g_prof[i][1], g_prof[i][2]);
+#endif
   if (c.warp == 0) {
     tc_fence_after();
     tmem_dealloc<512>(0);
