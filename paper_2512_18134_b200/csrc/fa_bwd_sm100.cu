@@ -18,15 +18,17 @@
 //             (MN-major, the A operand of DQ); P^T stays in registers
 //   DV        dV  += P^T dO_i           TS, TMEM cols 128..
 //   DK        dK  += dS^T Q_i           TS, TMEM cols 0..
-//   DQ        dQ_i = dS K               SS (A MN-major) -> TMEM cols 256..
+//   DQ        dQ_i = dS K               SS (A MN-major) -> TMEM cols 384..
 //   RD        dQ_i (fp32) -> smem -> TMA reduce-add into the global dQ
 //             accumulator
 // after the last tile: dK * scale, dV -> bf16 -> global (RD warpgroup).
 // A pre-pass computes D_i = rowsum(dO_i * O_i); a post-pass scales dQ.
 //
 // Every cross-warp edge of the loop graph is an mbarrier; the aliasing edges
-// (DV -> DQ, DK -> DP) are realized by tcgen05 in-order execution on the
-// single issuing thread, which the lowering checks.
+// (DV -> ST(i+1): S^T(i+1) overwrites P^T(i); DK -> DQ: dQ_i overwrites
+// dS^T) are realized by tcgen05 in-order execution on the single issuing
+// thread, which the lowering checks. S^T(i+1) never waits for the dQ_i
+// read-out, so the next tile's exponentials overlap this tile's DS .. RD.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -66,7 +68,7 @@ struct __align__(8) BwdBarriers {
   uint64_t q_full[2], q_empty[2], o_full[2], o_empty[2];
   uint64_t s_full, dp_full, dq_full;  // tcgen05.commit
   uint64_t p_full, ds_full;           // EXB / DS warpgroup (4 warp arrivals)
-  uint64_t s_free;                    // RD warpgroup read dQ_i out of TMEM (4)
+  uint64_t q_free;                    // RD warpgroup read dQ_i out of TMEM (4)
   uint64_t ds_free;                   // RD is done with the dS buffer as staging (1)
   uint64_t acc_full;                  // dK, dV final for the work item (commit)
   uint64_t acc_free;                  // RD warpgroup read dK, dV (4)
@@ -79,7 +81,7 @@ __shared__ float g_lse2[kT], g_dvec[kT];
 constexpr uint32_t kExBar = 3;  // named barrier of the EXB / DS warpgroup
 #if TWFA_BWD_PROF
 __shared__ int g_prof_n;
-__shared__ long long g_prof[64][3];
+__shared__ long long g_prof[24][3];
 #endif
 
 struct BwdCtx {
@@ -229,10 +231,10 @@ __device__ __forceinline__ void rd_op(const BwdCtx& c, const FaBwdArgs& a, const
   tc_fence_after();
 #pragma unroll
   for (int cc = 0; cc < 4; ++cc)
-    tmem_ld32(c.lane_off + kColS + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(&v[cc * 32]));
+    tmem_ld32(c.lane_off + kColP + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(&v[cc * 32]));
   tmem_ld_wait();
   tc_fence_before();
-  warp_arrive(&bar.s_free);  // S^T(i+1) may overwrite the columns
+  warp_arrive(&bar.q_free);  // dP^T(i+1) may overwrite the columns
   if (TWFA_BWD_WHATIF == 2) {
     if (leader) mbar_arrive(&bar.ds_free);
     return;
@@ -347,7 +349,7 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
     __device__ ~Out() {
       if (on) {
         const int n = atomicAdd(&g_prof_n, 1);
-        if (n < 64) { g_prof[n][0] = (int)(threadIdx.x / 32) * 1000 + kind * 10 + (it - 20); g_prof[n][1] = t0; g_prof[n][2] = clock64(); }
+        if (n < 24) { g_prof[n][0] = (int)(threadIdx.x / 32) * 1000 + kind * 10 + (it - 20); g_prof[n][1] = t0; g_prof[n][2] = clock64(); }
       }
     }
   } out_{prof, op.kind, it, clock64()};
@@ -368,10 +370,7 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
   const bool release = op.flags & TWFA_OPF_RELEASE;
   if (op.kind == TWFA_OP_ST) {
     if (it == 0) mbar_wait(&bar.kv_full, t.icount & 1);
-    if (g > 0)
-      mbar_wait_all(&bar.q_full[qs], (g / plan.k_depth) & 1, &bar.s_free, (g - 1) & 1);
-    else
-      mbar_wait(&bar.q_full[qs], (g / plan.k_depth) & 1);
+    mbar_wait(&bar.q_full[qs], (g / plan.k_depth) & 1);  // P^T(g-1) was read by DV(g-1): in order
     tc_fence_after();
     const uint32_t ad = sd_lo(c.k, 16), bd = sd_lo(c.q + qs * kTile, 16);
     if (elect_one()) {
@@ -386,7 +385,10 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
     __syncwarp();
   } else if (op.kind == TWFA_OP_DP) {
     if (it == 0) mbar_wait(&bar.kv_full, t.icount & 1);
-    mbar_wait(&bar.o_full[os], (g / plan.v_depth) & 1);
+    if (g > 0)  // dQ_(g-1) (over dP^T) has been read out
+      mbar_wait_all(&bar.o_full[os], (g / plan.v_depth) & 1, &bar.q_free, (g - 1) & 1);
+    else
+      mbar_wait(&bar.o_full[os], (g / plan.v_depth) & 1);
     tc_fence_after();
     const uint32_t ad = sd_lo(c.v, 16), bd = sd_lo(c.o + os * kTile, 16);
     if (elect_one()) {
@@ -428,7 +430,7 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
     if (elect_one()) {
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk)
-        mma_ss(kColS, sdesc_join(ad + kk * 2048 / 16, kSdHi), sdesc_join(bd + kk * 2048 / 16, kSdHi), kIdescMM,
+        mma_ss(kColP, sdesc_join(ad + kk * 2048 / 16, kSdHi), sdesc_join(bd + kk * 2048 / 16, kSdHi), kIdescMM,
                kk > 0);
       mma_commit(&bar.dq_full);
     }
@@ -515,7 +517,7 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
     mbar_init(&bar.dq_full, 1);
     mbar_init(&bar.p_full, 4);
     mbar_init(&bar.ds_full, 4);
-    mbar_init(&bar.s_free, 4);
+    mbar_init(&bar.q_free, 4);
     mbar_init(&bar.ds_free, 1);
     mbar_init(&bar.acc_full, 1);
     mbar_init(&bar.acc_free, 4);
@@ -553,7 +555,7 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
   __syncthreads();
 #if TWFA_BWD_PROF
   if (blockIdx.x == 0 && threadIdx.x == 0)
-    for (int i = 0; i < g_prof_n && i < 64; ++i) printf("PROF %lld %lld %lld\n", g_prof[i][0], g_prof[i][1], g_prof[i][2]);
+    for (int i = 0; i < g_prof_n && i < 24; ++i) printf("PROF %lld %lld %lld\n", g_prof[i][0], g_prof[i][1], g_prof[i][2]);
 #endif
   if (c.warp == 0) {
     tc_fence_after();

@@ -182,7 +182,7 @@ def test_fa_bwd_plan_roles_follow_the_solver(twfa):
     (lambda s: s["A"].update(DS=4), "share a warpgroup"),
     (lambda s: s["A"].update(DQ=14), "issue from one warp"),
     (lambda s: s["A"].update(RD=12), "cannot be inside"),
-    (lambda s: s["M"].update(DS=13, DK=13), "violates dependence|directly follow"),
+    (lambda s: s["M"].update(DS=s["M"]["EXB"]), "violates dependence"),
 ])
 def test_fa_bwd_unrealizable_solutions_are_rejected(twfa, mutate, msg):
     prob, sol = twfa.load_schedule("fa_bwd")

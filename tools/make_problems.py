@@ -169,7 +169,7 @@ def fa_forward_problem(tc_variable_latency=False, calibrated=False, s_ring=1, sp
     return {"machine": machine, "graph": {"nodes": nodes, "edges": edges}}
 
 
-def fa_backward_problem():
+def fa_backward_problem(calibrated=False):
     """FA-backward loop body on sm_100a (the paper's second workload,
     PAPER.md:1073-1148; the single-pass algorithm of FA3): one CTA owns a
     128-key K/V tile (K, V resident in shared memory, dK and dV accumulated
@@ -185,11 +185,13 @@ def fa_backward_problem():
       DQ        dQ_i = dS K              tcgen05.mma SS -> TMEM over S^T
       RD        dQ_i -> global           tcgen05.ld + TMA reduce-add (fp32)
 
-    Tensor memory (512 columns): dK, dV, S^T (P^T, dQ_i), dP^T (dS^T), 128
-    each. The aliasing is carried by edges: DV -> DQ (DQ overwrites the P^T
-    DV reads; in order on the issuing thread), RD -> ST (delta 1: S^T(i+1)
-    needs dQ_i read out), DK -> DP (delta 1: dP^T(i+1) overwrites dS^T(i)),
-    RD -> DS (delta 1: dS(i+1) reuses the smem buffer RD stages dQ_i in).
+    Tensor memory (512 columns): dK, dV, S^T (P^T), dP^T (dS^T, then dQ_i),
+    128 each. The aliasing is carried by edges: DV -> ST (delta 1: S^T(i+1)
+    overwrites the P^T DV(i) reads; in order on the issuing thread), DK -> DQ
+    (DQ overwrites the dS^T DK reads; in order), RD -> DP (delta 1: dP^T(i+1)
+    needs dQ_i read out), RD -> DS (delta 1: dS(i+1) reuses the smem buffer
+    RD stages dQ_i in). S^T(i+1) thus only waits for DV(i): the exponentials
+    of the next tile overlap DS, DK, DQ and RD of this one.
     EXB -> DS carries P in registers (spill cost: a re-read of P from tensor
     memory in bf16 changes the numerics, so a large cost keeps them on one
     warpgroup). The tensor-core ops are variable latency (the production
@@ -208,12 +210,15 @@ def fa_backward_problem():
         "vl_warp": 15,
     }
     g = 2  # one 128x128x128 tcgen05 GEMM
+    # calibrated: the in-kernel clock profile of the realized loop
+    # (TWFA_BWD_PROF): EXB ~1500 clk incl. the TMEM read of S^T, DS ~1000
+    ex, dsc = (6, 4) if calibrated else (4, 2)
     nodes = [node("LDQ", "TMA", 2, variable_latency=True), node("LDO", "TMA", 2, variable_latency=True)]
     for v in ("ST", "DP"):
         nodes.append(node(v, "TC", g, footprint={"tmem": 128}, variable_latency=True))
     nodes += [
-        node("EXB", "MUFU", 4, regs=128, spill_cost=16, warps_required=4),
-        node("DS", "FMA", 2, regs=64, warps_required=4),
+        node("EXB", "MUFU", ex, regs=128, spill_cost=16, warps_required=4),
+        node("DS", "FMA", dsc, regs=64, warps_required=4),
         node("DV", "TC", g, variable_latency=True),
         node("DK", "TC", g, variable_latency=True),
         node("DQ", "TC", g, variable_latency=True),
@@ -223,16 +228,16 @@ def fa_backward_problem():
         edge("LDQ", "ST", 0, blocking=True), edge("LDQ", "DK", 0, blocking=True),
         edge("LDO", "DP", 0, blocking=True), edge("LDO", "DV", 0, blocking=True),
         edge("ST", "EXB", g, blocking=True),
-        edge("EXB", "DV", 4, blocking=True), edge("EXB", "DS", 4),
+        edge("EXB", "DV", ex, blocking=True), edge("EXB", "DS", ex),
         edge("DP", "DS", g, blocking=True),
-        edge("DS", "DK", 2, blocking=True), edge("DS", "DQ", 2, blocking=True),
+        edge("DS", "DK", dsc, blocking=True), edge("DS", "DQ", dsc, blocking=True),
         edge("DQ", "RD", g, blocking=True),
-        edge("DV", "DQ", 0),
-        edge("RD", "ST", 2, delta=1, blocking=True),
-        edge("DK", "DP", 0, delta=1),
+        edge("DV", "ST", 0, delta=1),
+        edge("DK", "DQ", 0),
+        edge("RD", "DP", 2, delta=1, blocking=True),
         edge("RD", "DS", 2, delta=1, blocking=True),
         edge("DV", "DV", g, delta=1), edge("DK", "DK", g, delta=1),
-        edge("EXB", "EXB", 4, delta=1), edge("DS", "DS", 2, delta=1), edge("RD", "RD", 2, delta=1),
+        edge("EXB", "EXB", ex, delta=1), edge("DS", "DS", dsc, delta=1), edge("RD", "RD", 2, delta=1),
     ]
     for n in nodes:
         n["cycles"] *= T
@@ -339,6 +344,7 @@ def main():
         "fa_fwd_ring2": (fa_forward_problem(tc_variable_latency=True, s_ring=2), 4, None),
         # FA backward (single pass, K/V-stationary), datasheet costs
         "fa_bwd": (fa_backward_problem(), 2, 11),  # {512, 1024, 4096} clk exactly (F = 0)
+        "fa_bwd_cal": (fa_backward_problem(calibrated=True), 2, 14),
     }
     for name, (raw, depth, res) in probs.items():
         if args.only and name != args.only:
