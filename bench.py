@@ -324,6 +324,27 @@ def run_ours(args, world, rank, local):
     per_launch_ms = ms_local / args.steps
     achieved = flops / (per_launch_ms * 1e-3) / 1e12
 
+    # FA backward of the same workload (the paper's second loop; reported
+    # beside the headline, not part of it): dQ, dK, dV from Q, K, V, O, dO
+    # and the forward's LSE, 5 GEMMs = 10 B H S^2 d flops (causal: half)
+    bplan = twfa.Plan(*twfa.load_schedule("fa_bwd"))
+    o_f, lse = twfa.fa_fwd(plan, q, k, v, causal=causal, return_lse=True)
+    dout = torch.randn_like(q)
+    ws = torch.empty(B * H * S * 129 * 4, device=dev, dtype=torch.uint8)
+    bwd_steps = max(1, min(args.steps, 10))
+    for _ in range(3):
+        twfa.fa_bwd(bplan, q, k, v, o_f, dout, lse, causal=causal, workspace=ws)
+    torch.cuda.synchronize()
+    barrier(world)
+    e0.record(stream)
+    for _ in range(bwd_steps):
+        twfa.fa_bwd(bplan, q, k, v, o_f, dout, lse, causal=causal, workspace=ws)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    bwd_ms = max_over_ranks(e0.elapsed_time(e1), world) / bwd_steps
+    bwd_flops = 2.5 * flops
+    del o_f, lse, dout, ws
+
     # end to end through the public API with host buffers: pinned H2D of
     # Q, K, V, the kernel, D2H of O, every step
     hq, hk, hv = (x.cpu().pin_memory() for x in (q, k, v))
@@ -377,6 +398,11 @@ def run_ours(args, world, rank, local):
         "clocks": clocks.summary(),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "steps": e2e_steps, "path": "pinned host -> device copies + twfa fa_fwd + device -> host O"},
+        "fa_bwd": {"value": bwd_flops * world / (bwd_ms * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": bwd_ms,
+                   "steps": bwd_steps, "flops_per_step_per_gpu": bwd_flops,
+                   "schedule": "fa_bwd.solution.json (I=%d)" % bplan.describe()["I"],
+                   "note": "backward of the same workload; 4 launches per step (D pre-pass, dQ "
+                           "accumulator memset, main kernel, dQ post-pass); not the headline metric"},
         "gpu_launches": args.steps,
         "tensor_pipe": ncu_tensor_util(workload),
         "schedule_realized": realized_schedule(twfa, plan, q, k, v, causal),
