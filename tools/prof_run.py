@@ -17,6 +17,15 @@ if what in ("fa", "fa_causal"):
     q, k, v = (torch.randn(B, H, S, 128, device=dev).to(torch.bfloat16) for _ in range(3))
     for _ in range(n):
         twfa.fa_fwd(p, q, k, v, causal=(what == "fa_causal"))
+elif what in ("bwd", "bwd_causal"):
+    fp = twfa.Plan(*twfa.load_schedule("fa_fwd"))
+    bp = twfa.Plan(*twfa.load_schedule("fa_bwd"))
+    B, H, S = (4, 32, 8192) if what == "bwd" else (2, 32, 16384)
+    c = what == "bwd_causal"
+    q, k, v, do = (torch.randn(B, H, S, 128, device=dev).to(torch.bfloat16) for _ in range(4))
+    o, lse = twfa.fa_fwd(fp, q, k, v, causal=c, return_lse=True)
+    for _ in range(n):
+        twfa.fa_bwd(bp, q, k, v, o, do, lse, causal=c)
 elif what == "gemm":
     p = twfa.Plan(*twfa.load_schedule("gemm_mainloop"))
     a = torch.randn(8192, 8192, device=dev).to(torch.bfloat16)
