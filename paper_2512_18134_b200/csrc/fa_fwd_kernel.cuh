@@ -234,6 +234,75 @@ __device__ __forceinline__ float exp_store_row(const uint32_t (&s)[N], uint32_t 
   return (acc[0].x + acc[0].y) + (acc[1].x + acc[1].y);
 }
 
+// Fused MX_k + EX_k that starts the exponentials before the row max is
+// known. With the rescale threshold the running max rarely moves after the
+// first tiles, so chunk 0 of the S row is loaded first and exponentiated with
+// m_old while the rest of the row is still in flight from tensor memory.
+// Once the whole row is in registers its max decides, per row, whether m
+// moves; if any row of the warp moved, chunk 0 is recomputed with the new max
+// before anything is stored. The stored P and the row sum are therefore
+// exactly those of MX_k followed by EX_k; only the TMEM read of the row and
+// the max leave the S -> P critical path. `handoff(alpha)` passes the rescale
+// factor to the correction warpgroup once the max is known.
+#ifndef TWFA_SPEC_EX
+#define TWFA_SPEC_EX 1
+#endif
+template <int N, class Handoff>
+__device__ __forceinline__ float mx_ex_spec(uint32_t (&s)[N], uint32_t taddr, float sl, float& m_io, float& alpha,
+                                            uint64_t* part_bar, Handoff&& handoff) {
+  constexpr int kParts = kPParts;
+  constexpr int kPartKeys = N / kParts;
+  constexpr int kKeys = kPartKeys < 32 ? kPartKeys : 32;
+  constexpr int kRegs = kKeys / 2;
+  tmem_ld32(taddr, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
+  tmem_ld_wait();
+#pragma unroll
+  for (int c = 1; c < N / 32; ++c) tmem_ld32(taddr + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&s[c * 32]));
+  const float m_old = m_io;
+  const float2 sl2 = make_float2(sl, sl);
+  float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+  uint32_t pk0[kRegs];
+  auto chunk = [&](int c, float m, uint32_t (&pk)[kRegs]) {
+    const float2 nm2 = make_float2(-m, -m);
+#pragma unroll
+    for (int i = 0; i < kKeys; i += 2) {
+      const int e = c * kKeys + i;
+      const float2 x = ffma2(make_float2(__uint_as_float(s[e]), __uint_as_float(s[e + 1])), sl2, nm2);
+      float2 p;
+      p.x = fast_exp2(x.x);
+      p.y = fast_exp2(x.y);
+      acc[(i >> 1) & 1] = fadd2(acc[(i >> 1) & 1], p);
+      pk[i >> 1] = pack_bf16(p.x, p.y);
+    }
+  };
+  chunk(0, m_old, pk0);
+  tmem_ld_wait();
+  const float mx = row_max<N>(s);
+  const float m_cand = fmaxf(m_old, mx * sl);
+  const float m_new = (m_cand - m_old > kRescaleLog2) ? m_cand : m_old;
+  if (__any_sync(0xffffffffu, m_new != m_old)) {
+    acc[0] = acc[1] = make_float2(0.f, 0.f);
+    chunk(0, m_new, pk0);
+  }
+  alpha = m_new == m_old ? 1.f : fast_exp2(m_old - m_new);
+  m_io = m_new;
+  handoff(alpha);
+  tmem_st<kRegs>(taddr, pk0);
+#pragma unroll
+  for (int c = 1; c < N / kKeys; ++c) {
+    uint32_t pk[kRegs];
+    chunk(c, m_new, pk);
+    if ((c * kKeys) % kPartKeys == 0) {
+      tmem_st_wait();
+      tc_fence_before();
+      warp_arrive(&part_bar[c * kKeys / kPartKeys - 1]);
+    }
+    tmem_st<kRegs>(taddr + c * kRegs, pk);
+  }
+  tmem_st_wait();
+  return (acc[0].x + acc[0].y) + (acc[1].x + acc[1].y);
+}
+
 // ---------------------------------------------------------------- state
 struct FaCtx {
   uint8_t* q_smem;
@@ -494,6 +563,36 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
           mbar_wait(&bar.s_full[k][b], pb);
         trace_mark<kTrace>(tr, 4);
         tc_fence_after();
+        if constexpr (KV == 128) {
+          const float m_old = rd(st.m_run, k);
+          if (TWFA_SPEC_EX && !rg.split && !mask && (op.flags & TWFA_OPF_FUSE_NEXT) &&
+              __all_sync(0xffffffffu, m_old != -INFINITY)) {
+            float m = m_old, alpha = 1.f;
+            const uint32_t sb = g & 1;
+            const float sum = mx_ex_spec<KV>(srow, taddr, c.scale_log2, m, alpha, bar.p_part[k][b], [&](float al) {
+              mbar_wait(&bar.st_empty[k][sb], ((g >> 1) & 1) ^ 1);
+              g_sh.stats[k][sb][c.quad * 32 + lane] = al;
+              warp_arrive(&bar.st_full[k][sb]);
+            });
+            wr(st.m_run, k, m);
+            wr(st.alpha, k, alpha);
+            wr(st.l_run, k, rd(st.l_run, k) * alpha + sum);
+            tc_fence_before();
+            warp_arrive(&bar.p_part[k][b][kPParts - 1]);
+            if (it == N - 1) {
+              mbar_wait(&bar.l_empty[k], (t.tcount & 1) ^ 1);
+              g_sh.lbuf[k][0][c.quad * 32 + lane] = m;
+              g_sh.lbuf[k][1][c.quad * 32 + lane] = rd(st.l_run, k);
+              warp_arrive(&bar.l_full[k]);
+            }
+            // the trace keeps one record per op: EX_k ran inside this MX_k
+            trace_mark<kTrace>(tr, 5);
+            uint32_t* tr_ex = trace_begin<kTrace>(args, warp, st.trace_n, op.node + 1, it, r);
+            trace_mark<kTrace>(tr_ex, 4);
+            trace_mark<kTrace>(tr_ex, 5);
+            return;
+          }
+        }
         if (TWFA_WHATIF == 3) {
 #pragma unroll
           for (int c2 = 0; c2 < KV / 64; ++c2)

@@ -8,6 +8,7 @@
 #include "../../paper_2512_18134_b200/csrc/sm100.cuh"
 using namespace twfa;
 constexpr int kN = 48;
+template <bool kTS>
 __global__ void __launch_bounds__(128, 1) k_mmaq(uint32_t* out) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t tbase;
@@ -28,7 +29,10 @@ __global__ void __launch_bounds__(128, 1) k_mmaq(uint32_t* out) {
       t[0] = static_cast<uint32_t>(clock64());
 #pragma unroll
       for (int i = 0; i < kN; ++i) {
-        mma_ss(0, sdesc_join(a + (i & 3) * 2, hi), sdesc_join(b + (i & 3) * 2, hi), idesc_bf16_f32(128, 128, 0), i > 0);
+        if constexpr (kTS)  // A (bf16) from tensor memory columns 256.., like PV of the FA kernel
+          mma_ts(0, 256 + (i & 7) * 8, sdesc_join(b + (i & 3) * 128, hi), idesc_bf16_f32(128, 128, 1), i > 0);
+        else
+          mma_ss(0, sdesc_join(a + (i & 3) * 2, hi), sdesc_join(b + (i & 3) * 2, hi), idesc_bf16_f32(128, 128, 0), i > 0);
         t[i + 1] = static_cast<uint32_t>(clock64());
       }
       mma_commit(&done);
@@ -42,15 +46,18 @@ __global__ void __launch_bounds__(128, 1) k_mmaq(uint32_t* out) {
   __syncthreads();
   if (warp == 0) { tc_fence_after(); tmem_dealloc<512>(tbase); }
 }
-int main() {
+template <bool kTS>
+int run(const char* name) {
   uint32_t* d; cudaMalloc(&d, 4 * (kN + 2));
-  cudaFuncSetAttribute(k_mmaq, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
-  for (int rep = 0; rep < 3; ++rep) k_mmaq<<<1, 128, 65536>>>(d);
+  cudaFuncSetAttribute(k_mmaq<kTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+  for (int rep = 0; rep < 3; ++rep) k_mmaq<kTS><<<1, 128, 65536>>>(d);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
   uint32_t h[kN + 2]; cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
-  printf("issue clock after MMA i (M128 N128 K16, 64 clk each at full rate):\n");
+  printf("%s: issue clock after MMA i (M128 N128 K16, 64 clk each at full rate):\n", name);
   for (int i = 1; i <= kN; ++i) printf("%d:%u%s", i, h[i], i % 8 ? " " : "\n");
   printf("all complete: %u clk\n", h[kN + 1]);
+  cudaFree(d);
   return 0;
 }
+int main() { return run<false>("SS") | run<true>("TS (A in TMEM)"); }
