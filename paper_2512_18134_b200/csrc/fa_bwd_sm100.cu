@@ -52,9 +52,8 @@ constexpr uint32_t kIdescKK = idesc_bf16_f32(128, 128, 0);  // A, B K-major
 constexpr uint32_t kIdescKM = idesc_bf16_f32(128, 128, 1);  // A K-major (or TMEM), B MN-major
 constexpr uint32_t kIdescMM = idesc_bf16_f32(128, 128, 1) | (1u << 15);  // A and B MN-major
 constexpr uint32_t kSdHi = sdesc_hi(1024);
-constexpr uint32_t kRdBar = 2;  // named barrier of the RD warpgroup
-// timing-only experiments (results WRONG when set): 1 = RD skips the
-// reduce-add, 2 = RD skips staging and reduce
+// timing-only experiment (results WRONG when set): 1 = RD skips the
+// reduce-add
 #ifndef TWFA_BWD_WHATIF
 #define TWFA_BWD_WHATIF 0
 #endif
@@ -68,6 +67,7 @@ struct __align__(8) BwdBarriers {
   uint64_t q_full[2], q_empty[2], o_full[2], o_empty[2];
   uint64_t s_full, dp_full, dq_full;  // tcgen05.commit
   uint64_t p_full, ds_full;           // EXB / DS warpgroup (4 warp arrivals)
+  uint64_t p_read;                    // DS on its own warpgroup read P^T back (4)
   uint64_t q_free;                    // RD warpgroup read dQ_i out of TMEM (4)
   uint64_t ds_free;                   // RD is done with the dS buffer as staging (1)
   uint64_t acc_full;                  // dK, dV final for the work item (commit)
@@ -78,7 +78,6 @@ __shared__ BwdBarriers g_bb;
 // LSE * log2(e) and D of the current Q tile, broadcast to the EXB / DS
 // warpgroup (thread t stages query q0 + t)
 __shared__ float g_lse2[kT], g_dvec[kT];
-constexpr uint32_t kExBar = 3;  // named barrier of the EXB / DS warpgroup
 #if TWFA_BWD_PROF
 __shared__ int g_prof_n;
 __shared__ long long g_prof[24][3];
@@ -126,28 +125,31 @@ struct BwdState {
 
 __device__ __forceinline__ uint32_t sd_lo(const void* p, uint32_t lbo) { return sdesc_lo(smem_u32(p), lbo); }
 
-// P^T row of this thread (key kv0 + r) for Q tile q0: 128 fp32 registers
-// carried from EXB into the fused DS.
-template <bool kTrace>
-__device__ __forceinline__ void exb_ds(const BwdCtx& c, const FaBwdArgs& a, const BwdItem& t, int it,
-                                       uint32_t g) {
+// Stage one per-query vector of the current Q tile (LSE * log2e or D) in
+// shared memory for the warpgroup: thread t loads query q0 + t, the group
+// synchronizes on its named barrier before (previous tile's readers done)
+// and after the store.
+__device__ __forceinline__ void stage_tile_vec(float* dst, float v, uint32_t r, uint32_t bar_id) {
+  named_bar_sync(bar_id, 128);
+  dst[r] = v;
+  named_bar_sync(bar_id, 128);
+}
+
+// EXB: P^T row of this thread (key kv0 + r) for Q tile q0, stored to TMEM as
+// bf16 over S^T; the fp32 values stay in p[] for a fused DS.
+__device__ __forceinline__ void exb_part(const BwdCtx& c, const FaBwdArgs& a, const BwdItem& t, int it, uint32_t g,
+                                         uint32_t (&p)[kT]) {
   BwdBarriers& bar = g_bb;
   const int q0 = (t.q_first + it) * kT;
   const uint32_t r = c.quad * 32 + c.lane;
   const int key = t.kv0 + static_cast<int>(r);
   const int64_t row0 = static_cast<int64_t>(t.bh) * c.S + q0;
-  // this tile's LSE / D: one coalesced load per thread, issued before the
-  // S^T wait; staged in shared memory once every thread of the group is
-  // done with the previous tile's values
+  // this tile's LSE: one coalesced load per thread, issued before the S^T
+  // wait, then broadcast through shared memory
   const int qt = q0 + static_cast<int>(r);
   const float my_lse2 = qt < c.S ? a.lse[row0 + r] * kLog2e : INFINITY;  // rows past S: P = 0
-  const float my_d = qt < c.S ? a.dvec[row0 + r] : 0.f;
-  uint32_t p[kT];
   mbar_wait(&bar.s_full, g & 1);
-  named_bar_sync(kExBar, 128);
-  g_lse2[r] = my_lse2;
-  g_dvec[r] = my_d;
-  named_bar_sync(kExBar, 128);
+  stage_tile_vec(g_lse2, my_lse2, r, 1 + (c.warp >> 2));
   tc_fence_after();
 #pragma unroll
   for (int cc = 0; cc < 4; ++cc)
@@ -172,17 +174,42 @@ __device__ __forceinline__ void exb_ds(const BwdCtx& c, const FaBwdArgs& a, cons
   for (int cc = 0; cc < 4; ++cc) {
     uint32_t pk[16];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(__uint_as_float(p[cc * 32 + 2 * i]), __uint_as_float(p[cc * 32 + 2 * i + 1]));
+    for (int i = 0; i < 16; ++i)
+      pk[i] = pack_bf16(__uint_as_float(p[cc * 32 + 2 * i]), __uint_as_float(p[cc * 32 + 2 * i + 1]));
     tmem_st16(c.lane_off + kColS + cc * 16, pk);
   }
   tmem_st_wait();
   tc_fence_before();
   warp_arrive(&bar.p_full);
+}
 
-  // DS: dS^T = P^T (dP^T - D_q), chunk by chunk over the dP^T columns; the
-  // bf16 chunk goes to TMEM (over dP^T columns already read) for DK and to
-  // the smem A operand of DQ (MN-major: row = key, 64 queries per SW128 half)
+// DS: dS^T = P^T (dP^T - D_q), chunk by chunk over the dP^T columns; the
+// bf16 chunk goes to TMEM (over dP^T columns already read) for DK and to the
+// smem A operand of DQ (MN-major: row = key, 64 queries per SW128 half).
+// kFused: P^T in fp32 registers from the EXB just before on this warpgroup;
+// otherwise DS runs on its own warpgroup and reads P^T (bf16) back from
+// tensor memory first, then releases the columns to S^T(i+1) (p_read).
+template <bool kFused>
+__device__ __forceinline__ void ds_part(const BwdCtx& c, const FaBwdArgs& a, const BwdItem& t, int it, uint32_t g,
+                                        const uint32_t (&p)[kT]) {
+  BwdBarriers& bar = g_bb;
+  const int q0 = (t.q_first + it) * kT;
+  const uint32_t r = c.quad * 32 + c.lane;
+  const int64_t row0 = static_cast<int64_t>(t.bh) * c.S + q0;
+  const int qt = q0 + static_cast<int>(r);
+  const float my_d = qt < c.S ? a.dvec[row0 + r] : 0.f;
+  uint32_t pp[kFused ? 1 : kT / 2];  // packed bf16 P^T (unfused)
+  if constexpr (!kFused) {
+    mbar_wait(&bar.p_full, g & 1);
+    tc_fence_after();
+    tmem_ld32(c.lane_off + kColS, *reinterpret_cast<uint32_t(*)[32]>(&pp[0]));
+    tmem_ld32(c.lane_off + kColS + 32, *reinterpret_cast<uint32_t(*)[32]>(&pp[32]));
+    tmem_ld_wait();
+    tc_fence_before();
+    warp_arrive(&bar.p_read);
+  }
   if (g > 0) mbar_wait(&bar.ds_free, (g - 1) & 1);
+  stage_tile_vec(g_dvec, my_d, r, 1 + (c.warp >> 2));
   mbar_wait(&bar.dp_full, g & 1);
   tc_fence_after();
   const uint32_t ds_base = smem_u32(c.ds) + r * 128;
@@ -196,10 +223,22 @@ __device__ __forceinline__ void exb_ds(const BwdCtx& c, const FaBwdArgs& a, cons
     for (int j4 = 0; j4 < 8; ++j4) {
       const int j = cc * 32 + 4 * j4;
       const float4 d = reinterpret_cast<const float4*>(g_dvec)[j / 4];
-      const float s0 = __uint_as_float(p[j + 0]) * (__uint_as_float(dp[4 * j4 + 0]) - d.x);
-      const float s1 = __uint_as_float(p[j + 1]) * (__uint_as_float(dp[4 * j4 + 1]) - d.y);
-      const float s2 = __uint_as_float(p[j + 2]) * (__uint_as_float(dp[4 * j4 + 2]) - d.z);
-      const float s3 = __uint_as_float(p[j + 3]) * (__uint_as_float(dp[4 * j4 + 3]) - d.w);
+      float pv[4];
+      if constexpr (kFused) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) pv[u] = __uint_as_float(p[j + u]);
+      } else {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const uint32_t w = pp[j / 2 + u];
+          pv[2 * u] = __uint_as_float(w << 16);
+          pv[2 * u + 1] = __uint_as_float(w & 0xffff0000u);
+        }
+      }
+      const float s0 = pv[0] * (__uint_as_float(dp[4 * j4 + 0]) - d.x);
+      const float s1 = pv[1] * (__uint_as_float(dp[4 * j4 + 1]) - d.y);
+      const float s2 = pv[2] * (__uint_as_float(dp[4 * j4 + 2]) - d.z);
+      const float s3 = pv[3] * (__uint_as_float(dp[4 * j4 + 3]) - d.w);
       pk[2 * j4] = pack_bf16(s0, s1);
       pk[2 * j4 + 1] = pack_bf16(s2, s3);
     }
@@ -226,40 +265,36 @@ __device__ __forceinline__ void rd_op(const BwdCtx& c, const FaBwdArgs& a, const
   const int q0 = (t.q_first + it) * kT;
   const uint32_t r = c.quad * 32 + c.lane;
   const bool leader = (c.warp & 3u) == 0 && c.lane == 0;
-  uint32_t v[kT];
+  const uint32_t nb = 1 + (c.warp >> 2);  // named barrier of this warpgroup
   mbar_wait(&bar.dq_full, g & 1);
   tc_fence_after();
-#pragma unroll
-  for (int cc = 0; cc < 4; ++cc)
-    tmem_ld32(c.lane_off + kColP + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(&v[cc * 32]));
-  tmem_ld_wait();
-  tc_fence_before();
-  warp_arrive(&bar.q_free);  // dP^T(i+1) may overwrite the columns
-  if (TWFA_BWD_WHATIF == 2) {
-    if (leader) mbar_arrive(&bar.ds_free);
-    return;
-  }
-  // DQ_i has completed (dq_full): the dS buffer is free for staging
-#pragma unroll
-  for (int pair = 0; pair < 2; ++pair) {
-    if (pair == 1) {
-      if (leader) bulk_wait_read();
-      named_bar_sync(kRdBar, 128);
+  // DQ_i has completed (dq_full): the dS buffer is free for staging. Two
+  // halves of 64 columns (two 16 KiB boxes each) keep the row at 64 registers.
+#pragma unroll 1
+  for (int h = 0; h < 2; ++h) {
+    uint32_t v[64];
+    tmem_ld32(c.lane_off + kColP + h * 64, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+    tmem_ld32(c.lane_off + kColP + h * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+    tmem_ld_wait();
+    if (h == 1) {
+      tc_fence_before();
+      warp_arrive(&bar.q_free);      // dP^T(i+1) may overwrite the columns
+      if (leader) bulk_wait_read();  // half 0's reduce has read the staging buffer
+      named_bar_sync(nb, 128);
     }
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int box = 2 * pair + h;
-      const uint32_t base = smem_u32(c.ds) + h * kHalf + r * 128;
+    for (int box = 0; box < 2; ++box) {
+      const uint32_t base = smem_u32(c.ds) + box * kHalf + r * 128;
 #pragma unroll
       for (int ch = 0; ch < 8; ++ch)
         st_shared_v4(base + ((ch ^ (r & 7)) << 4), v[box * 32 + 4 * ch], v[box * 32 + 4 * ch + 1],
                      v[box * 32 + 4 * ch + 2], v[box * 32 + 4 * ch + 3]);
     }
     fence_proxy_async_shared();
-    named_bar_sync(kRdBar, 128);
+    named_bar_sync(nb, 128);
     if (leader && TWFA_BWD_WHATIF != 1) {
 #pragma unroll
-      for (int h = 0; h < 2; ++h) tma_reduce_add_3d(&a.tm_dq, c.ds + h * kHalf, 32 * (2 * pair + h), q0, t.bh);
+      for (int box = 0; box < 2; ++box) tma_reduce_add_3d(&a.tm_dq, c.ds + box * kHalf, 64 * h + 32 * box, q0, t.bh);
       bulk_commit();
     }
   }
@@ -305,9 +340,11 @@ __device__ __forceinline__ void kv_epilogue(const BwdCtx& c, const FaBwdArgs& a,
 }
 
 // Register classes (each compiled under its setmaxnreg budget): the TMA / MMA
-// warps, the RD warpgroup (RD + the dK / dV epilogue), the EXB / DS
-// warpgroup (which also runs RD when the schedule puts it there).
-enum BwdRole { kLight = 0, kReduce = 1, kHeavyRole = 2 };
+// warps, the RD warpgroup (RD + the dK / dV epilogue), and the EXB and DS
+// warpgroups -- one warpgroup running both (P^T carried in registers) or
+// one each (DS reads P^T back from tensor memory), as the schedule places
+// them.
+enum BwdRole { kLight = 0, kReduce = 1, kExbDs = 2, kExb = 3, kDs = 4 };
 
 // One op of the trip program on this warp, trip r.
 template <int kRole>
@@ -355,13 +392,19 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
   } out_{prof, op.kind, it, clock64()};
 #endif
   if (op.kind == TWFA_OP_EXB || op.kind == TWFA_OP_DS) {
-    if constexpr (kRole == kHeavyRole) {
-      if (op.kind == TWFA_OP_EXB) exb_ds<false>(c, a, t, it, g);  // DS is fused (lowering guarantees)
+    if constexpr (kRole == kExbDs || kRole == kExb || kRole == kDs) {
+      uint32_t p[kT];
+      if (op.kind == TWFA_OP_EXB) {
+        exb_part(c, a, t, it, g, p);
+        if constexpr (kRole == kExbDs) ds_part<true>(c, a, t, it, g, p);  // fused (lowering guarantees)
+      } else if constexpr (kRole == kDs) {
+        ds_part<false>(c, a, t, it, g, p);
+      }
     }
     return;
   }
   if (op.kind == TWFA_OP_RD) {
-    if constexpr (kRole != kLight) rd_op(c, a, t, it, g);
+    if constexpr (kRole == kReduce) rd_op(c, a, t, it, g);
     return;
   }
   if constexpr (kRole != kLight) return;
@@ -370,7 +413,12 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
   const bool release = op.flags & TWFA_OPF_RELEASE;
   if (op.kind == TWFA_OP_ST) {
     if (it == 0) mbar_wait(&bar.kv_full, t.icount & 1);
-    mbar_wait(&bar.q_full[qs], (g / plan.k_depth) & 1);  // P^T(g-1) was read by DV(g-1): in order
+    // P^T(g-1) was read by DV(g-1) (in order) and, with DS on its own
+    // warpgroup, by DS(g-1) (p_read)
+    if (g > 0 && (op.flags & TWFA_OPF_WAIT_PREAD))
+      mbar_wait_all(&bar.q_full[qs], (g / plan.k_depth) & 1, &bar.p_read, (g - 1) & 1);
+    else
+      mbar_wait(&bar.q_full[qs], (g / plan.k_depth) & 1);
     tc_fence_after();
     const uint32_t ad = sd_lo(c.k, 16), bd = sd_lo(c.q + qs * kTile, 16);
     if (elect_one()) {
@@ -444,7 +492,6 @@ __device__ __forceinline__ void bwd_run(const BwdCtx& c, const TwfaDevicePlan& p
   const int plen = plan.prog_len[c.warp];
   const bool is_load = c.warp == static_cast<uint32_t>(plan.load_warp);
   const bool is_mma = c.warp == static_cast<uint32_t>(plan.mma_warp);
-  const bool is_rd = static_cast<int>(c.warp & ~3u) == plan.cr_warp[0];
   BwdState st{0, 0};
   uint32_t gbase = 0, icount = 0;
   for (int work = blockIdx.x; work < c.num_work; work += gridDim.x, ++icount) {
@@ -474,8 +521,8 @@ __device__ __forceinline__ void bwd_run(const BwdCtx& c, const TwfaDevicePlan& p
         }
         __syncwarp();
       }
-    } else {
-      if (is_rd) kv_epilogue(c, a, t);
+    } else if constexpr (kRole == kReduce) {
+      kv_epilogue(c, a, t);
     }
     gbase += static_cast<uint32_t>(t.N);
   }
@@ -517,6 +564,7 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
     mbar_init(&bar.dq_full, 1);
     mbar_init(&bar.p_full, 4);
     mbar_init(&bar.ds_full, 4);
+    mbar_init(&bar.p_read, 4);
     mbar_init(&bar.q_free, 4);
     mbar_init(&bar.ds_free, 1);
     mbar_init(&bar.acc_full, 1);
@@ -536,15 +584,20 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
   if (bar.tmem_base != 0) __trap();  // one CTA per SM owns all 512 columns from 0
   c.pol = policy_evict_last();
   const int wg = static_cast<int>(c.warp >> 2);
-  const bool heavy = (plan.heavy_wg_mask >> wg) & 1;
-  const bool rd = wg * 4 == plan.cr_warp[0];
-  // registers: the EXB/DS warpgroup carries the 128-float P^T row, the RD
-  // warpgroup a 128-float dQ row; the TMA / MMA warps need few
-  if (heavy) {
+  const bool exb = wg * 4 == plan.sm_warp[0], ds = wg * 4 == plan.sm_warp[1], rd = wg * 4 == plan.cr_warp[0];
+  // registers: EXB carries the 128-float S^T / P^T row, DS the packed P^T
+  // (64) and a dP^T chunk, RD half a dQ row; the TMA / MMA warps need few
+  if (exb && ds) {
     setmaxnreg_inc<200>();
-    bwd_run<kHeavyRole>(c, plan, a);
-  } else if (rd) {
+    bwd_run<kExbDs>(c, plan, a);
+  } else if (exb) {
     setmaxnreg_inc<168>();
+    bwd_run<kExb>(c, plan, a);
+  } else if (ds) {
+    setmaxnreg_inc<144>();
+    bwd_run<kDs>(c, plan, a);
+  } else if (rd) {
+    setmaxnreg_dec<128>();
     bwd_run<kReduce>(c, plan, a);
   } else {
     setmaxnreg_dec<64>();

@@ -229,26 +229,38 @@ void derive_bwd(LoweredSchedule& s, NodeId&& node_id, DepthOf&& depth_of, Prefet
   for (const TwfaPlanOp* o : {&exb, &ds, &rd})
     if (o->warp_count != 4 || o->warp_start % 4 != 0)
       throw DomainError("EXB, DS and RD are row-wise over 128 TMEM lanes: they need a warpgroup");
-  if (exb.warp_start != ds.warp_start) throw DomainError("EXB and DS must share a warpgroup (P stays in registers)");
   for (int w : {p.load_warp, p.mma_warp})
-    for (const TwfaPlanOp* o : {&exb, &rd})
+    for (const TwfaPlanOp* o : {&exb, &ds, &rd})
       if (w >= o->warp_start && w < o->warp_start + 4)
-        throw DomainError("the TMA / MMA warp cannot be inside the EXB or RD warpgroup");
-  // P^T (128 fp32 registers) lives from EXB to DS: DS must be the next op of
-  // every warp of the group, in the same iteration
-  const int exi = node_id("EXB"), dsi = node_id("DS");
-  for (int w = exb.warp_start; w < exb.warp_start + 4; ++w) {
-    const std::vector<int>& prog = s.warp_prog[static_cast<size_t>(w)];
-    auto it = std::find(prog.begin(), prog.end(), exi);
-    if (it == prog.end() || it + 1 == prog.end() || *(it + 1) != dsi ||
-        s.stage[static_cast<size_t>(exi)] != s.stage[static_cast<size_t>(dsi)])
-      throw DomainError("DS must directly follow EXB on its warpgroup (P is carried in registers)");
+        throw DomainError("the TMA / MMA warp cannot be inside the EXB, DS or RD warpgroup");
+  if (rd.warp_start == exb.warp_start || rd.warp_start == ds.warp_start)
+    throw DomainError("RD needs its own warpgroup (register budget of the dQ staging)");
+  const int exi = node_id("EXB"), dsi = node_id("DS"), sti = node_id("ST");
+  if (exb.warp_start == ds.warp_start) {
+    // one warpgroup: P^T (128 fp32 registers) lives from EXB to DS, so DS
+    // must be the next op of every warp of the group, in the same iteration
+    for (int w = exb.warp_start; w < exb.warp_start + 4; ++w) {
+      const std::vector<int>& prog = s.warp_prog[static_cast<size_t>(w)];
+      auto it = std::find(prog.begin(), prog.end(), exi);
+      if (it == prog.end() || it + 1 == prog.end() || *(it + 1) != dsi ||
+          s.stage[static_cast<size_t>(exi)] != s.stage[static_cast<size_t>(dsi)])
+        throw DomainError("DS must directly follow EXB on a shared warpgroup (P is carried in registers)");
+    }
+    p.ops[exi].flags |= TWFA_OPF_FUSE_NEXT;
+    p.ops[dsi].flags |= TWFA_OPF_FUSED;
+  } else {
+    // two warpgroups: DS reads P^T (bf16) back from the S^T columns, which
+    // S^T(i+1) overwrites; the graph must order that read (DS -> ST, delta >= 1)
+    bool ordered = false;
+    for (const LEdge& e : s.edges)
+      ordered = ordered || (e.src == dsi && e.dst == sti && e.delta >= 1);
+    if (!ordered) throw DomainError("EXB and DS on different warpgroups need a DS -> ST (delta 1) edge");
+    p.ops[sti].flags |= TWFA_OPF_WAIT_PREAD;
   }
-  p.ops[exi].flags |= TWFA_OPF_FUSE_NEXT;
-  p.ops[dsi].flags |= TWFA_OPF_FUSED;
   p.sm_warp[0] = exb.warp_start;
+  p.sm_warp[1] = ds.warp_start;
   p.cr_warp[0] = rd.warp_start;  // RD warpgroup (also writes dK, dV)
-  p.heavy_wg_mask = 1 << (exb.warp_start / 4);
+  p.heavy_wg_mask = (1 << (exb.warp_start / 4)) | (1 << (ds.warp_start / 4));
   // the later tensor-core reader of Q_i (ST, DK) and of dO_i (DP, DV)
   // releases the ring slot with its commit
   auto later = [&](const char* a, const char* b) {
@@ -306,37 +318,43 @@ void derive(LoweredSchedule& s) {
   // realizes the same modulo schedule, and the ring prefetch (prefetch_of)
   // already serves its consumers from an earlier trip.
   auto streamed = [&](int v) { return s.nodes[static_cast<size_t>(v)].cycles == 0; };
+  // streamed loads moved to the end of their trip program (see below)
+  std::vector<bool> late(n, false);
   auto order_key = [&](int v) {
-    return std::make_tuple(s.slot[static_cast<size_t>(v)], streamed(v) ? 1 : 0, v);
+    const bool l = late[static_cast<size_t>(v)];
+    return std::make_tuple(l ? s.ii : s.slot[static_cast<size_t>(v)], streamed(v) ? 1 : 0, v);
   };
-  s.warp_prog.assign(static_cast<size_t>(s.num_warps), {});
-  for (int w = 0; w < s.num_warps; ++w) {
-    std::vector<int>& prog = s.warp_prog[static_cast<size_t>(w)];
-    for (size_t v = 0; v < n; ++v)
-      if (p.ops[v].warp_start <= w && w < p.ops[v].warp_start + p.ops[v].warp_count)
-        prog.push_back(static_cast<int>(v));
-    std::stable_sort(prog.begin(), prog.end(), [&](int x, int y) { return order_key(x) < order_key(y); });
-    p.prog_len[w] = static_cast<uint8_t>(prog.size());
-    for (size_t i = 0; i < prog.size(); ++i) {
-      p.prog[w][i] = static_cast<uint8_t>(prog[i]);
-      if (w == p.ops[prog[i]].warp_start) p.ops[prog[i]].order = static_cast<uint8_t>(i);
+  auto build_programs = [&] {
+    s.warp_prog.assign(static_cast<size_t>(s.num_warps), {});
+    for (int w = 0; w < s.num_warps; ++w) {
+      std::vector<int>& prog = s.warp_prog[static_cast<size_t>(w)];
+      for (size_t v = 0; v < n; ++v)
+        if (p.ops[v].warp_start <= w && w < p.ops[v].warp_start + p.ops[v].warp_count)
+          prog.push_back(static_cast<int>(v));
+      std::stable_sort(prog.begin(), prog.end(), [&](int x, int y) { return order_key(x) < order_key(y); });
+      p.prog_len[w] = static_cast<uint8_t>(prog.size());
+      for (size_t i = 0; i < prog.size(); ++i) {
+        p.prog[w][i] = static_cast<uint8_t>(prog[i]);
+        if (w == p.ops[prog[i]].warp_start) p.ops[prog[i]].order = static_cast<uint8_t>(i);
+      }
     }
-  }
-  // Realizability of the order: a consumer that issues in the same cycle as
-  // its producer on a shared warp must come after it in the trip program,
-  // otherwise the warp would wait on itself.
-  for (const LEdge& e : s.edges) {
-    if (e.src == e.dst) continue;
-    const TwfaPlanOp& u = p.ops[e.src];
-    const TwfaPlanOp& v = p.ops[e.dst];
-    const int64_t gap = s.m[static_cast<size_t>(e.dst)] + e.delta * s.ii - s.m[static_cast<size_t>(e.src)];
-    if (gap < e.d)
-      throw DomainError("schedule violates dependence " + s.nodes[e.src].id + " -> " + s.nodes[e.dst].id);
-    const bool share = u.warp_start < v.warp_start + v.warp_count && v.warp_start < u.warp_start + u.warp_count;
-    if (gap == 0 && share && !streamed(e.src) && order_key(e.dst) < order_key(e.src))
-      throw DomainError("same-cycle dependence " + s.nodes[e.src].id + " -> " + s.nodes[e.dst].id +
-                        " is ordered consumer-first on a shared warp");
-  }
+    // Realizability of the order: a consumer that issues in the same cycle as
+    // its producer on a shared warp must come after it in the trip program,
+    // otherwise the warp would wait on itself.
+    for (const LEdge& e : s.edges) {
+      if (e.src == e.dst) continue;
+      const TwfaPlanOp& u = p.ops[e.src];
+      const TwfaPlanOp& v = p.ops[e.dst];
+      const int64_t gap = s.m[static_cast<size_t>(e.dst)] + e.delta * s.ii - s.m[static_cast<size_t>(e.src)];
+      if (gap < e.d)
+        throw DomainError("schedule violates dependence " + s.nodes[e.src].id + " -> " + s.nodes[e.dst].id);
+      const bool share = u.warp_start < v.warp_start + v.warp_count && v.warp_start < u.warp_start + u.warp_count;
+      if (gap == 0 && share && !streamed(e.src) && order_key(e.dst) < order_key(e.src))
+        throw DomainError("same-cycle dependence " + s.nodes[e.src].id + " -> " + s.nodes[e.dst].id +
+                          " is ordered consumer-first on a shared warp");
+    }
+  };
+  build_programs();
 
   auto depth_of = [&](const char* id) -> int32_t {
     auto it = s.streaming_depths.find(id);
@@ -373,6 +391,39 @@ void derive(LoweredSchedule& s) {
                         " cannot cover a consumer on its own warp");
     return static_cast<int32_t>(pf);
   };
+
+  // A streamed load whose ring slot is released by a consumer later in its
+  // own warp's trip program cannot run ahead from its slot position
+  // (prefetch 0): the iteration it loads is then consumed in the same trip,
+  // and a consumer ordered before it would wait on it. Such a load issues at
+  // the end of its trip program instead -- after every same-warp consumer --
+  // which lets it run one iteration ahead. Zero-cycle streamed ops occupy no
+  // part of the cycle, so the modulo schedule is unchanged.
+  bool moved = false;
+  for (size_t v = 0; v < n; ++v) {
+    if (!streamed(static_cast<int>(v))) continue;
+    auto it = s.streaming_depths.find(s.nodes[v].id);
+    if (it == s.streaming_depths.end() || it->second < 2) continue;
+    if (prefetch_of(static_cast<int>(v), static_cast<int32_t>(it->second)) > 0) continue;
+    late[v] = true;
+    moved = true;
+  }
+  if (moved) build_programs();
+  for (size_t v = 0; v < n; ++v) {  // no consumer may wait on a later load of its own warp
+    if (!streamed(static_cast<int>(v))) continue;
+    auto it = s.streaming_depths.find(s.nodes[v].id);
+    if (it == s.streaming_depths.end()) continue;
+    if (prefetch_of(static_cast<int>(v), static_cast<int32_t>(it->second)) > 0) continue;
+    for (const LEdge& e : s.edges) {
+      if (static_cast<size_t>(e.src) != v) continue;
+      const TwfaPlanOp &L = p.ops[v], &C = p.ops[e.dst];
+      const bool share = L.warp_start < C.warp_start + C.warp_count && C.warp_start < L.warp_start + L.warp_count;
+      const int64_t lag = s.stage[static_cast<size_t>(e.dst)] + e.delta - s.stage[v];
+      if (share && lag == 0 && order_key(e.dst) < order_key(static_cast<int>(v)))
+        throw DomainError("streamed load " + s.nodes[v].id + " cannot run ahead of " + s.nodes[e.dst].id +
+                          " on their shared warp");
+    }
+  }
 
   const bool is_fa = (kinds.count(TWFA_OP_S) || (kinds.count(TWFA_OP_SA) && kinds.count(TWFA_OP_SB))) &&
                      kinds.count(TWFA_OP_PV);
@@ -584,7 +635,8 @@ std::string describe(const LoweredSchedule& s) {
     rings["dO"] = p.v_depth;
     j["prefetch"] = {{"LDQ", p.k_prefetch}, {"LDO", p.v_prefetch}};
     j["mma_warp"] = p.mma_warp;
-    j["warpgroups"] = {{"exp_ds", p.sm_warp[0]}, {"dq_reduce", p.cr_warp[0]}};
+    j["warpgroups"] = {{"exp", p.sm_warp[0]}, {"ds", p.sm_warp[1]}, {"dq_reduce", p.cr_warp[0]}};
+    j["p_transfer"] = p.sm_warp[0] == p.sm_warp[1] ? "registers (EXB and DS fused)" : "tensor memory (bf16 P^T re-read)";
     json rel = json::array();
     for (int v = 0; v < p.num_nodes; ++v)
       if (p.ops[v].flags & TWFA_OPF_RELEASE) rel.push_back(s.nodes[static_cast<size_t>(v)].id);

@@ -76,6 +76,9 @@ struct alignas(16) TwfaPlanOp {  // 16 bytes: one vector load on the device
 // FA backward: the last tensor-core reader of its streamed ring slot in the
 // iteration (releases Q_i / dO_i with its commit).
 #define TWFA_OPF_RELEASE 8
+// FA backward ST: DS runs on another warpgroup and reads P^T(i-1) back from
+// the S^T columns; S^T(i) waits for that read (edge DS -> ST, delta 1).
+#define TWFA_OPF_WAIT_PREAD 16
 
 // Kind of the workload the plan drives.
 enum TwfaPlanFamily : int32_t { TWFA_FAMILY_FA_FWD = 1, TWFA_FAMILY_GEMM = 2, TWFA_FAMILY_FA_BWD = 3 };

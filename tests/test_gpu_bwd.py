@@ -72,3 +72,13 @@ def test_rejects_forward_plan_and_bad_args(twfa, plans):
         twfa.fa_bwd(fp, x, x, x, x, x, lse)
     with pytest.raises(ValueError, match="lse"):
         twfa.fa_bwd(bp, x, x, x, x, x, lse[..., :64])
+
+
+@pytest.mark.parametrize("S,causal", [(256, False), (384, True), (200, False)])
+def test_split_schedule_matches_oracle(twfa, plans, S, causal):
+    # fa_bwd_split: the solver puts EXB and DS on different warpgroups and
+    # pipelines across iterations; DS reads P^T (bf16) back from tensor
+    # memory and S^T(i+1) waits for that read
+    split = twfa.Plan(*twfa.load_schedule("fa_bwd_split"))
+    assert split.describe()["p_transfer"].startswith("tensor memory")
+    _check(twfa, (plans[0], split), 1, 2, S, causal, 12)

@@ -110,7 +110,7 @@ def test_fa_ring_depth_follows_solution(twfa):
     (lambda s: s["A"].update(MX0=3), "aligned warp range"),
     (lambda s: s["A"].update(EX0=8, MX0=4), "share a warpgroup"),
     (lambda s: s["A"].update(S0=16), "aligned warp range"),
-    (lambda s: s.update(streaming_depths={"LDK": 1, "LDV": 1}), "shallower than its consumer lag"),
+    (lambda s: s.update(streaming_depths={"LDK": 1, "LDV": 1}), "shallower than its consumer lag|cannot run ahead"),
 ])
 def test_bad_or_unrealizable_solutions_are_rejected(twfa, mutate, msg):
     prob, sol = twfa.load_schedule("fa_fwd")
@@ -167,19 +167,20 @@ def test_fa_bwd_plan_roles_follow_the_solver(twfa):
     s = json.loads(sol)
     d = twfa.Plan(prob, sol).describe()
     assert d["family"] == "fa_bwd"
-    assert d["warpgroups"] == {"exp_ds": s["A"]["EXB"], "dq_reduce": s["A"]["RD"]}
+    assert d["warpgroups"] == {"exp": s["A"]["EXB"], "ds": s["A"]["DS"], "dq_reduce": s["A"]["RD"]}
+    assert d["p_transfer"].startswith("registers" if s["A"]["EXB"] == s["A"]["DS"] else "tensor memory")
     assert d["mma_warp"] == s["A"]["ST"] and d["load_warp"] == s["A"]["LDQ"]
     mma = d["warp_programs"][str(d["mma_warp"])]
     tc = [v for v in mma if v in ("ST", "DP", "DV", "DK", "DQ")]
-    # issue order = slot order of the solution (all stage 0 here)
-    assert tc == sorted(tc, key=lambda v: s["M"][v])
+    # issue order = slot order (M mod I) of the solution
+    assert tc == sorted(tc, key=lambda v: s["M"][v] % s["I"])
     # the later reader of Q_i (ST, DK) / dO_i (DP, DV) releases the ring slot
     later = lambda a, b: a if s["M"][a] > s["M"][b] else b  # noqa: E731
     assert sorted(d["ring_release"]) == sorted([later("ST", "DK"), later("DP", "DV")])
 
 
 @pytest.mark.parametrize("mutate,msg", [
-    (lambda s: s["A"].update(DS=4), "share a warpgroup"),
+    (lambda s: s["A"].update(DS=s["A"]["RD"]), "own warpgroup"),
     (lambda s: s["A"].update(DQ=14), "issue from one warp"),
     (lambda s: s["A"].update(RD=12), "cannot be inside"),
     (lambda s: s["M"].update(DS=s["M"]["EXB"]), "violates dependence"),

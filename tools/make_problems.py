@@ -169,7 +169,7 @@ def fa_forward_problem(tc_variable_latency=False, calibrated=False, s_ring=1, sp
     return {"machine": machine, "graph": {"nodes": nodes, "edges": edges}}
 
 
-def fa_backward_problem(calibrated=False):
+def fa_backward_problem(calibrated=False, fused=False, exb_spill=16):
     """FA-backward loop body on sm_100a (the paper's second workload,
     PAPER.md:1073-1148; the single-pass algorithm of FA3): one CTA owns a
     128-key K/V tile (K, V resident in shared memory, dK and dV accumulated
@@ -216,9 +216,20 @@ def fa_backward_problem(calibrated=False):
     nodes = [node("LDQ", "TMA", 2, variable_latency=True), node("LDO", "TMA", 2, variable_latency=True)]
     for v in ("ST", "DP"):
         nodes.append(node(v, "TC", g, footprint={"tmem": 128}, variable_latency=True))
+    if fused:
+        # EXB and DS as one warpgroup op (P^T is carried in registers from the
+        # exponentials into dS^T, so they cannot sit on different warps). Its
+        # consumers read through memory: P^T (TMEM) after the exponential part
+        # (edge delay ex < the op's duration), dS^T (TMEM + smem) at the end,
+        # each behind an mbarrier handoff (spill cost 1 = 256 clk). dP^T is
+        # only needed by the DS part: DP -> EXDS with delay 0 is conservative.
+        nodes.append(node("EXDS", "MUFU", ex + dsc, regs=128, spill_cost=1, warps_required=4))
+    else:
+        nodes += [
+            node("EXB", "MUFU", ex, regs=128, spill_cost=exb_spill, warps_required=4),
+            node("DS", "FMA", dsc, regs=64, warps_required=4),
+        ]
     nodes += [
-        node("EXB", "MUFU", ex, regs=128, spill_cost=16, warps_required=4),
-        node("DS", "FMA", dsc, regs=64, warps_required=4),
         node("DV", "TC", g, variable_latency=True),
         node("DK", "TC", g, variable_latency=True),
         node("DQ", "TC", g, variable_latency=True),
@@ -227,17 +238,33 @@ def fa_backward_problem(calibrated=False):
     edges = [
         edge("LDQ", "ST", 0, blocking=True), edge("LDQ", "DK", 0, blocking=True),
         edge("LDO", "DP", 0, blocking=True), edge("LDO", "DV", 0, blocking=True),
-        edge("ST", "EXB", g, blocking=True),
-        edge("EXB", "DV", ex, blocking=True), edge("EXB", "DS", ex),
-        edge("DP", "DS", g, blocking=True),
-        edge("DS", "DK", dsc, blocking=True), edge("DS", "DQ", dsc, blocking=True),
+    ]
+    if fused:
+        edges += [
+            edge("ST", "EXDS", g, blocking=True), edge("DP", "EXDS", 0, blocking=True),
+            edge("EXDS", "DV", ex, blocking=True),
+            edge("EXDS", "DK", ex + dsc, blocking=True), edge("EXDS", "DQ", ex + dsc, blocking=True),
+            edge("RD", "EXDS", 2, delta=1, blocking=True), edge("EXDS", "EXDS", ex + dsc, delta=1),
+        ]
+    else:
+        edges += [
+            edge("ST", "EXB", g, blocking=True),
+            edge("EXB", "DV", ex, blocking=True), edge("EXB", "DS", ex),
+            edge("DP", "DS", g, blocking=True),
+            edge("DS", "DK", dsc, blocking=True), edge("DS", "DQ", dsc, blocking=True),
+            edge("RD", "DS", 2, delta=1, blocking=True),
+            edge("EXB", "EXB", ex, delta=1), edge("DS", "DS", dsc, delta=1),
+        ]
+        if exb_spill < ex:
+            # a DS on another warpgroup reads P^T back from tensor memory
+            # (bf16) at its start: S^T(i+1) may overwrite it only after that
+            edges.append(edge("DS", "ST", 1, delta=1, blocking=True))
+    edges += [
         edge("DQ", "RD", g, blocking=True),
         edge("DV", "ST", 0, delta=1),
         edge("DK", "DQ", 0),
         edge("RD", "DP", 2, delta=1, blocking=True),
-        edge("RD", "DS", 2, delta=1, blocking=True),
-        edge("DV", "DV", g, delta=1), edge("DK", "DK", g, delta=1),
-        edge("EXB", "EXB", ex, delta=1), edge("DS", "DS", dsc, delta=1), edge("RD", "RD", 2, delta=1),
+        edge("DV", "DV", g, delta=1), edge("DK", "DK", g, delta=1), edge("RD", "RD", 2, delta=1),
     ]
     for n in nodes:
         n["cycles"] *= T
@@ -342,8 +369,15 @@ def main():
         "fa_fwd_split": (fa_forward_problem(tc_variable_latency=True, calibrated=True, split_s=True), 2, 9),
         # double-buffered S (64-key K/V tiles): S_k(i+1) independent of PV_k(i)
         "fa_fwd_ring2": (fa_forward_problem(tc_variable_latency=True, s_ring=2), 4, None),
-        # FA backward (single pass, K/V-stationary), datasheet costs
+        # FA backward (single pass, K/V-stationary), datasheet costs; P^T
+        # carried in registers from EXB to DS (a large spill cost keeps them
+        # on one warpgroup)
         "fa_bwd": (fa_backward_problem(), 2, 11),  # {512, 1024, 4096} clk exactly (F = 0)
+        # EXB's consumers read P^T through tensor memory behind an mbarrier
+        # (spill cost 256 clk): the solver splits EXB and DS over two
+        # warpgroups and pipelines across iterations (I = 12 x 256 clk); the
+        # realized loop is slower (DESIGN 12: the dS / dQ-staging buffer)
+        "fa_bwd_split": (fa_backward_problem(exb_spill=1), 2, 13),
         "fa_bwd_cal": (fa_backward_problem(calibrated=True), 2, 14),
     }
     for name, (raw, depth, res) in probs.items():
