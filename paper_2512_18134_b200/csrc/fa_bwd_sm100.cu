@@ -57,6 +57,12 @@ constexpr uint32_t kSdHi = sdesc_hi(1024);
 #ifndef TWFA_BWD_WHATIF
 #define TWFA_BWD_WHATIF 0
 #endif
+// dQ reduction: 0 = staged through shared memory (the dS buffer) and
+// cp.reduce.async.bulk.tensor; 1 = red.global.add.v4.f32 straight from
+// registers (no staging buffer, so DS(i+1) does not wait for RD(i))
+#ifndef TWFA_BWD_RED
+#define TWFA_BWD_RED 0
+#endif
 // debug variant: CTA 0 prints per-op enter / exit clocks of iterations 20-21
 #ifndef TWFA_BWD_PROF
 #define TWFA_BWD_PROF 0
@@ -268,6 +274,31 @@ __device__ __forceinline__ void rd_op(const BwdCtx& c, const FaBwdArgs& a, const
   const uint32_t nb = 1 + (c.warp >> 2);  // named barrier of this warpgroup
   mbar_wait(&bar.dq_full, g & 1);
   tc_fence_after();
+  if (TWFA_BWD_RED) {
+    // the dS buffer is not used for staging: DS(i+1) may proceed
+    if (leader) mbar_arrive(&bar.ds_free);
+    float* dst = a.dq_acc + (static_cast<int64_t>(t.bh) * c.S + q0 + r) * 128;
+    const bool in = q0 + static_cast<int>(r) < c.S;
+#pragma unroll 1
+    for (int h = 0; h < 4; ++h) {
+      uint32_t v[32];
+      tmem_ld32(c.lane_off + kColP + h * 32, v);
+      tmem_ld_wait();
+      if (h == 3) {
+        tc_fence_before();
+        warp_arrive(&bar.q_free);
+      }
+      if (in) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + h * 32 + 4 * j),
+                       "f"(__uint_as_float(v[4 * j])), "f"(__uint_as_float(v[4 * j + 1])),
+                       "f"(__uint_as_float(v[4 * j + 2])), "f"(__uint_as_float(v[4 * j + 3]))
+                       : "memory");
+      }
+    }
+    return;
+  }
   // DQ_i has completed (dq_full): the dS buffer is free for staging. Two
   // halves of 64 columns (two 16 KiB boxes each) keep the row at 64 registers.
 #pragma unroll 1
