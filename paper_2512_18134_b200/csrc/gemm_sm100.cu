@@ -116,12 +116,15 @@ __global__ void __launch_bounds__(256, 1)
         mbar_wait(&bar->full[s], ph);
         tc_fence_after();
         const uint32_t sa = smem_u32(smem + s * kStageBytes);
-        const uint32_t sb = sa + kABytes;
+        // descriptors as base + 16-byte offset (the start-address field of
+        // one stage cannot carry; see sdesc_lo)
+        const uint32_t da = sdesc_lo(sa, 16), db = sdesc_lo(sa + kABytes, 16);
+        constexpr uint32_t hi = sdesc_hi(1024);
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < kBK / 16; ++kk)
-            mma_ss(tmem + acc * kBN, sdesc_sw128(sa + kk * 32, 16, 1024), sdesc_sw128(sb + kk * 32, 16, 1024),
-                   kIdesc, (kb | kk) != 0);
+            mma_ss(tmem + acc * kBN, sdesc_join(da + kk * 2, hi), sdesc_join(db + kk * 2, hi), kIdesc,
+                   (kb | kk) != 0);
           mma_commit(&bar->empty[s]);
         }
         __syncwarp();

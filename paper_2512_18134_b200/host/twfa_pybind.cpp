@@ -55,6 +55,20 @@ struct Plan {
                       S, 128, causal ? 1 : 0, scale, reinterpret_cast<void*>(stream)));
   }
 
+  // FA backward (plan from an FA-backward schedule); workspace of at least
+  // workspace_size(B, H, S) bytes, device pointers as integers
+  void fa_bwd(std::uintptr_t q, std::uintptr_t k, std::uintptr_t v, std::uintptr_t o, std::uintptr_t dout,
+              std::uintptr_t lse, std::uintptr_t dq, std::uintptr_t dk, std::uintptr_t dv, std::uintptr_t ws,
+              std::size_t ws_bytes, int B, int H, int S, bool causal, float scale, std::uintptr_t stream) const {
+    py::gil_scoped_release nogil;
+    check(twfa_fa_bwd(p, reinterpret_cast<const void*>(q), reinterpret_cast<const void*>(k),
+                      reinterpret_cast<const void*>(v), reinterpret_cast<const void*>(o),
+                      reinterpret_cast<const void*>(dout), reinterpret_cast<const float*>(lse),
+                      reinterpret_cast<void*>(dq), reinterpret_cast<void*>(dk), reinterpret_cast<void*>(dv),
+                      reinterpret_cast<void*>(ws), ws_bytes, B, H, S, 128, causal ? 1 : 0, scale,
+                      reinterpret_cast<void*>(stream)));
+  }
+
   void gemm(std::uintptr_t a, std::uintptr_t b, std::uintptr_t c, int M, int N, int K, std::uintptr_t stream) const {
     py::gil_scoped_release nogil;
     check(twfa_gemm(p, reinterpret_cast<const void*>(a), reinterpret_cast<const void*>(b), reinterpret_cast<void*>(c), M,
@@ -73,8 +87,20 @@ PYBIND11_MODULE(_twfa, m) {
       .def("fa_fwd", &Plan::fa_fwd, py::arg("q"), py::arg("k"), py::arg("v"), py::arg("o"), py::arg("lse") = 0,
            py::arg("B"), py::arg("H"), py::arg("S"), py::arg("causal") = false, py::arg("scale"),
            py::arg("stream") = 0)
+      .def("fa_bwd", &Plan::fa_bwd, py::arg("q"), py::arg("k"), py::arg("v"), py::arg("o"), py::arg("dout"),
+           py::arg("lse"), py::arg("dq"), py::arg("dk"), py::arg("dv"), py::arg("workspace"),
+           py::arg("workspace_bytes"), py::arg("B"), py::arg("H"), py::arg("S"), py::arg("causal") = false,
+           py::arg("scale"), py::arg("stream") = 0)
       .def("gemm", &Plan::gemm, py::arg("a"), py::arg("b"), py::arg("c"), py::arg("M"), py::arg("N"), py::arg("K"),
            py::arg("stream") = 0);
+  m.def(
+      "fa_bwd_workspace_size",
+      [](int B, int H, int S) {
+        size_t n = 0;
+        check(twfa_fa_bwd_workspace_size(B, H, S, 128, &n));
+        return n;
+      },
+      py::arg("B"), py::arg("H"), py::arg("S"));
   m.def(
       "describe",
       [](const std::string& problem, const std::string& solution) { return Plan(problem, solution).describe(); },

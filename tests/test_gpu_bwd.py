@@ -82,3 +82,31 @@ def test_split_schedule_matches_oracle(twfa, plans, S, causal):
     split = twfa.Plan(*twfa.load_schedule("fa_bwd_split"))
     assert split.describe()["p_transfer"].startswith("tensor memory")
     _check(twfa, (plans[0], split), 1, 2, S, causal, 12)
+
+
+def test_pybind_module_runs_the_same_backward(twfa, plans):
+    """_twfa.Plan.fa_bwd and the ctypes fa_bwd call the same C ABI: dK, dV
+    bit-identical (tensor-memory accumulation in a fixed order); dQ within
+    fp32 reduce-order noise (TMA reduce-add from several CTAs)."""
+    import os
+    import sys
+    from paper_2512_18134_b200 import _build
+    pkg = os.path.dirname(_build.LIB)
+    if pkg not in sys.path:
+        sys.path.insert(0, pkg)
+    import _twfa
+    fp, bp = plans
+    g = torch.Generator(device="cpu").manual_seed(21)
+    q, k, v, do = (torch.randn(1, 2, 384, 128, generator=g).to(torch.bfloat16).cuda() for _ in range(4))
+    o, lse = twfa.fa_fwd(fp, q, k, v, return_lse=True)
+    ref = twfa.fa_bwd(bp, q, k, v, o, do, lse)
+    p = _twfa.Plan(*twfa.load_schedule("fa_bwd"))
+    n = _twfa.fa_bwd_workspace_size(1, 2, 384)
+    ws = torch.empty(n, dtype=torch.uint8, device="cuda")
+    dq, dk, dv = (torch.empty_like(q) for _ in range(3))
+    p.fa_bwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), do.data_ptr(), lse.data_ptr(), dq.data_ptr(),
+             dk.data_ptr(), dv.data_ptr(), ws.data_ptr(), n, B=1, H=2, S=384, scale=128 ** -0.5,
+             stream=torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert torch.equal(dk, ref[1]) and torch.equal(dv, ref[2])
+    assert (dq.float() - ref[0].float()).abs().max().item() <= 1e-2 * ref[0].float().abs().max().item()
