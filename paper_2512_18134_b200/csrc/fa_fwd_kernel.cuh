@@ -312,6 +312,7 @@ struct FaCtx {
   uint32_t tmem;
   uint32_t warp, lane, quad, lane_off;
   int S, BH, q_blocks, num_work;
+  int q_warp;  // idle warp loading the Q tiles (-1: the load warp does)
   float scale_log2;
   uint64_t pol_q, pol_kv;
 };
@@ -354,8 +355,11 @@ __device__ __forceinline__ int valid_keys(const FaArgs& a, int row, int key0) {
 // running per-warp state
 struct WarpState {
   float m_run[TWFA_MAX_TILES], l_run[TWFA_MAX_TILES], alpha[TWFA_MAX_TILES];
-  int k_next, v_next;  // next K / V iteration to load (TMA warp)
+  int k_next, v_next;  // next K / V iteration to load (TMA warp); may run into the next tile
   uint32_t trace_n;
+  // TMA warp: the CTA's next work tile (its first K / V iterations are
+  // prefetched while this tile's pipeline drains)
+  int next_bh, next_N;  // next_N = 0: no next tile
 };
 
 // per-tile scalars indexed by a (possibly runtime) tile: selects keep the
@@ -400,10 +404,15 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
       // Warp-uniform address arithmetic (uniform datapath); one elected lane
       // issues the TMA.
       const bool is_k = op.kind == TWFA_OP_LDK;
-      const int target = min(N - 1, r - static_cast<int>(op.stage) + (is_k ? rg.kpf : rg.vpf));
+      const int pf = is_k ? rg.kpf : rg.vpf;
+      // iterations past N belong to the next work tile (global iteration
+      // numbering, and with it the ring slots and phases, runs on)
+      const int target = min(N - 1 + min(pf, st.next_N), r - static_cast<int>(op.stage) + pf);
       int& next = is_k ? st.k_next : st.v_next;
       while (next <= target) {
         const int lit = next++;
+        const bool cross = lit >= N;
+        const int key0 = (cross ? lit - N : lit) * KV, bh = cross ? st.next_bh : t.bh;
         uint32_t* tr = trace_begin<kTrace>(args, warp, st.trace_n, op.node, lit, r);
         const uint32_t g = t.gbase + static_cast<uint32_t>(lit);
         const int depth = is_k ? rg.kd : rg.vd;
@@ -416,8 +425,8 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
         trace_mark<kTrace>(tr, 4);
         if (elect_one()) {
           mbar_arrive_expect_tx(full, G::tile);
-          tma_load_3d(dst, map, full, 0, lit * KV, t.bh, c.pol_kv);
-          tma_load_3d(dst + G::half, map, full, 64, lit * KV, t.bh, c.pol_kv);
+          tma_load_3d(dst, map, full, 0, key0, bh, c.pol_kv);
+          tma_load_3d(dst + G::half, map, full, 64, key0, bh, c.pol_kv);
         }
         __syncwarp();
         trace_mark<kTrace>(tr, 5);
@@ -741,26 +750,50 @@ __device__ __forceinline__ void epilogue(const FaCtx& c, const WorkTile& t, int 
 }
 
 // Work-tile loop of one warp. `trip` runs the warp's trip program for trip r.
+template <int KV>
+__device__ __forceinline__ int work_of(const FaArgs& args, int round) {
+  // causal tiles are ordered longest first; alternating the direction of
+  // each round over the persistent CTAs ("snake") balances their totals
+  return round * static_cast<int>(gridDim.x) +
+         ((args.causal && (round & 1)) ? static_cast<int>(gridDim.x - 1 - blockIdx.x) : static_cast<int>(blockIdx.x));
+}
+
+// cross-tile prefetch (Q on an idle warp, the next tile's first K / V
+// iterations on the TMA warp); 0 = each tile starts from empty rings
+#ifndef TWFA_XTILE
+#define TWFA_XTILE 1
+#endif
 template <int KV, class Trip>
 __device__ __forceinline__ void work_loop(const FaCtx& c, const FaArgs& args, const Maps& tm, int tiles, int max_stage,
-                                          bool is_load_warp, const int* cr_warp, WarpState& st, Trip&& trip) {
+                                          bool is_load_warp, bool is_q_warp, const int* cr_warp, WarpState& st,
+                                          Trip&& trip) {
   uint32_t gbase = 0, tcount = 0;
+  st.k_next = st.v_next = 0;
   for (int round = 0;; ++round, ++tcount) {
-    // causal tiles are ordered longest first; alternating the direction of
-    // each round over the persistent CTAs ("snake") balances their totals
-    const int work = round * static_cast<int>(gridDim.x) +
-                     ((args.causal && (round & 1)) ? static_cast<int>(gridDim.x - 1 - blockIdx.x)
-                                                   : static_cast<int>(blockIdx.x));
+    const int work = work_of<KV>(args, round);
     if (work >= c.num_work) break;
     const WorkTile t = work_tile<KV>(c, args, work, gbase, tcount);
-    if (is_load_warp) load_q(c, t, tiles, tm);
+    if (TWFA_XTILE && is_q_warp) {  // Q of every tile, as soon as the previous tile's last S_k released it
+      load_q(c, t, tiles, tm);
+      gbase += static_cast<uint32_t>(t.N);
+      continue;
+    }
+    if (is_load_warp) {
+      if (!TWFA_XTILE || !(c.q_warp >= 0)) load_q(c, t, tiles, tm);
+      const int nwork = work_of<KV>(args, round + 1);
+      st.next_N = 0;
+      if (TWFA_XTILE && nwork < c.num_work) {
+        const WorkTile nt = work_tile<KV>(c, args, nwork, gbase + static_cast<uint32_t>(t.N), tcount + 1);
+        st.next_bh = nt.bh;
+        st.next_N = nt.N;
+      }
+    }
 #pragma unroll
     for (int k = 0; k < TWFA_MAX_TILES; ++k) {
       st.m_run[k] = -INFINITY;
       st.l_run[k] = 0.f;
       st.alpha[k] = 1.f;
     }
-    st.k_next = st.v_next = 0;
     // trip -1 only tops up the streamed-load rings (every timed op has
     // iteration < 0 there): a consumer that precedes its load in the trip
     // program finds iteration 0 already in flight
@@ -768,14 +801,17 @@ __device__ __forceinline__ void work_loop(const FaCtx& c, const FaArgs& args, co
     for (int r = -1; r < trips; ++r) trip(r, t);
     for (int k = 0; k < tiles; ++k)
       if (static_cast<int>(c.warp & ~3u) == cr_warp[k]) epilogue<KV>(c, t, k, args);
+    // iterations of the next tile already in flight keep their count
+    st.k_next = max(0, st.k_next - t.N);
+    st.v_next = max(0, st.v_next - t.N);
     gbase += static_cast<uint32_t>(t.N);
   }
 }
 
 // Shared prologue of both kernels: smem carve-up, barriers, TMEM allocation.
 template <int KV>
-__device__ __forceinline__ FaCtx fa_setup(int tiles, int kd, int vd, int load_warp, int split, const FaArgs& args,
-                                          const Maps& tm, uint8_t* smem_raw) {
+__device__ __forceinline__ FaCtx fa_setup(int tiles, int kd, int vd, int load_warp, int q_warp, int split,
+                                          const FaArgs& args, const Maps& tm, uint8_t* smem_raw) {
   // 1 KiB alignment of the tile buffers (SW128 atoms) by offset arithmetic on
   // the shared window address, keeping the pointer in the shared space
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -787,6 +823,7 @@ __device__ __forceinline__ FaCtx fa_setup(int tiles, int kd, int vd, int load_wa
   FaBarriers& bar = g_sh.bar;
   c.warp = warp_id();
   c.lane = lane_id();
+  c.q_warp = q_warp;
   if (threadIdx.x == 0) {
     for (int k = 0; k < tiles; ++k) {
       mbar_init(&bar.q_full[k], 1);
@@ -817,7 +854,7 @@ __device__ __forceinline__ FaCtx fa_setup(int tiles, int kd, int vd, int load_wa
     }
     fence_mbar_init();
   }
-  if (c.warp == static_cast<uint32_t>(load_warp) && c.lane == 0) {
+  if ((c.warp == static_cast<uint32_t>(load_warp) || static_cast<int>(c.warp) == q_warp) && c.lane == 0) {
     tma_prefetch_desc(tm.q);
     tma_prefetch_desc(tm.k);
     tma_prefetch_desc(tm.v);
@@ -869,7 +906,8 @@ __device__ __forceinline__ void run_interp(const FaCtx& c, const Maps& tm, const
   st.trace_n = 0;
   int plen = 0;
   while (plen < TWFA_MAX_NODES && g_sh.prog_len[c.warp] > plen) ++plen;
-  work_loop<KV>(c, args, tm, tiles, max_stage, !kHeavy && c.warp == static_cast<uint32_t>(load_warp), cr_warp, st,
+  work_loop<KV>(c, args, tm, tiles, max_stage, !kHeavy && c.warp == static_cast<uint32_t>(load_warp),
+                !kHeavy && static_cast<int>(c.warp) == c.q_warp, cr_warp, st,
                 [&](int r, const WorkTile& t) {
                   for (int j = 0; j < plen; ++j)
                     exec_op<KV, kHeavy, kTrace>(g_sh.prog[c.warp][j], r, c, t, st, rg, tm, args);
@@ -888,8 +926,8 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
     if (j < plan.prog_len[w]) g_sh.prog[w][j] = plan.ops[plan.prog[w][j]];
     if (j == 0) g_sh.prog_len[w] = plan.prog_len[w];
   }
-  const FaCtx c =
-      fa_setup<KV>(plan.num_tiles, plan.k_depth, plan.v_depth, plan.load_warp, plan.s_split, args, tm, smem_raw);
+  const FaCtx c = fa_setup<KV>(plan.num_tiles, plan.k_depth, plan.v_depth, plan.load_warp, plan.q_warp, plan.s_split,
+                               args, tm, smem_raw);
   const Rings rg{plan.k_depth,   plan.v_depth,    plan.k_prefetch, plan.v_prefetch,
                  plan.ex_ring_len, plan.ex_ring[0], plan.ex_ring[1], plan.s_split};
   const bool heavy = (plan.heavy_wg_mask >> (c.warp >> 2)) & 1;
@@ -954,7 +992,8 @@ __device__ __forceinline__ void run_spec(const FaCtx& c, const Maps& tm, const F
   constexpr int cr_warp[TWFA_MAX_TILES] = {TWFA_PLAN(I).cr_warp[0], TWFA_PLAN(I).cr_warp[1]};
   WarpState st;
   st.trace_n = 0;
-  work_loop<TWFA_PLAN(I).kv_tile>(c, args, tm, TWFA_PLAN(I).num_tiles, TWFA_PLAN(I).max_stage, kLoad, cr_warp, st,
+  work_loop<TWFA_PLAN(I).kv_tile>(c, args, tm, TWFA_PLAN(I).num_tiles, TWFA_PLAN(I).max_stage, kLoad,
+                                  !kHeavy && static_cast<int>(c.warp) == c.q_warp, cr_warp, st,
             [&](int r, const WorkTile& t) {
               spec_trip<I, W, kTrace>(r, c, t, st, tm, args, std::make_integer_sequence<int, plen>{});
             });
@@ -986,7 +1025,7 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
   constexpr int cr_warp[TWFA_MAX_TILES] = {TWFA_PLAN(I).cr_warp[0], TWFA_PLAN(I).cr_warp[1]};
   constexpr int KV = TWFA_PLAN(I).kv_tile;
   const FaCtx c = fa_setup<KV>(TWFA_PLAN(I).num_tiles, TWFA_PLAN(I).k_depth, TWFA_PLAN(I).v_depth,
-                               TWFA_PLAN(I).load_warp, TWFA_PLAN(I).s_split, args, tm, smem_raw);
+                               TWFA_PLAN(I).load_warp, TWFA_PLAN(I).q_warp, TWFA_PLAN(I).s_split, args, tm, smem_raw);
   // the register class is per warpgroup; the warp roles of each class are
   // dispatched inside its branch so ptxas allocates them under that budget
   constexpr int mask = TWFA_PLAN(I).heavy_wg_mask;
@@ -1010,6 +1049,7 @@ bool same_plan(const TwfaDevicePlan& a, const TwfaDevicePlan& b) {
   if (a.family != b.family || a.ii != b.ii || a.max_stage != b.max_stage || a.num_nodes != b.num_nodes ||
       a.num_warps != b.num_warps || a.num_tiles != b.num_tiles || a.k_depth != b.k_depth || a.v_depth != b.v_depth ||
       a.load_warp != b.load_warp || a.k_prefetch != b.k_prefetch || a.v_prefetch != b.v_prefetch ||
+      a.q_warp != b.q_warp ||
       a.heavy_wg_mask != b.heavy_wg_mask || a.s_depth != b.s_depth || a.kv_tile != b.kv_tile ||
       a.s_split != b.s_split)
     return false;

@@ -55,7 +55,7 @@ std::string emit(int id, const std::string& name, const twfa::LoweredSchedule& s
     << ", .kv_tile = " << p.kv_tile << ", .s_split = " << p.s_split
     << ", .cr_warp = " << ints(p.cr_warp, TWFA_MAX_TILES) << ", .sm_warp = " << ints(p.sm_warp, TWFA_MAX_TILES)
     << ", .mma_warp = " << p.mma_warp << ",\n";
-  o << "    .heavy_wg_mask = " << p.heavy_wg_mask << ", .ex_ring_len = " << p.ex_ring_len
+  o << "    .heavy_wg_mask = " << p.heavy_wg_mask << ", .q_warp = " << p.q_warp << ", .ex_ring_len = " << p.ex_ring_len
     << ", .ex_ring = " << bytes(p.ex_ring, TWFA_MAX_TILES) << ",\n";
   o << "    .ops = {\n";
   for (int v = 0; v < TWFA_MAX_NODES; ++v) {

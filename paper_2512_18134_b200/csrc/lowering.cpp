@@ -558,6 +558,17 @@ void derive(LoweredSchedule& s) {
   const int64_t smem = 32768LL * tiles + kv_bytes * (p.k_depth + p.v_depth) + 16384;
   if (p.k_depth > 4 || p.v_depth > 4) throw DomainError("ring depth above 4");
   if (smem > 216 * 1024) throw DomainError("ring depths exceed shared memory");
+  // Q tiles are loaded once per work tile, outside the loop body: an idle
+  // warp (no op of the schedule, outside the softmax and correction
+  // warpgroups) waits for the last S_k of a tile and loads the next tile's
+  // Q_k while the pipeline drains, so the load warp never blocks on it
+  p.q_warp = -1;
+  for (int w = 0; w < s.num_warps && p.q_warp < 0; ++w) {
+    if (p.prog_len[w] != 0 || w == p.load_warp || ((p.heavy_wg_mask >> (w / 4)) & 1)) continue;
+    bool cr = false;
+    for (int k = 0; k < tiles; ++k) cr = cr || (w / 4) * 4 == p.cr_warp[k];
+    if (!cr) p.q_warp = w;
+  }
   // one epilogue staging buffer: the sub-tiles' corrections (and with them
   // the epilogues) must run on one warpgroup
   for (int k = 1; k < tiles; ++k)
@@ -630,6 +641,7 @@ std::string describe(const LoweredSchedule& s) {
     json ring = json::array();
     for (int i = 0; i < p.ex_ring_len; ++i) ring.push_back("EX" + std::to_string(p.ex_ring[i]));
     j["mufu_order"] = ring;
+    j["q_warp"] = p.q_warp;
   } else if (p.family == TWFA_FAMILY_FA_BWD) {
     rings["Q"] = p.k_depth;
     rings["dO"] = p.v_depth;

@@ -114,6 +114,7 @@ struct TwfaDevicePlan {
   // modulo schedule orders them inside the trip; the kernel realizes that
   // reservation order with a token passed EX -> EX in slot order.
   int32_t heavy_wg_mask;            // bit w: warpgroup w runs MX/EX (gets the big register budget)
+  int32_t q_warp;                   // FA forward: idle warp that loads the Q tiles (-1: the load warp)
   int32_t ex_ring_len;              // 0 = no token (stages differ / single EX)
   uint8_t ex_ring[TWFA_MAX_TILES];  // tiles of the EX ops in slot order
   TwfaPlanOp ops[TWFA_MAX_NODES];
