@@ -269,8 +269,12 @@ __device__ __forceinline__ float mx_ex_spec(uint32_t (&s)[N], uint32_t taddr, fl
       const int e = c * kKeys + i;
       const float2 x = ffma2(make_float2(__uint_as_float(s[e]), __uint_as_float(s[e + 1])), sl2, nm2);
       float2 p;
-      p.x = fast_exp2(x.x);
-      p.y = fast_exp2(x.y);
+      if (((e >> 1) % kPolyEvery) == kPolyEvery - 1) {  // unmasked rows only: x is finite
+        p = poly_exp2x2(x);
+      } else {
+        p.x = fast_exp2(x.x);
+        p.y = fast_exp2(x.y);
+      }
       acc[(i >> 1) & 1] = fadd2(acc[(i >> 1) & 1], p);
       pk[i >> 1] = pack_bf16(p.x, p.y);
     }
