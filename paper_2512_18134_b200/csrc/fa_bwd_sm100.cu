@@ -155,17 +155,21 @@ __device__ __forceinline__ void exb_part(const BwdCtx& c, const FaBwdArgs& a, co
   const int qt = q0 + static_cast<int>(r);
   const float my_lse2 = qt < c.S ? a.lse[row0 + r] * kLog2e : INFINITY;  // rows past S: P = 0
   mbar_wait(&bar.s_full, g & 1);
-  stage_tile_vec(g_lse2, my_lse2, r, 1 + (c.warp >> 2));
   tc_fence_after();
-#pragma unroll
-  for (int cc = 0; cc < 4; ++cc)
-    tmem_ld32(c.lane_off + kColS + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(&p[cc * 32]));
+  // chunk 0 of the S^T row first; the rest streams in from tensor memory
+  // while chunk 0 is exponentiated (and while the LSE is staged)
+  tmem_ld32(c.lane_off + kColS, *reinterpret_cast<uint32_t(*)[32]>(&p[0]));
   tmem_ld_wait();
+#pragma unroll
+  for (int cc = 1; cc < 4; ++cc)
+    tmem_ld32(c.lane_off + kColS + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(&p[cc * 32]));
+  stage_tile_vec(g_lse2, my_lse2, r, 1 + (c.warp >> 2));
   // P^T[key][q] = exp2(S^T * scale*log2e - LSE_q * log2e)
   const float sl = a.scale_log2;
   const bool diag = a.causal && it == 0;  // the diagonal tile (q0 == kv0)
 #pragma unroll
   for (int j4 = 0; j4 < kT / 4; ++j4) {
+    if (j4 == 8) tmem_ld_wait();  // chunks 1..3
     const float4 l = reinterpret_cast<const float4*>(g_lse2)[j4];
     const float lv[4] = {l.x, l.y, l.z, l.w};
 #pragma unroll

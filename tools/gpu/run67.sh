@@ -1,0 +1,4 @@
+timeout 200 python -m pytest tests/test_gpu_bwd.py -x -q 2>&1 | tail -1
+timeout 120 python tools/gpu/bwd_time.py paper_2512_18134_b200/libtwfa.so
+timeout 120 python tools/gpu/bwd_time.py paper_2512_18134_b200/libtwfa.so
+CAUSAL=1 SHAPE=2,32,16384 timeout 120 python tools/gpu/bwd_time.py paper_2512_18134_b200/libtwfa.so
