@@ -66,6 +66,15 @@ def test_many_work_tiles_per_cta(twfa, plan):
     _check(twfa, plan, 2, 96, 512, True, 11)
 
 
+@pytest.mark.parametrize("S,causal", [(300, True), (700, False), (129, True)])
+def test_cross_tile_prefetch_with_ragged_tiles(twfa, plan, S, causal):
+    # many work tiles per CTA whose lengths differ (causal) and end in a
+    # ragged tail: the next tile's K/V iterations and Q are prefetched while
+    # the current one drains (idle-warp Q loader, continuous ring phases)
+    assert plan.describe()["q_warp"] >= 0
+    _check(twfa, plan, 3, 64, S, causal, 14)
+
+
 def test_softmax_scale(twfa, plan):
     _check(twfa, plan, 1, 2, 256, False, 12, scale=0.3)
 
