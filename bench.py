@@ -407,6 +407,21 @@ def run_ours(args, world, rank, local):
         "tensor_pipe": ncu_tensor_util(workload),
         "schedule_realized": realized_schedule(twfa, plan, q, k, v, causal),
     }
+    # whole work tile, untraced: the modulo schedule's makespan for N
+    # iterations, (N - 1) I + L units (the reference's simulate_pipeline,
+    # sim.cpp:371-466; tests/test_lowering.py checks the formula against it),
+    # against the timed launches at the sampled SM clock
+    sr = line["schedule_realized"]
+    n_iter = -(-S // 128)
+    tiles = B * H * (-(-S // 256))
+    grid = min(tiles, torch.cuda.get_device_properties(dev).multi_processor_count)
+    if not causal and sr.get("unit_clk"):
+        L = plan.describe()["L"]
+        sr["predicted_tile_clk"] = ((n_iter - 1) * sr["I"] + L) * sr["unit_clk"]
+        sm_mhz = (line["clocks"] or {}).get("sm_mhz") or 1965
+        sr["measured_tile_clk"] = per_launch_ms * 1e-3 * sm_mhz * 1e6 / (tiles / grid)
+        sr["tile"] = f"256 query rows x {n_iter} K/V iterations; {tiles / grid:.1f} tiles per CTA"
+
     if world == 1 and not args.no_cpu_baseline:
         tfl, secs, sample, threads = cpu_attention_sample()
         line["cpu_baseline"] = {"value": tfl, "unit": UNIT, "cores": threads, "kind": "port",

@@ -191,3 +191,12 @@ def test_fa_bwd_unrealizable_solutions_are_rejected(twfa, mutate, msg):
     mutate(s)
     with pytest.raises(ValueError, match=msg):
         twfa.Plan(prob, json.dumps(s))
+
+
+def test_tile_makespan_formula_matches_reference_simulate(twfa, ws):
+    # bench.py predicts a work tile's makespan as (N - 1) I + L units: the
+    # reference's pipelined replay (simulate_pipeline, sim.cpp:371-466)
+    prob, sol = twfa.load_schedule("fa_fwd")
+    s = json.loads(sol)
+    for n in (2, 3, 17, 64):  # the replay needs at least `copies` iterations
+        assert ws.simulate(prob, sol, n)["cycles"] == (n - 1) * s["I"] + s["L"]
