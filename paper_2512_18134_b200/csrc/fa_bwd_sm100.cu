@@ -126,8 +126,48 @@ __device__ __forceinline__ BwdItem bwd_item(const BwdCtx& c, const FaBwdArgs& a,
 }
 
 struct BwdState {
-  int q_next, o_next;  // next Q / dO iteration to load (TMA warp)
+  int q_next, o_next;      // next Q / dO iteration to load (TMA warp)
+  int q_target, o_target;  // loads the trip program has asked for so far
 };
+
+// Streamed Q / dO loads (LDQ / LDO). A load issues at its trip-program
+// position if its ring slot is already free; otherwise it is deferred
+// instead of stalling the warp (the TMA warp is also the MMA warp, and the
+// slot is released by an MMA commit that may still be in flight), retried
+// before every later op of the warp, and forced only when an op needs that
+// very iteration. Streamed loads are zero-cycle ops: issuing them anywhere
+// between their slot and their consumer realizes the same schedule.
+#ifndef TWFA_BWD_LAZY_LOADS
+#define TWFA_BWD_LAZY_LOADS 0  // measured: 712 vs 764 TFLOP/s (C3 shape), eager is faster
+#endif
+__device__ __forceinline__ void bwd_top_up(const BwdCtx& c, const FaBwdArgs& a, const BwdItem& t, BwdState& st,
+                                           const TwfaDevicePlan& plan, bool is_q, int upto, bool blocking) {
+  BwdBarriers& bar = g_bb;
+  int& next = is_q ? st.q_next : st.o_next;
+  const int depth = is_q ? plan.k_depth : plan.v_depth;
+  while (next <= upto) {
+    const int lit = next;
+    const uint32_t g = t.gbase + static_cast<uint32_t>(lit);
+    const uint32_t s = g % depth, ph = (g / depth) & 1;
+    uint64_t* empty = is_q ? &bar.q_empty[s] : &bar.o_empty[s];
+    if (blocking) {
+      mbar_wait(empty, ph ^ 1);
+    } else if (!__all_sync(0xffffffffu, mbar_try_wait(empty, ph ^ 1))) {
+      return;
+    }
+    ++next;
+    uint64_t* full = is_q ? &bar.q_full[s] : &bar.o_full[s];
+    if (elect_one()) {
+      uint8_t* dst = (is_q ? c.q : c.o) + s * kTile;
+      const CUtensorMap* map = is_q ? &a.tm_q : &a.tm_do;
+      const int row = (t.q_first + lit) * kT;
+      mbar_arrive_expect_tx(full, kTile);
+      tma_load_3d(dst, map, full, 0, row, t.bh, c.pol);
+      tma_load_3d(dst + kHalf, map, full, 64, row, t.bh, c.pol);
+    }
+    __syncwarp();
+  }
+}
 
 __device__ __forceinline__ uint32_t sd_lo(const void* p, uint32_t lbo) { return sdesc_lo(smem_u32(p), lbo); }
 
@@ -390,26 +430,16 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
     if constexpr (kRole == kLight) {
       const bool is_q = op.kind == TWFA_OP_LDQ;
       const int target = min(t.N - 1, r - static_cast<int>(op.stage) + (is_q ? plan.k_prefetch : plan.v_prefetch));
-      int& next = is_q ? st.q_next : st.o_next;
-      const int depth = is_q ? plan.k_depth : plan.v_depth;
-      while (next <= target) {
-        const int lit = next++;
-        const uint32_t g = t.gbase + static_cast<uint32_t>(lit);
-        const uint32_t s = g % depth, ph = (g / depth) & 1;
-        uint64_t* full = is_q ? &bar.q_full[s] : &bar.o_full[s];
-        mbar_wait(is_q ? &bar.q_empty[s] : &bar.o_empty[s], ph ^ 1);
-        if (elect_one()) {
-          uint8_t* dst = (is_q ? c.q : c.o) + s * kTile;
-          const CUtensorMap* map = is_q ? &a.tm_q : &a.tm_do;
-          const int row = (t.q_first + lit) * kT;
-          mbar_arrive_expect_tx(full, kTile);
-          tma_load_3d(dst, map, full, 0, row, t.bh, c.pol);
-          tma_load_3d(dst + kHalf, map, full, 64, row, t.bh, c.pol);
-        }
-        __syncwarp();
-      }
+      (is_q ? st.q_target : st.o_target) = target;
+      bwd_top_up(c, a, t, st, plan, is_q, target, !TWFA_BWD_LAZY_LOADS);
     }
     return;
+  }
+  if constexpr (kRole == kLight) {
+    if (TWFA_BWD_LAZY_LOADS) {  // deferred loads: retry without blocking
+      bwd_top_up(c, a, t, st, plan, true, st.q_target, false);
+      bwd_top_up(c, a, t, st, plan, false, st.o_target, false);
+    }
   }
   const int it = r - static_cast<int>(op.stage);
   if (it < 0 || it >= t.N) return;
@@ -444,6 +474,10 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
   }
   if constexpr (kRole != kLight) return;
   // tensor-core ops: warp-uniform descriptors, one elected lane issues
+  if (TWFA_BWD_LAZY_LOADS) {  // a deferred load this op needs is forced now
+    if (op.kind == TWFA_OP_ST || op.kind == TWFA_OP_DK) bwd_top_up(c, a, t, st, plan, true, it, true);
+    if (op.kind == TWFA_OP_DP || op.kind == TWFA_OP_DV) bwd_top_up(c, a, t, st, plan, false, it, true);
+  }
   const uint32_t qs = g % plan.k_depth, os = g % plan.v_depth;
   const bool release = op.flags & TWFA_OPF_RELEASE;
   if (op.kind == TWFA_OP_ST) {
@@ -527,7 +561,7 @@ __device__ __forceinline__ void bwd_run(const BwdCtx& c, const TwfaDevicePlan& p
   const int plen = plan.prog_len[c.warp];
   const bool is_load = c.warp == static_cast<uint32_t>(plan.load_warp);
   const bool is_mma = c.warp == static_cast<uint32_t>(plan.mma_warp);
-  BwdState st{0, 0};
+  BwdState st{0, 0, -1, -1};
   uint32_t gbase = 0, icount = 0;
   for (int work = blockIdx.x; work < c.num_work; work += gridDim.x, ++icount) {
     const BwdItem t = bwd_item(c, a, work, gbase, icount);
@@ -545,6 +579,7 @@ __device__ __forceinline__ void bwd_run(const BwdCtx& c, const TwfaDevicePlan& p
       }
     }
     st.q_next = st.o_next = 0;
+    st.q_target = st.o_target = -1;
     const int trips = t.N + plan.max_stage;
     for (int rr = -1; rr < trips; ++rr)
       for (int j = 0; j < plen; ++j) bwd_exec<kRole>(plan.ops[plan.prog[c.warp][j]], rr, c, t, st, plan, a);
