@@ -86,7 +86,8 @@ __shared__ BwdBarriers g_bb;
 __shared__ float g_lse2[kT], g_dvec[kT];
 #if TWFA_BWD_PROF
 __shared__ int g_prof_n;
-__shared__ long long g_prof[24][3];
+__shared__ long long g_prof[24][4];
+__device__ long long g_prof_ready;  // per-op "inputs ready" clock (MMA warp, debug variant)
 #endif
 
 struct BwdCtx {
@@ -451,7 +452,12 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
     __device__ ~Out() {
       if (on) {
         const int n = atomicAdd(&g_prof_n, 1);
-        if (n < 24) { g_prof[n][0] = (int)(threadIdx.x / 32) * 1000 + kind * 10 + (it - 20); g_prof[n][1] = t0; g_prof[n][2] = clock64(); }
+        if (n < 24) {
+          g_prof[n][0] = (int)(threadIdx.x / 32) * 1000 + kind * 10 + (it - 20);
+          g_prof[n][1] = t0;
+          g_prof[n][2] = clock64();
+          g_prof[n][3] = g_prof_ready;
+        }
       }
     }
   } out_{prof, op.kind, it, clock64()};
@@ -489,6 +495,9 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
     else
       mbar_wait(&bar.q_full[qs], (g / plan.k_depth) & 1);
     tc_fence_after();
+#if TWFA_BWD_PROF
+    g_prof_ready = clock64();
+#endif
     const uint32_t ad = sd_lo(c.k, 16), bd = sd_lo(c.q + qs * kTile, 16);
     if (elect_one()) {
 #pragma unroll
@@ -507,6 +516,9 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
     else
       mbar_wait(&bar.o_full[os], (g / plan.v_depth) & 1);
     tc_fence_after();
+#if TWFA_BWD_PROF
+    g_prof_ready = clock64();
+#endif
     const uint32_t ad = sd_lo(c.v, 16), bd = sd_lo(c.o + os * kTile, 16);
     if (elect_one()) {
 #pragma unroll
@@ -528,6 +540,9 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
     else
       mbar_wait_all(&bar.ds_full, g & 1, &bar.q_full[qs], (g / plan.k_depth) & 1);
     tc_fence_after();
+#if TWFA_BWD_PROF
+    g_prof_ready = clock64();
+#endif
     // B = dO_i / Q_i as [K = query][N = d], MN-major
     const uint32_t bd = dv ? sd_lo(c.o + os * kTile, kHalf) : sd_lo(c.q + qs * kTile, kHalf);
     const uint32_t a_t = dv ? kColS : kColP, d_t = dv ? kColDV : kColDK;
@@ -541,6 +556,9 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
   } else if (op.kind == TWFA_OP_DQ) {
     mbar_wait(&bar.ds_full, g & 1);
     tc_fence_after();
+#if TWFA_BWD_PROF
+    g_prof_ready = clock64();
+#endif
     // A = dS as [M = query][K = key], MN-major (row = key in smem);
     // B = K as [K = key][N = d], MN-major
     const uint32_t ad = sd_lo(c.ds, kHalf), bd = sd_lo(c.k, kHalf);
@@ -678,10 +696,14 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
   __syncthreads();
 #if TWFA_BWD_PROF
   if (blockIdx.x == 0 && threadIdx.x == 0)
-    for (int i = 0; i < g_prof_n && i < 24; ++i) printf("PROF %lld %lld %lld\n", g_prof[i][0], g_prof[i][1], g_prof[i][2]);
+    for (int i = 0; i < g_prof_n && i < 24; ++i)
+      printf("PROF %lld %lld %lld %lld\n", g_prof[i][0], g_prof[i][1], g_prof[i][2], g_prof[i][3]);
 #endif
   if (c.warp == 0) {
     tc_fence_after();
+#if TWFA_BWD_PROF
+    g_prof_ready = clock64();
+#endif
     tmem_dealloc<512>(0);
   }
 }
