@@ -107,3 +107,24 @@ def test_pybind_module_mirrors_reference_conventions(twfa):
         m.Plan("{}", "{}")
     with pytest.raises(ValueError, match="unknown key"):
         m.Plan(prob, json.dumps(dict(json.loads(sol), bogus=1)))
+
+
+def test_fa_bwd_entry_points_check_arguments_without_a_gpu(twfa):
+    L = twfa.lib()
+    n = ctypes.c_size_t()
+    assert L.twfa_fa_bwd_workspace_size(2, 4, 1000, 128, ctypes.byref(n)) == 0
+    rows = 2 * 4 * 1000
+    assert n.value == rows * 128 * 4 + rows * 4  # fp32 dQ accumulator + rowsum(dO * O)
+    assert L.twfa_fa_bwd_workspace_size(1, 1, 128, 64, ctypes.byref(n)) == 2
+    h = ctypes.c_void_p()
+    prob, sol = twfa.load_schedule("fa_fwd")
+    assert L.twfa_plan_create(prob.encode(), sol.encode(), ctypes.byref(h)) == 0
+    args = [None] * 10 + [0, 1, 1, 128, 128, 0, ctypes.c_float(1.0), None]
+    # a forward plan is a usage error, detected before any CUDA call
+    assert L.twfa_fa_bwd(h, *args) == 2 and b"FA-backward plan" in L.twfa_last_error()
+    assert L.twfa_fa_bwd(None, *args) == 2
+    L.twfa_plan_destroy(h)
+    prob, sol = twfa.load_schedule("fa_bwd")
+    assert L.twfa_plan_create(prob.encode(), sol.encode(), ctypes.byref(h)) == 0
+    assert L.twfa_fa_bwd(h, *args) == 2 and b"NULL" in L.twfa_last_error()  # q is NULL
+    L.twfa_plan_destroy(h)
