@@ -344,8 +344,10 @@ __device__ __forceinline__ void rd_op(const BwdCtx& c, const FaBwdArgs& a, const
     }
     return;
   }
-  // DQ_i has completed (dq_full): the dS buffer is free for staging. Two
-  // halves of 64 columns (two 16 KiB boxes each) keep the row at 64 registers.
+  // DQ_i has completed (dq_full): the dS buffer is free for staging. Its two
+  // 16 KiB halves alternate as staging for the four 32-column boxes of the
+  // dQ tile, so the bulk reduction of one box overlaps the staging of the
+  // next; the row is read in two 64-column halves (64 registers).
 #pragma unroll 1
   for (int h = 0; h < 2; ++h) {
     uint32_t v[64];
@@ -354,24 +356,26 @@ __device__ __forceinline__ void rd_op(const BwdCtx& c, const FaBwdArgs& a, const
     tmem_ld_wait();
     if (h == 1) {
       tc_fence_before();
-      warp_arrive(&bar.q_free);      // dP^T(i+1) may overwrite the columns
-      if (leader) bulk_wait_read();  // half 0's reduce has read the staging buffer
-      named_bar_sync(nb, 128);
+      warp_arrive(&bar.q_free);  // dP^T(i+1) may overwrite the columns
     }
 #pragma unroll
-    for (int box = 0; box < 2; ++box) {
-      const uint32_t base = smem_u32(c.ds) + box * kHalf + r * 128;
+    for (int hb = 0; hb < 2; ++hb) {
+      const int box = 2 * h + hb;  // staging half = hb
+      if (box >= 2) {
+        if (leader) bulk_wait_read_1();  // the reduce of box - 2 has read this half
+        named_bar_sync(nb, 128);
+      }
+      const uint32_t base = smem_u32(c.ds) + hb * kHalf + r * 128;
 #pragma unroll
       for (int ch = 0; ch < 8; ++ch)
-        st_shared_v4(base + ((ch ^ (r & 7)) << 4), v[box * 32 + 4 * ch], v[box * 32 + 4 * ch + 1],
-                     v[box * 32 + 4 * ch + 2], v[box * 32 + 4 * ch + 3]);
-    }
-    fence_proxy_async_shared();
-    named_bar_sync(nb, 128);
-    if (leader && TWFA_BWD_WHATIF != 1) {
-#pragma unroll
-      for (int box = 0; box < 2; ++box) tma_reduce_add_3d(&a.tm_dq, c.ds + box * kHalf, 64 * h + 32 * box, q0, t.bh);
-      bulk_commit();
+        st_shared_v4(base + ((ch ^ (r & 7)) << 4), v[hb * 32 + 4 * ch], v[hb * 32 + 4 * ch + 1],
+                     v[hb * 32 + 4 * ch + 2], v[hb * 32 + 4 * ch + 3]);
+      fence_proxy_async_shared();
+      named_bar_sync(nb, 128);
+      if (leader) {
+        if (TWFA_BWD_WHATIF != 1) tma_reduce_add_3d(&a.tm_dq, c.ds + hb * kHalf, 32 * box, q0, t.bh);
+        bulk_commit();
+      }
     }
   }
   if (leader) {
