@@ -115,6 +115,7 @@ struct __align__(8) FaBarriers {
   uint64_t l_full[TWFA_MAX_TILES], l_empty[TWFA_MAX_TILES];
   uint64_t sm_tok[TWFA_MAX_TILES];  // softmax order token (TWFA_SOFTMAX_TOKEN)
   uint64_t s_half[TWFA_MAX_TILES];  // split S: SA_k committed
+  uint64_t s_lo[TWFA_MAX_TILES][2];  // TWFA_S_HALVES: keys 0-63 of S_k committed
   uint64_t s_read[TWFA_MAX_TILES];  // split S: MX_k has the S row in registers
   uint32_t tmem_base;
 };
@@ -247,17 +248,26 @@ __device__ __forceinline__ float exp_store_row(const uint32_t (&s)[N], uint32_t 
 #ifndef TWFA_SPEC_EX
 #define TWFA_SPEC_EX 1
 #endif
-template <int N, class Handoff>
+// S_k issued as two N = 64 halves with a commit after the first (the
+// speculative EX starts on keys 0-63 while keys 64-127 are computed)
+#ifndef TWFA_S_HALVES
+#define TWFA_S_HALVES 0  // measured: -5 % C3 (twice the MMA issues for S outweigh the earlier start)
+#endif
+template <int N, class Handoff, class WaitRest>
 __device__ __forceinline__ float mx_ex_spec(uint32_t (&s)[N], uint32_t taddr, float sl, float& m_io, float& alpha,
-                                            uint64_t* part_bar, Handoff&& handoff) {
+                                            uint64_t* part_bar, Handoff&& handoff, WaitRest&& wait_rest) {
   constexpr int kParts = kPParts;
   constexpr int kPartKeys = N / kParts;
   constexpr int kKeys = kPartKeys < 32 ? kPartKeys : 32;
   constexpr int kRegs = kKeys / 2;
   tmem_ld32(taddr, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
   tmem_ld_wait();
+  // with S in halves, keys 64.. may still be in flight in the tensor core:
+  // load the rest of the first half, then wait for the second
+  tmem_ld32(taddr + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
+  wait_rest();
 #pragma unroll
-  for (int c = 1; c < N / 32; ++c) tmem_ld32(taddr + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&s[c * 32]));
+  for (int c = 2; c < N / 32; ++c) tmem_ld32(taddr + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&s[c * 32]));
   const float m_old = m_io;
   const float2 sl2 = make_float2(sl, sl);
   float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
@@ -491,10 +501,24 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
     const uint32_t kd = sdesc_lo(smem_u32(c.k_smem + s * G::tile), 16);
     const uint32_t d_s = tmem + k * 128 + b * KV;
     if (elect_one()) {
+      if (TWFA_S_HALVES && KV == 128) {
+        // keys 0-63, committed on their own, then keys 64-127: the softmax
+        // starts on the first half while the second is computed
 #pragma unroll
-      for (int kk = 0; kk < kHeadDim / 16; ++kk)  // 16 head dims per step, 4 per SW128 half
-        mma_ss(d_s, sdesc_join(qd + ((kk >> 2) * kHalfBytes + (kk & 3) * 32) / 16, kSdescHi),
-               sdesc_join(kd + ((kk >> 2) * G::half + (kk & 3) * 32) / 16, kSdescHi), G::idesc_s, kk > 0);
+        for (int h = 0; h < 2; ++h) {
+#pragma unroll
+          for (int kk = 0; kk < kHeadDim / 16; ++kk)
+            mma_ss(d_s + 64 * h, sdesc_join(qd + ((kk >> 2) * kHalfBytes + (kk & 3) * 32) / 16, kSdescHi),
+                   sdesc_join(kd + ((kk >> 2) * G::half + h * 64 * 128 + (kk & 3) * 32) / 16, kSdescHi), kIdescS64,
+                   kk > 0);
+          if (h == 0) mma_commit(&bar.s_lo[k][b]);
+        }
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < kHeadDim / 16; ++kk)  // 16 head dims per step, 4 per SW128 half
+          mma_ss(d_s, sdesc_join(qd + ((kk >> 2) * kHalfBytes + (kk & 3) * 32) / 16, kSdescHi),
+                 sdesc_join(kd + ((kk >> 2) * G::half + (kk & 3) * 32) / 16, kSdescHi), G::idesc_s, kk > 0);
+      }
       mma_commit(&bar.s_full[k][b]);
       mma_commit(&bar.k_empty[s]);
       if (it == N - 1) mma_commit(&bar.q_empty[k]);
@@ -570,22 +594,30 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
       const bool tok = TWFA_SOFTMAX_TOKEN && rg.ring_len == 2 && (op.flags & TWFA_OPF_FUSE_NEXT);
       if (op.kind == TWFA_OP_MX) {
         if (tok) mbar_wait(&bar.sm_tok[k], (g & 1) ^ (k == rg.ring0 ? 1u : 0u));
+        const bool spec = KV == 128 && TWFA_SPEC_EX && !rg.split && !mask && (op.flags & TWFA_OPF_FUSE_NEXT) &&
+                          __all_sync(0xffffffffu, rd(st.m_run, k) != -INFINITY);
         if (rg.split)
           mbar_wait_all(&bar.s_half[k], g & 1, &bar.s_full[k][b], pb);
+        else if (TWFA_S_HALVES && spec)
+          mbar_wait(&bar.s_lo[k][b], pb);  // keys 0-63; the rest is awaited inside the speculative EX
         else
           mbar_wait(&bar.s_full[k][b], pb);
         trace_mark<kTrace>(tr, 4);
         tc_fence_after();
         if constexpr (KV == 128) {
           const float m_old = rd(st.m_run, k);
-          if (TWFA_SPEC_EX && !rg.split && !mask && (op.flags & TWFA_OPF_FUSE_NEXT) &&
-              __all_sync(0xffffffffu, m_old != -INFINITY)) {
+          if (spec) {
             float m = m_old, alpha = 1.f;
             const uint32_t sb = g & 1;
             const float sum = mx_ex_spec<KV>(srow, taddr, c.scale_log2, m, alpha, bar.p_part[k][b], [&](float al) {
               mbar_wait(&bar.st_empty[k][sb], ((g >> 1) & 1) ^ 1);
               g_sh.stats[k][sb][c.quad * 32 + lane] = al;
               warp_arrive(&bar.st_full[k][sb]);
+            }, [&] {
+              if (TWFA_S_HALVES) {
+                mbar_wait(&bar.s_full[k][b], pb);
+                tc_fence_after();
+              }
             });
             wr(st.m_run, k, m);
             wr(st.alpha, k, alpha);
@@ -844,6 +876,8 @@ __device__ __forceinline__ FaCtx fa_setup(int tiles, int kd, int vd, int load_wa
       }
       mbar_init(&bar.sm_tok[k], 4);
       mbar_init(&bar.s_half[k], 1);
+      mbar_init(&bar.s_lo[k][0], 1);
+      mbar_init(&bar.s_lo[k][1], 1);
       mbar_init(&bar.s_read[k], 4);
       mbar_init(&bar.l_full[k], 4);
       mbar_init(&bar.l_empty[k], 4);
