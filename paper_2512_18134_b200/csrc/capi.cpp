@@ -6,8 +6,12 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <queue>
 #include <string>
+#include <tuple>
+#include <vector>
 
 #include "../../include/twfa.h"
 #include "fa_bwd.h"
@@ -106,6 +110,83 @@ void require_aligned(const void* p, const char* what) {
   if (reinterpret_cast<uintptr_t>(p) % 16 != 0) throw twfa::UsageError(std::string(what) + " is not 16-byte aligned");
 }
 
+// Causal work lists. A causal launch has work tiles of very different
+// length (query block qb of a (b, h) needs 2 (qb + 1) K / V iterations).
+// Tiles are taken in (b, h) groups small enough that the group's K and V
+// stay in L2 (<= 48 MiB), longest first inside a group, and each goes to the
+// CTA with the least work so far (LPT): the CTAs move through the groups
+// together, so the tiles running at any moment share K / V, and their totals
+// stay balanced. The lists depend only on (device, B*H, S, grid) and are
+// built once and kept for the process lifetime (read-only on the device).
+struct WorkLists {
+  int* list = nullptr;
+  int* off = nullptr;
+};
+
+// kind 0: forward (tile = 256 queries; causal work index w = (qbl-1-qb)*bh + b,
+// 2 (qb + 1) K/V iterations); kind 1: backward (tile = 128 keys; causal work
+// index w = j*bh + b, nq - j Q iterations). The group bound applies to the
+// streamed operands of one (b, h): K, V (forward) or Q, dO (backward).
+WorkLists causal_work_lists(int kind, int bh, int S, int grid) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, int, int, int>, WorkLists> cache;
+  int dev = 0;
+  check(cudaGetDevice(&dev), "cudaGetDevice");
+  std::lock_guard<std::mutex> lock(mu);
+  const auto key = std::make_tuple(kind, dev, bh, S, grid);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  const int tile = kind == 0 ? 256 : 128;
+  const int nt = (S + tile - 1) / tile;  // tiles per (b, h)
+  const int num = bh * nt;
+  const long long stream_bytes = 2LL * S * 128 * 2;  // the two streamed operands of one (b, h)
+  const int group = static_cast<int>(std::max<long long>(1, (48LL << 20) / stream_bytes));
+  // candidate order: (b, h) groups, longest first inside a group
+  std::vector<int> order;
+  order.reserve(static_cast<size_t>(num));
+  for (int g0 = 0; g0 < bh; g0 += group)
+    for (int rank = 0; rank < nt; ++rank)  // rank 0 = the longest tile of a (b, h)
+      for (int b = g0; b < std::min(bh, g0 + group); ++b) order.push_back(rank * bh + b);
+  using Load = std::pair<long long, int>;
+  std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
+  for (int x = 0; x < grid; ++x) heap.push({0, x});
+  std::vector<std::vector<int>> per(static_cast<size_t>(grid));
+  for (int w : order) {
+    const int rank = w / bh;
+    long long iters;
+    if (kind == 0) {
+      const int qb = nt - 1 - rank;
+      iters = (std::min<long long>(S, 256LL * (qb + 1)) + 127) / 128;
+    } else {
+      iters = nt - rank;  // K/V tile j = rank sees Q tiles j .. nt-1
+    }
+    const long long cost = iters + 2;  // iterations + the tile boundary
+    Load l = heap.top();
+    heap.pop();
+    per[static_cast<size_t>(l.second)].push_back(w);
+    heap.push({l.first + cost, l.second});
+  }
+  std::vector<int> list, off(static_cast<size_t>(grid) + 1, 0);
+  for (int x = 0; x < grid; ++x) {
+    off[static_cast<size_t>(x)] = static_cast<int>(list.size());
+    list.insert(list.end(), per[static_cast<size_t>(x)].begin(), per[static_cast<size_t>(x)].end());
+  }
+  off[static_cast<size_t>(grid)] = static_cast<int>(list.size());
+  WorkLists wl;
+  check(cudaMalloc(&wl.list, list.size() * sizeof(int)), "cudaMalloc work list");
+  check(cudaMalloc(&wl.off, off.size() * sizeof(int)), "cudaMalloc work offsets");
+  check(cudaMemcpy(wl.list, list.data(), list.size() * sizeof(int), cudaMemcpyHostToDevice), "H2D work list");
+  check(cudaMemcpy(wl.off, off.data(), off.size() * sizeof(int), cudaMemcpyHostToDevice), "H2D work offsets");
+  cache[key] = wl;
+  return wl;
+}
+
+// TWFA_WORK_LISTS=0 keeps the arithmetic causal order (comparison runs)
+bool use_work_lists() {
+  const char* e = std::getenv("TWFA_WORK_LISTS");
+  return !(e && std::strcmp(e, "0") == 0);
+}
+
 int fa_fwd_impl(const twfa_plan* plan, const void* q, const void* k, const void* v, void* o, float* lse, int B,
                 int H, int S, int D, int causal, float scale, uint32_t* trace, uint32_t cap, void* stream) {
   if (!plan) throw twfa::UsageError("plan is NULL");
@@ -141,6 +222,13 @@ int fa_fwd_impl(const twfa_plan* plan, const void* q, const void* k, const void*
   a.scale_log2 = scale * 1.4426950408889634f;
   const long long work = static_cast<long long>(bh) * ((S + 255) / 256);
   const int grid = static_cast<int>(std::min<long long>(work, sm_count()));
+  a.work_list = nullptr;
+  a.work_off = nullptr;
+  if (causal && use_work_lists()) {
+    const WorkLists wl = causal_work_lists(0, static_cast<int>(bh), S, grid);
+    a.work_list = wl.list;
+    a.work_off = wl.off;
+  }
   check(twfa::fa_fwd_launch(tq, tk, tv, p, a, grid, static_cast<cudaStream_t>(stream), allow_specialized()),
         "fa_fwd launch");
   return TWFA_OK;
@@ -187,6 +275,13 @@ int fa_bwd_impl(const twfa_plan* plan, const void* q, const void* k, const void*
   a.scale_log2 = scale * 1.4426950408889634f;
   const long long work = static_cast<long long>(bh) * ((S + 127) / 128);
   const int grid = static_cast<int>(std::min<long long>(work, sm_count()));
+  a.work_list = nullptr;
+  a.work_off = nullptr;
+  if (causal && use_work_lists()) {
+    const WorkLists wl = causal_work_lists(1, static_cast<int>(bh), S, grid);
+    a.work_list = wl.list;
+    a.work_off = wl.off;
+  }
   check(twfa::fa_bwd_launch(p, a, static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(dout),
                             static_cast<__nv_bfloat16*>(dq), grid, static_cast<cudaStream_t>(stream)),
         "fa_bwd launch");

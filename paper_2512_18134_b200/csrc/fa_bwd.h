@@ -27,6 +27,10 @@ struct FaBwdArgs {
   int causal;
   float scale;        // softmax scale
   float scale_log2;   // scale * log2(e)
+  // optional per-CTA work lists (causal): CTA x runs work_list[work_off[x]
+  // .. work_off[x + 1]) in order; nullptr = round-robin over the CTAs
+  const int* work_list;
+  const int* work_off;
 };
 
 size_t fa_bwd_smem_bytes(const TwfaDevicePlan& plan);

@@ -585,7 +585,16 @@ __device__ __forceinline__ void bwd_run(const BwdCtx& c, const TwfaDevicePlan& p
   const bool is_mma = c.warp == static_cast<uint32_t>(plan.mma_warp);
   BwdState st{0, 0, -1, -1};
   uint32_t gbase = 0, icount = 0;
-  for (int work = blockIdx.x; work < c.num_work; work += gridDim.x, ++icount) {
+  for (int i = 0;; ++i, ++icount) {
+    int work;
+    if (a.work_list != nullptr) {
+      const int o = a.work_off[blockIdx.x] + i;
+      if (o >= a.work_off[blockIdx.x + 1]) break;
+      work = a.work_list[o];
+    } else {
+      work = static_cast<int>(blockIdx.x) + i * static_cast<int>(gridDim.x);
+      if (work >= c.num_work) break;
+    }
     const BwdItem t = bwd_item(c, a, work, gbase, icount);
     if constexpr (kRole == kLight) {
       if (is_load) {  // K and V of the work item

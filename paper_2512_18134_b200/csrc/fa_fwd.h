@@ -22,6 +22,10 @@ struct FaArgs {
   int B, H, S;
   int causal;
   float scale_log2;    // softmax_scale * log2(e)
+  // optional per-CTA work lists (causal): CTA x runs work_list[work_off[x]
+  // .. work_off[x + 1]) in order; nullptr = the arithmetic round order
+  const int* work_list;
+  const int* work_off;
 };
 
 size_t fa_fwd_smem_bytes(const TwfaDevicePlan& plan);

@@ -786,12 +786,19 @@ __device__ __forceinline__ void epilogue(const FaCtx& c, const WorkTile& t, int 
 }
 
 // Work-tile loop of one warp. `trip` runs the warp's trip program for trip r.
+// The i-th work tile of this CTA: from the host's per-CTA list (causal:
+// load-balanced, (b, h)-grouped for L2 reuse of K / V), else round-robin
+// over the persistent CTAs.
 template <int KV>
-__device__ __forceinline__ int work_of(const FaArgs& args, int round) {
-  // causal tiles are ordered longest first; alternating the direction of
-  // each round over the persistent CTAs ("snake") balances their totals
-  return round * static_cast<int>(gridDim.x) +
-         ((args.causal && (round & 1)) ? static_cast<int>(gridDim.x - 1 - blockIdx.x) : static_cast<int>(blockIdx.x));
+__device__ __forceinline__ int work_of(const FaCtx& c, const FaArgs& args, int i) {
+  if (args.work_list != nullptr) {
+    const int o = args.work_off[blockIdx.x] + i;
+    return o < args.work_off[blockIdx.x + 1] ? args.work_list[o] : c.num_work;
+  }
+  // causal without a list: longest first, alternating the direction of each
+  // round over the persistent CTAs ("snake") to balance their totals
+  return i * static_cast<int>(gridDim.x) +
+         ((args.causal && (i & 1)) ? static_cast<int>(gridDim.x - 1 - blockIdx.x) : static_cast<int>(blockIdx.x));
 }
 
 // cross-tile prefetch (Q on an idle warp, the next tile's first K / V
@@ -806,7 +813,7 @@ __device__ __forceinline__ void work_loop(const FaCtx& c, const FaArgs& args, co
   uint32_t gbase = 0, tcount = 0;
   st.k_next = st.v_next = 0;
   for (int round = 0;; ++round, ++tcount) {
-    const int work = work_of<KV>(args, round);
+    const int work = work_of<KV>(c, args, round);
     if (work >= c.num_work) break;
     const WorkTile t = work_tile<KV>(c, args, work, gbase, tcount);
     if (TWFA_XTILE && is_q_warp) {  // Q of every tile, as soon as the previous tile's last S_k released it
@@ -816,7 +823,7 @@ __device__ __forceinline__ void work_loop(const FaCtx& c, const FaArgs& args, co
     }
     if (is_load_warp) {
       if (!TWFA_XTILE || !(c.q_warp >= 0)) load_q(c, t, tiles, tm);
-      const int nwork = work_of<KV>(args, round + 1);
+      const int nwork = work_of<KV>(c, args, round + 1);
       st.next_N = 0;
       if (TWFA_XTILE && nwork < c.num_work) {
         const WorkTile nt = work_tile<KV>(c, args, nwork, gbase + static_cast<uint32_t>(t.N), tcount + 1);
