@@ -311,7 +311,13 @@ __device__ __forceinline__ void ds_part(const BwdCtx& c, const FaBwdArgs& a, con
 // RD: dQ_i from TMEM (row = query) -> smem staging (fp32, SW128 boxes of
 // 128 rows x 32 columns) -> cp.reduce.async.bulk add into the fp32 dQ
 // accumulator (the atomic reduction of the paper's backward loop).
-__device__ __forceinline__ void rd_op(const BwdCtx& c, const FaBwdArgs& a, const BwdItem& t, int it, uint32_t g) {
+__device__ __forceinline__ void rd_op(const BwdCtx& c, const FaBwdArgs& a, const BwdItem& t, int it, uint32_t g,
+                                      const TwfaDevicePlan& plan) {
+  // staging buffer: Q_i's ring slot when the schedule says so (plan.s_split
+  // for the backward family; DK_i is complete once DQ_i is), else dS's
+  const bool q_stage = plan.s_split != 0;
+  const uint32_t qs = g % plan.k_depth;
+  uint8_t* const stage_buf = q_stage ? c.q + qs * kTile : c.ds;
   BwdBarriers& bar = g_bb;
   const int q0 = (t.q_first + it) * kT;
   const uint32_t r = c.quad * 32 + c.lane;
@@ -320,8 +326,9 @@ __device__ __forceinline__ void rd_op(const BwdCtx& c, const FaBwdArgs& a, const
   mbar_wait(&bar.dq_full, g & 1);
   tc_fence_after();
   if (TWFA_BWD_RED) {
-    // the dS buffer is not used for staging: DS(i+1) may proceed
-    if (leader) mbar_arrive(&bar.ds_free);
+    // the dS buffer is not used for staging: DS(i+1) may proceed (with Q-slot
+    // staging DQ's commit frees it, and RD releases the unused Q slot)
+    if (leader) mbar_arrive(q_stage ? &bar.q_empty[qs] : &bar.ds_free);
     float* dst = a.dq_acc + (static_cast<int64_t>(t.bh) * c.S + q0 + r) * 128;
     const bool in = q0 + static_cast<int>(r) < c.S;
 #pragma unroll 1
@@ -365,7 +372,7 @@ __device__ __forceinline__ void rd_op(const BwdCtx& c, const FaBwdArgs& a, const
         if (leader) bulk_wait_read_1();  // the reduce of box - 2 has read this half
         named_bar_sync(nb, 128);
       }
-      const uint32_t base = smem_u32(c.ds) + hb * kHalf + r * 128;
+      const uint32_t base = smem_u32(stage_buf) + hb * kHalf + r * 128;
 #pragma unroll
       for (int ch = 0; ch < 8; ++ch)
         st_shared_v4(base + ((ch ^ (r & 7)) << 4), v[hb * 32 + 4 * ch], v[hb * 32 + 4 * ch + 1],
@@ -373,14 +380,14 @@ __device__ __forceinline__ void rd_op(const BwdCtx& c, const FaBwdArgs& a, const
       fence_proxy_async_shared();
       named_bar_sync(nb, 128);
       if (leader) {
-        if (TWFA_BWD_WHATIF != 1) tma_reduce_add_3d(&a.tm_dq, c.ds + hb * kHalf, 32 * box, q0, t.bh);
+        if (TWFA_BWD_WHATIF != 1) tma_reduce_add_3d(&a.tm_dq, stage_buf + hb * kHalf, 32 * box, q0, t.bh);
         bulk_commit();
       }
     }
   }
   if (leader) {
     bulk_wait_read();
-    mbar_arrive(&bar.ds_free);
+    mbar_arrive(q_stage ? &bar.q_empty[qs] : &bar.ds_free);
   }
 }
 
@@ -479,7 +486,7 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
     return;
   }
   if (op.kind == TWFA_OP_RD) {
-    if constexpr (kRole == kReduce) rd_op(c, a, t, it, g);
+    if constexpr (kRole == kReduce) rd_op(c, a, t, it, g, plan);
     return;
   }
   if constexpr (kRole != kLight) return;
@@ -572,6 +579,7 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
         mma_ss(kColP, sdesc_join(ad + kk * 2048 / 16, kSdHi), sdesc_join(bd + kk * 2048 / 16, kSdHi), kIdescMM,
                kk > 0);
       mma_commit(&bar.dq_full);
+      if (op.flags & TWFA_OPF_RELEASE) mma_commit(&bar.ds_free);  // dQ staged in the Q slot: dS is free
     }
     __syncwarp();
   }

@@ -261,8 +261,6 @@ void derive_bwd(LoweredSchedule& s, NodeId&& node_id, DepthOf&& depth_of, Prefet
   p.sm_warp[1] = ds.warp_start;
   p.cr_warp[0] = rd.warp_start;  // RD warpgroup (also writes dK, dV)
   p.heavy_wg_mask = (1 << (exb.warp_start / 4)) | (1 << (ds.warp_start / 4));
-  // the later tensor-core reader of Q_i (ST, DK) and of dO_i (DP, DV)
-  // releases the ring slot with its commit
   auto later = [&](const char* a, const char* b) {
     const int x = node_id(a), y = node_id(b);
     return std::make_pair(s.m[static_cast<size_t>(x)], p.ops[x].order) >
@@ -270,6 +268,20 @@ void derive_bwd(LoweredSchedule& s, NodeId&& node_id, DepthOf&& depth_of, Prefet
                ? x
                : y;
   };
+  // dQ staging buffer: the graph says where RD stages dQ_i -- an LDQ -> RD
+  // edge puts it in Q_i's ring slot (RD then releases that slot, and DQ's
+  // commit frees the dS buffer); otherwise the dS buffer (RD frees it)
+  bool q_staging = false;
+  for (const LEdge& e : s.edges) q_staging = q_staging || (e.src == node_id("LDQ") && e.dst == node_id("RD"));
+  p.s_split = q_staging ? 1 : 0;  // FA backward: RD stages dQ in the Q ring slot
+  if (q_staging) {
+    p.ops[node_id("RD")].flags |= TWFA_OPF_RELEASE;
+    p.ops[node_id("DQ")].flags |= TWFA_OPF_RELEASE;  // DQ's commit frees the dS buffer
+    p.ops[later("DP", "DV")].flags |= TWFA_OPF_RELEASE;
+    return;
+  }
+  // the later tensor-core reader of Q_i (ST, DK) and of dO_i (DP, DV)
+  // releases the ring slot with its commit
   p.ops[later("ST", "DK")].flags |= TWFA_OPF_RELEASE;
   p.ops[later("DP", "DV")].flags |= TWFA_OPF_RELEASE;
 }
@@ -653,6 +665,7 @@ std::string describe(const LoweredSchedule& s) {
     for (int v = 0; v < p.num_nodes; ++v)
       if (p.ops[v].flags & TWFA_OPF_RELEASE) rel.push_back(s.nodes[static_cast<size_t>(v)].id);
     j["ring_release"] = rel;
+    j["dq_staging"] = p.s_split ? "Q ring slot" : "dS buffer";
     j["tmem_columns"] = {{"dK", 0}, {"dV", 128}, {"S^T/P^T/dQ", 256}, {"dP^T/dS^T", 384}};
   } else {
     rings["AB"] = p.k_depth;

@@ -110,3 +110,12 @@ def test_pybind_module_runs_the_same_backward(twfa, plans):
     torch.cuda.synchronize()
     assert torch.equal(dk, ref[1]) and torch.equal(dv, ref[2])
     assert (dq.float() - ref[0].float()).abs().max().item() <= 1e-2 * ref[0].float().abs().max().item()
+
+
+@pytest.mark.parametrize("S,causal", [(256, False), (384, True), (200, False)])
+def test_q_slot_staging_schedule_matches_oracle(twfa, plans, S, causal):
+    # fa_bwd_qstage: the graph's LDQ -> RD edge makes RD stage dQ_i in Q_i's
+    # ring slot (released by RD), and DQ's commit frees the dS buffer
+    p = twfa.Plan(*twfa.load_schedule("fa_bwd_qstage"))
+    assert p.describe()["dq_staging"] == "Q ring slot"
+    _check(twfa, (plans[0], p), 1, 2, S, causal, 13)

@@ -169,7 +169,7 @@ def fa_forward_problem(tc_variable_latency=False, calibrated=False, s_ring=1, sp
     return {"machine": machine, "graph": {"nodes": nodes, "edges": edges}}
 
 
-def fa_backward_problem(calibrated=False, fused=False, exb_spill=16):
+def fa_backward_problem(calibrated=False, fused=False, exb_spill=16, q_staging=False):
     """FA-backward loop body on sm_100a (the paper's second workload,
     PAPER.md:1073-1148; the single-pass algorithm of FA3): one CTA owns a
     128-key K/V tile (K, V resident in shared memory, dK and dV accumulated
@@ -252,7 +252,13 @@ def fa_backward_problem(calibrated=False, fused=False, exb_spill=16):
             edge("EXB", "DV", ex, blocking=True), edge("EXB", "DS", ex),
             edge("DP", "DS", g, blocking=True),
             edge("DS", "DK", dsc, blocking=True), edge("DS", "DQ", dsc, blocking=True),
-            edge("RD", "DS", 2, delta=1, blocking=True),
+            # RD stages dQ_i in shared memory: in the dS buffer (DS(i+1) then
+            # waits for RD(i)), or -- q_staging -- in Q_i's ring slot, which
+            # DK(i) has finished reading once DQ(i) completed: DS(i+1) then
+            # only waits for DQ(i) to have read dS(i), and RD(i) holds the Q
+            # slot (edge LDQ -> RD) until its bulk reductions have read it
+            *([edge("DQ", "DS", g, delta=1, blocking=True), edge("LDQ", "RD", 0)] if q_staging
+              else [edge("RD", "DS", 2, delta=1, blocking=True)]),
             edge("EXB", "EXB", ex, delta=1), edge("DS", "DS", dsc, delta=1),
         ]
         if exb_spill < ex:
@@ -378,6 +384,8 @@ def main():
         # warpgroups and pipelines across iterations (I = 12 x 256 clk); the
         # realized loop is slower (DESIGN 12: the dS / dQ-staging buffer)
         "fa_bwd_split": (fa_backward_problem(exb_spill=1), 2, 13),
+        # the split model with dQ staged in the Q ring slot (no RD -> DS chain)
+        "fa_bwd_qstage": (fa_backward_problem(exb_spill=1, q_staging=True), 2, 13),
         "fa_bwd_cal": (fa_backward_problem(calibrated=True), 2, 14),
     }
     for name, (raw, depth, res) in probs.items():
