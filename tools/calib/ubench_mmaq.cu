@@ -8,7 +8,7 @@
 #include "../../paper_2512_18134_b200/csrc/sm100.cuh"
 using namespace twfa;
 constexpr int kN = 48;
-template <bool kTS>
+template <int kMode>  // 0: SS K-major, 1: TS (A in TMEM) B MN-major, 2: SS A and B MN-major
 __global__ void __launch_bounds__(128, 1) k_mmaq(uint32_t* out) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t tbase;
@@ -29,8 +29,12 @@ __global__ void __launch_bounds__(128, 1) k_mmaq(uint32_t* out) {
       t[0] = static_cast<uint32_t>(clock64());
 #pragma unroll
       for (int i = 0; i < kN; ++i) {
-        if constexpr (kTS)  // A (bf16) from tensor memory columns 256.., like PV of the FA kernel
+        if constexpr (kMode == 1)  // A (bf16) from tensor memory columns 256.., like PV of the FA kernel
           mma_ts(0, 256 + (i & 7) * 8, sdesc_join(b + (i & 3) * 128, hi), idesc_bf16_f32(128, 128, 1), i > 0);
+        else if constexpr (kMode == 2)  // like DQ of the backward: A and B MN-major (LBO = 16 KiB halves)
+          mma_ss(0, sdesc_join(sdesc_lo(smem_u32(smem) + (i & 3) * 2048, 16384), hi),
+                 sdesc_join(sdesc_lo(smem_u32(smem) + 32768 + (i & 3) * 2048, 16384), hi),
+                 idesc_bf16_f32(128, 128, 1) | (1u << 15), i > 0);
         else
           mma_ss(0, sdesc_join(a + (i & 3) * 2, hi), sdesc_join(b + (i & 3) * 2, hi), idesc_bf16_f32(128, 128, 0), i > 0);
         t[i + 1] = static_cast<uint32_t>(clock64());
@@ -46,7 +50,7 @@ __global__ void __launch_bounds__(128, 1) k_mmaq(uint32_t* out) {
   __syncthreads();
   if (warp == 0) { tc_fence_after(); tmem_dealloc<512>(tbase); }
 }
-template <bool kTS>
+template <int kTS>
 int run(const char* name) {
   uint32_t* d; cudaMalloc(&d, 4 * (kN + 2));
   cudaFuncSetAttribute(k_mmaq<kTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
@@ -60,4 +64,4 @@ int run(const char* name) {
   cudaFree(d);
   return 0;
 }
-int main() { return run<false>("SS") | run<true>("TS (A in TMEM)"); }
+int main() { return run<0>("SS") | run<1>("TS (A in TMEM)") | run<2>("SS, A and B MN-major"); }

@@ -3,7 +3,7 @@ cat > /tmp/p.py <<'PY'
 import os, sys, torch
 sys.path.insert(0, os.getcwd())
 import paper_2512_18134_b200 as twfa
-fp = twfa.Plan(*twfa.load_schedule("fa_fwd")); bp = twfa.Plan(*twfa.load_schedule("fa_bwd"))
+fp = twfa.Plan(*twfa.load_schedule("fa_fwd")); bp = twfa.Plan(*twfa.load_schedule(os.environ.get("BSCHED", "fa_bwd")))
 B, H, S = 4, 32, 8192
 q, k, v, do = (torch.randn(B, H, S, 128, device="cuda").to(torch.bfloat16) for _ in range(4))
 o, lse = twfa.fa_fwd(fp, q, k, v, return_lse=True)
