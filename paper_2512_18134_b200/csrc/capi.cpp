@@ -140,7 +140,10 @@ WorkLists causal_work_lists(int kind, int bh, int S, int grid) {
   const int nt = (S + tile - 1) / tile;  // tiles per (b, h)
   const int num = bh * nt;
   const long long stream_bytes = 2LL * S * 128 * 2;  // the two streamed operands of one (b, h)
-  const int group = static_cast<int>(std::max<long long>(1, (48LL << 20) / stream_bytes));
+  // L2 budget of one group (TWFA_WL_GROUP_MB overrides, for measurements)
+  long long budget = 48LL << 20;
+  if (const char* e = std::getenv("TWFA_WL_GROUP_MB")) budget = std::atoll(e) << 20;
+  const int group = static_cast<int>(std::max<long long>(1, budget / stream_bytes));
   // candidate order: (b, h) groups, longest first inside a group
   std::vector<int> order;
   order.reserve(static_cast<size_t>(num));
