@@ -195,3 +195,15 @@ def test_split_s_schedule_matches_oracle(twfa, S, causal):
     p = twfa.Plan(*twfa.load_schedule("fa_fwd_split"))
     assert p.describe()["s_split"] == 1
     _check(twfa, p, 1, 2, S, causal, 14)
+
+
+def test_causal_work_lists_do_not_change_results(twfa, plan, monkeypatch):
+    # the per-CTA work lists only reorder tiles over the CTAs: every tile is
+    # computed the same way, so O is bit-identical to the arithmetic order
+    q, k, v = (x.cuda() for x in _inputs(2, 48, 640, 128, 17))
+    with_lists = twfa.fa_fwd(plan, q, k, v, causal=True)
+    torch.cuda.synchronize()
+    monkeypatch.setenv("TWFA_WORK_LISTS", "0")
+    without = twfa.fa_fwd(plan, q, k, v, causal=True)
+    torch.cuda.synchronize()
+    assert torch.equal(with_lists, without)
