@@ -119,3 +119,20 @@ def test_q_slot_staging_schedule_matches_oracle(twfa, plans, S, causal):
     p = twfa.Plan(*twfa.load_schedule("fa_bwd_qstage"))
     assert p.describe()["dq_staging"] == "Q ring slot"
     _check(twfa, (plans[0], p), 1, 2, S, causal, 13)
+
+
+def test_causal_work_lists_keep_dk_dv(twfa, plans, monkeypatch):
+    # reordering the K/V tiles over the CTAs leaves dK, dV bit-identical
+    # (each accumulates inside one CTA); dQ sums the same terms in another
+    # order (fp32 reduce-adds)
+    fp, bp = plans
+    g = torch.Generator(device="cpu").manual_seed(23)
+    q, k, v, do = (torch.randn(2, 24, 640, 128, generator=g).to(torch.bfloat16).cuda() for _ in range(4))
+    o, lse = twfa.fa_fwd(fp, q, k, v, causal=True, return_lse=True)
+    a = twfa.fa_bwd(bp, q, k, v, o, do, lse, causal=True)
+    torch.cuda.synchronize()
+    monkeypatch.setenv("TWFA_WORK_LISTS", "0")
+    b = twfa.fa_bwd(bp, q, k, v, o, do, lse, causal=True)
+    torch.cuda.synchronize()
+    assert torch.equal(a[1], b[1]) and torch.equal(a[2], b[2])
+    assert (a[0].float() - b[0].float()).abs().max().item() <= 1e-2 * b[0].float().abs().max().item()
