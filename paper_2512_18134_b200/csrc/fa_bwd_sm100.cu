@@ -52,8 +52,8 @@ constexpr uint32_t kIdescKK = idesc_bf16_f32(128, 128, 0);  // A, B K-major
 constexpr uint32_t kIdescKM = idesc_bf16_f32(128, 128, 1);  // A K-major (or TMEM), B MN-major
 constexpr uint32_t kIdescMM = idesc_bf16_f32(128, 128, 1) | (1u << 15);  // A and B MN-major
 constexpr uint32_t kSdHi = sdesc_hi(1024);
-// timing-only experiment (results WRONG when set): 1 = RD skips the
-// reduce-add
+// timing-only experiments (results WRONG when set): 1 = RD skips the
+// reduce-add; 2 = no shared-memory traffic from DS (dS) and RD (staging)
 #ifndef TWFA_BWD_WHATIF
 #define TWFA_BWD_WHATIF 0
 #endif
@@ -295,6 +295,7 @@ __device__ __forceinline__ void ds_part(const BwdCtx& c, const FaBwdArgs& a, con
     }
     tmem_st16(c.lane_off + kColP + cc * 16, pk);
     // queries 32cc .. 32cc+31: SW128 half cc/2, 16-byte chunks 4(cc%2) .. +3
+    if (TWFA_BWD_WHATIF == 2) continue;  // timing only: no dS in shared memory
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
       const uint32_t ch = (cc & 1) * 4 + m;
@@ -349,6 +350,20 @@ __device__ __forceinline__ void rd_op(const BwdCtx& c, const FaBwdArgs& a, const
                        : "memory");
       }
     }
+    return;
+  }
+  if (TWFA_BWD_WHATIF == 2) {  // timing only: read dQ_i out, no staging / reduction
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+      uint32_t v[64];
+      tmem_ld32(c.lane_off + kColP + h * 64, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+      tmem_ld32(c.lane_off + kColP + h * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+      tmem_ld_wait();
+      asm volatile("" ::"r"(v[0]), "r"(v[63]));
+    }
+    tc_fence_before();
+    warp_arrive(&bar.q_free);
+    if (leader) mbar_arrive(q_stage ? &bar.q_empty[qs] : &bar.ds_free);
     return;
   }
   // DQ_i has completed (dq_full): the dS buffer is free for staging. Its two
