@@ -148,16 +148,29 @@ def fa_fwd(plan, q, k, v, causal=False, softmax_scale=None, return_lse=False, ou
     q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
     B, H, S, D = q.shape
     scale = float(softmax_scale) if softmax_scale is not None else 1.0 / math.sqrt(D)
+    if out is not None:
+        # the C side encodes O's tensor map as a contiguous bf16 [B, H, S, 128]
+        if out.shape != q.shape or out.dtype != torch.bfloat16 or out.device != q.device or not out.is_contiguous():
+            raise ValueError("out must be a contiguous bf16 tensor of q's shape on q's device")
+    if k.device != q.device or v.device != q.device:
+        raise ValueError("q, k, v must be on one device")
     o = out if out is not None else torch.empty_like(q)
     lse = torch.empty((B, H, S), device=q.device, dtype=torch.float32) if return_lse else None
+    if trace is not None:
+        need = plan.describe()["num_warps"] * int(trace_cap) * 8
+        if trace.dtype not in (torch.int32, torch.uint32) or not trace.is_contiguous() or trace.device != q.device \
+                or trace.numel() < need or trace_cap < 2:
+            raise ValueError(f"trace must be a contiguous int32 tensor on q's device with >= num_warps * trace_cap "
+                             f"* 8 = {need} elements (trace_cap >= 2)")
     args = (plan.handle, ctypes.c_void_p(q.data_ptr()), ctypes.c_void_p(k.data_ptr()),
             ctypes.c_void_p(v.data_ptr()), ctypes.c_void_p(o.data_ptr()),
             ctypes.c_void_p(lse.data_ptr()) if lse is not None else None,
             B, H, S, D, int(bool(causal)), scale)
-    if trace is not None:
-        _check(lib().twfa_fa_fwd_traced(*args, ctypes.c_void_p(trace.data_ptr()), trace_cap, _stream_ptr(q)))
-    else:
-        _check(lib().twfa_fa_fwd(*args, _stream_ptr(q)))
+    with torch.cuda.device(q.device):
+        if trace is not None:
+            _check(lib().twfa_fa_fwd_traced(*args, ctypes.c_void_p(trace.data_ptr()), trace_cap, _stream_ptr(q)))
+        else:
+            _check(lib().twfa_fa_fwd(*args, _stream_ptr(q)))
     return (o, lse) if return_lse else o
 
 
@@ -199,10 +212,13 @@ def fa_bwd(plan, q, k, v, o, dout, lse, causal=False, softmax_scale=None, worksp
     if workspace is None or workspace.numel() * workspace.element_size() < need.value:
         workspace = torch.empty(need.value, device=q.device, dtype=torch.uint8)
     dq, dk, dv = (torch.empty_like(q) for _ in range(3))
+    if any(t.device != q.device for t in ts) or lse.device != q.device:
+        raise ValueError("inputs must be on one device")
     ptr = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
-    _check(lib().twfa_fa_bwd(plan.handle, ptr(q), ptr(k), ptr(v), ptr(o), ptr(dout), ptr(lse), ptr(dq), ptr(dk),
-                             ptr(dv), ptr(workspace), need.value, B, H, S, D, int(bool(causal)), scale,
-                             _stream_ptr(q)))
+    with torch.cuda.device(q.device):
+        _check(lib().twfa_fa_bwd(plan.handle, ptr(q), ptr(k), ptr(v), ptr(o), ptr(dout), ptr(lse), ptr(dq), ptr(dk),
+                                 ptr(dv), ptr(workspace), need.value, B, H, S, D, int(bool(causal)), scale,
+                                 _stream_ptr(q)))
     return dq, dk, dv
 
 
@@ -216,7 +232,13 @@ def gemm(plan, a, b, out=None):
     N = b.shape[0]
     if b.shape[1] != K:
         raise ValueError("a and b must share K")
+    if b.device != a.device:
+        raise ValueError("a and b must be on one device")
+    if out is not None and (tuple(out.shape) != (M, N) or out.dtype != torch.bfloat16 or out.device != a.device
+                            or not out.is_contiguous()):
+        raise ValueError("out must be a contiguous bf16 [M, N] tensor on a's device")
     c = out if out is not None else torch.empty((M, N), device=a.device, dtype=torch.bfloat16)
-    _check(lib().twfa_gemm(plan.handle, ctypes.c_void_p(a.data_ptr()), ctypes.c_void_p(b.data_ptr()),
-                           ctypes.c_void_p(c.data_ptr()), M, N, K, _stream_ptr(a)))
+    with torch.cuda.device(a.device):
+        _check(lib().twfa_gemm(plan.handle, ctypes.c_void_p(a.data_ptr()), ctypes.c_void_p(b.data_ptr()),
+                               ctypes.c_void_p(c.data_ptr()), M, N, K, _stream_ptr(a)))
     return c

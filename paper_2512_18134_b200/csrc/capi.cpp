@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <map>
 #include <mutex>
 #include <queue>
@@ -116,33 +117,45 @@ void require_aligned(const void* p, const char* what) {
 // stay in L2 (<= 48 MiB), longest first inside a group, and each goes to the
 // CTA with the least work so far (LPT): the CTAs move through the groups
 // together, so the tiles running at any moment share K / V, and their totals
-// stay balanced. The lists depend only on (device, B*H, S, grid) and are
-// built once and kept for the process lifetime (read-only on the device).
+// stay balanced. The lists depend only on (device, B*H, S, grid, group
+// budget); they are built once, uploaded on the launch stream (which is then
+// synchronized, so the first launch of a shape reads finished lists and the
+// host copy may be released) and kept read-only on the device. The cache
+// holds at most kMaxWorkLists shapes; the oldest entry is freed (after a
+// device synchronize, since an earlier launch may still read it) when a new
+// shape would exceed that.
 struct WorkLists {
   int* list = nullptr;
   int* off = nullptr;
 };
+constexpr size_t kMaxWorkLists = 64;
+
+long long work_list_budget() {
+  long long mb = 48;  // TWFA_WL_GROUP_MB overrides (measurements); clamped to >= 1 MiB
+  if (const char* e = std::getenv("TWFA_WL_GROUP_MB")) mb = std::max(1LL, std::atoll(e));
+  return mb * (1LL << 20);
+}
 
 // kind 0: forward (tile = 256 queries; causal work index w = (qbl-1-qb)*bh + b,
 // 2 (qb + 1) K/V iterations); kind 1: backward (tile = 128 keys; causal work
 // index w = j*bh + b, nq - j Q iterations). The group bound applies to the
 // streamed operands of one (b, h): K, V (forward) or Q, dO (backward).
-WorkLists causal_work_lists(int kind, int bh, int S, int grid) {
+WorkLists causal_work_lists(int kind, int bh, int S, int grid, cudaStream_t stream) {
+  using Key = std::tuple<int, int, int, int, int, long long>;
   static std::mutex mu;
-  static std::map<std::tuple<int, int, int, int, int>, WorkLists> cache;
+  static std::map<Key, WorkLists> cache;
+  static std::deque<Key> order_of_use;
   int dev = 0;
   check(cudaGetDevice(&dev), "cudaGetDevice");
+  const long long budget = work_list_budget();
   std::lock_guard<std::mutex> lock(mu);
-  const auto key = std::make_tuple(kind, dev, bh, S, grid);
+  const Key key = std::make_tuple(kind, dev, bh, S, grid, budget);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   const int tile = kind == 0 ? 256 : 128;
   const int nt = (S + tile - 1) / tile;  // tiles per (b, h)
   const int num = bh * nt;
   const long long stream_bytes = 2LL * S * 128 * 2;  // the two streamed operands of one (b, h)
-  // L2 budget of one group (TWFA_WL_GROUP_MB overrides, for measurements)
-  long long budget = 48LL << 20;
-  if (const char* e = std::getenv("TWFA_WL_GROUP_MB")) budget = std::atoll(e) << 20;
   const int group = static_cast<int>(std::max<long long>(1, budget / stream_bytes));
   // candidate order: (b, h) groups, longest first inside a group
   std::vector<int> order;
@@ -175,14 +188,58 @@ WorkLists causal_work_lists(int kind, int bh, int S, int grid) {
     list.insert(list.end(), per[static_cast<size_t>(x)].begin(), per[static_cast<size_t>(x)].end());
   }
   off[static_cast<size_t>(grid)] = static_cast<int>(list.size());
+  if (cache.size() >= kMaxWorkLists) {  // evict the oldest shape
+    const Key old = order_of_use.front();
+    order_of_use.pop_front();
+    const WorkLists w = cache[old];
+    int cur = 0;
+    check(cudaGetDevice(&cur), "cudaGetDevice");
+    check(cudaSetDevice(std::get<1>(old)), "cudaSetDevice");
+    check(cudaDeviceSynchronize(), "cudaDeviceSynchronize (work-list eviction)");
+    cudaFree(w.list);
+    cudaFree(w.off);
+    check(cudaSetDevice(cur), "cudaSetDevice");
+    cache.erase(old);
+  }
   WorkLists wl;
-  check(cudaMalloc(&wl.list, list.size() * sizeof(int)), "cudaMalloc work list");
+  check(cudaMalloc(&wl.list, std::max<size_t>(1, list.size()) * sizeof(int)), "cudaMalloc work list");
   check(cudaMalloc(&wl.off, off.size() * sizeof(int)), "cudaMalloc work offsets");
-  check(cudaMemcpy(wl.list, list.data(), list.size() * sizeof(int), cudaMemcpyHostToDevice), "H2D work list");
-  check(cudaMemcpy(wl.off, off.data(), off.size() * sizeof(int), cudaMemcpyHostToDevice), "H2D work offsets");
+  check(cudaMemcpyAsync(wl.list, list.data(), list.size() * sizeof(int), cudaMemcpyHostToDevice, stream),
+        "H2D work list");
+  check(cudaMemcpyAsync(wl.off, off.data(), off.size() * sizeof(int), cudaMemcpyHostToDevice, stream),
+        "H2D work offsets");
+  check(cudaStreamSynchronize(stream), "work-list upload");
   cache[key] = wl;
+  order_of_use.push_back(key);
   return wl;
 }
+
+// The device of a caller's buffer becomes the current device for the call
+// (sm count, work-list cache, kernel attributes and the launch all follow
+// it), and is restored afterwards. A host pointer is a usage error.
+struct DeviceGuard {
+  int prev = -1;
+  DeviceGuard(const void* p, const char* what) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+      cudaGetLastError();
+      throw twfa::UsageError(std::string(what) + " is not a CUDA device pointer");
+    }
+    if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged)
+      throw twfa::UsageError(std::string(what) + " is not a CUDA device pointer");
+    int cur = 0;
+    check(cudaGetDevice(&cur), "cudaGetDevice");
+    if (cur != at.device) {
+      check(cudaSetDevice(at.device), "cudaSetDevice");
+      prev = cur;
+    }
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
 
 // TWFA_WORK_LISTS=0 keeps the arithmetic causal order (comparison runs)
 bool use_work_lists() {
@@ -203,6 +260,7 @@ int fa_fwd_impl(const twfa_plan* plan, const void* q, const void* k, const void*
   require_aligned(k, "k");
   require_aligned(v, "v");
   require_aligned(o, "o");
+  DeviceGuard guard(q, "q");
   const cuuint64_t bh = static_cast<cuuint64_t>(B) * H;
   const cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(S), bh};
   const cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 2, static_cast<cuuint64_t>(S) * D * 2};
@@ -228,7 +286,7 @@ int fa_fwd_impl(const twfa_plan* plan, const void* q, const void* k, const void*
   a.work_list = nullptr;
   a.work_off = nullptr;
   if (causal && use_work_lists()) {
-    const WorkLists wl = causal_work_lists(0, static_cast<int>(bh), S, grid);
+    const WorkLists wl = causal_work_lists(0, static_cast<int>(bh), S, grid, static_cast<cudaStream_t>(stream));
     a.work_list = wl.list;
     a.work_off = wl.off;
   }
@@ -250,6 +308,7 @@ int fa_bwd_impl(const twfa_plan* plan, const void* q, const void* k, const void*
                            {dout, "dout"}, {lse, "lse"}, {dq, "dq"}, {dk, "dk"}, {dv, "dv"}, {ws, "workspace"}})
     require_aligned(ptr, name);
   if (ws_bytes < twfa::fa_bwd_workspace_bytes(B, H, S)) throw twfa::UsageError("workspace too small");
+  DeviceGuard guard(q, "q");
   const cuuint64_t bh = static_cast<cuuint64_t>(B) * H;
   const cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(S), bh};
   const cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 2, static_cast<cuuint64_t>(S) * D * 2};
@@ -281,7 +340,7 @@ int fa_bwd_impl(const twfa_plan* plan, const void* q, const void* k, const void*
   a.work_list = nullptr;
   a.work_off = nullptr;
   if (causal && use_work_lists()) {
-    const WorkLists wl = causal_work_lists(1, static_cast<int>(bh), S, grid);
+    const WorkLists wl = causal_work_lists(1, static_cast<int>(bh), S, grid, static_cast<cudaStream_t>(stream));
     a.work_list = wl.list;
     a.work_off = wl.off;
   }
@@ -430,6 +489,7 @@ int twfa_gemm(const twfa_plan* plan, const void* a, const void* b, void* c, int 
     require_aligned(a, "a");
     require_aligned(b, "b");
     require_aligned(c, "c");
+    DeviceGuard guard(a, "a");
     const cuuint64_t da[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(M)};
     const cuuint64_t db[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(N)};
     const cuuint64_t st[1] = {static_cast<cuuint64_t>(K) * 2};

@@ -25,6 +25,7 @@ exact (F = 0) with one unit = 256 SM cycles.
 import argparse
 import json
 import os
+import subprocess
 import sys
 import time
 
@@ -315,6 +316,20 @@ def load_ref():
     return _weftsched
 
 
+def solver_version(solver):
+    """`z3 --version` of the external backend (pinned with the schedule)."""
+    if not solver or solver == "internal":
+        return "internal DPLL (solverio.cpp)"
+    exe = solver.split()[0]
+    cand = os.path.join(os.path.dirname(sys.executable), exe)
+    try:
+        out = subprocess.run([cand if os.path.exists(cand) else exe, "--version"], capture_output=True, text=True,
+                             timeout=30).stdout.strip()
+    except OSError as e:
+        out = f"unavailable: {e}"
+    return out
+
+
 def solve(name, raw, resolution, stream_depth, solver=""):
     w = load_ref()
     os.makedirs(OUT, exist_ok=True)
@@ -332,6 +347,10 @@ def solve(name, raw, resolution, stream_depth, solver=""):
         "cost_map": {str(k): v for k, v in norm["cost_map"].items()},
         "F": norm["F"],
         "backend": solver or "internal",
+        "backend_version": solver_version(solver),
+        # SolveOptions defaults of the reference binding (solverio.hpp:75-81;
+        # py_joint, bindings/module.cpp:95-101): only external_command is set
+        "max_decisions": 28,
         "stream_depth": stream_depth,
         "normalize_s": round(t1 - t0, 4),
         "joint_s": round(t2 - t1, 4),
