@@ -51,6 +51,17 @@ const char* twfa_last_error(void);
  * same stage / region semantics. On success *out owns the plan. */
 int twfa_plan_create(const char* problem_json, const char* solution_json, twfa_plan** out);
 
+/* The reference's schedule checker on a (problem, solution) pair without
+ * lowering it: validate_program (sim.cpp:79-311) over the tables
+ * expand_solution (sim.cpp:57-77) builds from the reconstructed solution
+ * (cli.cpp:161-168), restated. Writes the JSON list [[family, message], ...]
+ * the reference's binding returns (bindings/module.cpp:176-184; "[]" when
+ * the schedule is exact) into buf (at most cap bytes including the NUL);
+ * *needed receives the full size. Returns 1 for malformed documents.
+ * twfa_plan_create runs the same checks and rejects any violation. */
+int twfa_schedule_validate(const char* problem_json, const char* solution_json, char* buf, size_t cap,
+                           size_t* needed);
+
 /* Release a plan (NULL is ignored). */
 void twfa_plan_destroy(twfa_plan* plan);
 

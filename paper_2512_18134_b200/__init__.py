@@ -29,6 +29,7 @@ __all__ = [
     "lib",
     "load_schedule",
     "schedule_dir",
+    "validate",
 ]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
@@ -53,6 +54,8 @@ def lib():
         L.twfa_last_error.restype = ctypes.c_char_p
         L.twfa_plan_create.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(vp)]
         L.twfa_plan_destroy.argtypes = [vp]
+        L.twfa_schedule_validate.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, sz,
+                                             ctypes.POINTER(sz)]
         L.twfa_plan_describe.argtypes = [vp, ctypes.c_char_p, sz, ctypes.POINTER(sz)]
         L.twfa_plan_raw.argtypes = [vp, vp, sz, ctypes.POINTER(sz)]
         L.twfa_fa_fwd.argtypes = [vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, i32, f32, vp]
@@ -63,7 +66,7 @@ def lib():
         L.twfa_grid_size.argtypes = [ctypes.POINTER(i32)]
         L.twfa_fa_bwd_workspace_size.argtypes = [i32, i32, i32, i32, ctypes.POINTER(sz)]
         L.twfa_fa_bwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, i32, i32, i32, i32, i32, f32, vp]
-        for name in ("twfa_plan_create", "twfa_plan_describe", "twfa_plan_raw", "twfa_fa_fwd",
+        for name in ("twfa_schedule_validate", "twfa_plan_create", "twfa_plan_describe", "twfa_plan_raw", "twfa_fa_fwd",
                      "twfa_fa_fwd_traced", "twfa_fa_fwd_host", "twfa_gemm", "twfa_grid_size",
                      "twfa_fa_bwd_workspace_size", "twfa_fa_bwd"):
             getattr(L, name).restype = i32
@@ -94,6 +97,17 @@ def load_schedule(name):
     with open(os.path.join(d, name + ".solution.json")) as f:
         sol = f.read()
     return prob, sol
+
+
+def validate(problem_json, solution_json):
+    """The reference checker (validate_program, sim.cpp:79-311) restated in
+    libtwfa: [(family, message), ...], empty when the schedule is exact."""
+    need = ctypes.c_size_t()
+    p, q = problem_json.encode(), solution_json.encode()
+    _check(lib().twfa_schedule_validate(p, q, None, 0, ctypes.byref(need)))
+    buf = ctypes.create_string_buffer(need.value)
+    _check(lib().twfa_schedule_validate(p, q, buf, need.value, ctypes.byref(need)))
+    return [tuple(x) for x in json.loads(buf.value.decode())]
 
 
 class Plan:

@@ -371,7 +371,7 @@ struct HostStaging {
 
 extern "C" {
 
-int twfa_abi_version(void) { return 1; }
+int twfa_abi_version(void) { return 2; }
 
 const char* twfa_last_error(void) { return g_last_error.c_str(); }
 
@@ -392,6 +392,22 @@ int twfa_plan_create(const char* problem_json, const char* solution_json, twfa_p
 }
 
 void twfa_plan_destroy(twfa_plan* plan) { delete plan; }
+
+int twfa_schedule_validate(const char* problem_json, const char* solution_json, char* buf, size_t cap,
+                           size_t* needed) {
+  return guarded([&] {
+    if (!problem_json || !solution_json) throw twfa::UsageError("NULL argument");
+    const twfa::LoweredSchedule s = twfa::parse(problem_json, solution_json);
+    const std::string d = twfa::violations_json(twfa::validate_schedule(s));
+    if (needed) *needed = d.size() + 1;
+    if (buf && cap > 0) {
+      const size_t n = std::min(cap - 1, d.size());
+      std::memcpy(buf, d.data(), n);
+      buf[n] = '\0';
+    }
+    return TWFA_OK;
+  });
+}
 
 int twfa_plan_describe(const twfa_plan* plan, char* buf, size_t cap, size_t* needed) {
   return guarded([&] {

@@ -31,7 +31,7 @@ int64_t get_int(const json& obj, const char* what, const char* key, bool require
   return it->get<int64_t>();
 }
 
-// ---- problem: the subset of ir.cpp:93-229 the executor needs, same strictness
+// ---- problem: parse_problem (ir.cpp:93-229), same keys, checks and messages
 void parse_problem(const std::string& text, LoweredSchedule& s) {
   json root;
   try {
@@ -46,17 +46,48 @@ void parse_problem(const std::string& text, LoweredSchedule& s) {
   const json& mj = root["machine"];
   if (!mj.is_object()) throw DomainError("\"machine\" must be an object");
   require_keys(mj, "machine", {"units", "memories", "num_warps", "reg_limit", "vl_warp"});
-  s.num_warps = static_cast<int>(get_int(mj, "machine", "num_warps", true, 1));
-  s.vl_warp = static_cast<int>(get_int(mj, "machine", "vl_warp", true, 0));
-  if (s.num_warps <= 0) throw DomainError("num_warps must be positive");
-  if (s.vl_warp < 0 || s.vl_warp >= s.num_warps) throw DomainError("vl_warp must lie in [0, num_warps)");
   if (!mj.contains("units") || !mj["units"].is_array()) throw DomainError("machine requires a \"units\" array");
+  auto get_name = [](const json& o, const char* what) {
+    if (!o.contains("name") || !o["name"].is_string())
+      throw DomainError(std::string(what) + " requires a string \"name\"");
+    return o["name"].get<std::string>();
+  };
+  auto index_of = [](const std::vector<LResource>& v, const std::string& name) {
+    for (size_t i = 0; i < v.size(); ++i)
+      if (v[i].name == name) return static_cast<int>(i);
+    return -1;
+  };
+  for (const json& uj : mj["units"]) {
+    if (!uj.is_object()) throw DomainError("unit entries must be objects");
+    require_keys(uj, "unit", {"name", "capacity"});
+    LResource u{get_name(uj, "unit"), get_int(uj, "unit", "capacity", true, 0)};
+    if (u.capacity <= 0) throw DomainError("unit \"" + u.name + "\" capacity must be positive");
+    if (index_of(s.units, u.name) >= 0) throw DomainError("duplicate unit \"" + u.name + "\"");
+    s.units.push_back(u);
+  }
+  if (mj.contains("memories")) {
+    if (!mj["memories"].is_array()) throw DomainError("\"memories\" must be an array");
+    for (const json& memj : mj["memories"]) {
+      if (!memj.is_object()) throw DomainError("memory entries must be objects");
+      require_keys(memj, "memory", {"name", "capacity"});
+      LResource m{get_name(memj, "memory"), get_int(memj, "memory", "capacity", true, 0)};
+      if (m.capacity < 0) throw DomainError("memory \"" + m.name + "\" capacity must be >= 0");
+      if (index_of(s.memories, m.name) >= 0) throw DomainError("duplicate memory \"" + m.name + "\"");
+      s.memories.push_back(m);
+    }
+  }
+  s.num_warps = static_cast<int>(get_int(mj, "machine", "num_warps", true, 1));
+  if (s.num_warps <= 0) throw DomainError("num_warps must be positive");
+  s.reg_limit = get_int(mj, "machine", "reg_limit", true, 0);
+  if (s.reg_limit < 0) throw DomainError("reg_limit must be >= 0");
+  s.vl_warp = static_cast<int>(get_int(mj, "machine", "vl_warp", true, 0));
+  if (s.vl_warp < 0 || s.vl_warp >= s.num_warps) throw DomainError("vl_warp must lie in [0, num_warps)");
 
   const json& gj = root["graph"];
   if (!gj.is_object()) throw DomainError("\"graph\" must be an object");
   require_keys(gj, "graph", {"nodes", "edges"});
-  if (!gj.contains("nodes") || !gj["nodes"].is_array() || gj["nodes"].empty())
-    throw DomainError("graph requires a nonempty \"nodes\" array");
+  if (!gj.contains("nodes") || !gj["nodes"].is_array()) throw DomainError("graph requires a \"nodes\" array");
+  if (gj["nodes"].empty()) throw DomainError("graph has no nodes");
   std::map<std::string, int> index;
   for (const json& nj : gj["nodes"]) {
     if (!nj.is_object()) throw DomainError("node entries must be objects");
@@ -69,13 +100,47 @@ void parse_problem(const std::string& text, LoweredSchedule& s) {
     if (index.count(n.id)) throw DomainError("duplicate node \"" + n.id + "\"");
     n.cycles = get_int(nj, "node", "cycles", true, 1);
     if (n.cycles < 1) throw DomainError("node \"" + n.id + "\" cycles must be >= 1");
-    n.warps_required = static_cast<int>(get_int(nj, "node", "warps_required", false, 1));
-    if (n.warps_required < 1) throw DomainError("warps_required must be >= 1");
+    n.rrt.assign(s.units.size(), std::vector<int64_t>(static_cast<size_t>(n.cycles), 0));
+    if (nj.contains("rrt")) {
+      if (!nj["rrt"].is_object()) throw DomainError("node \"" + n.id + "\" rrt must be an object");
+      for (auto it = nj["rrt"].begin(); it != nj["rrt"].end(); ++it) {
+        const int f = index_of(s.units, it.key());
+        if (f < 0) throw DomainError("node \"" + n.id + "\" uses undeclared unit \"" + it.key() + "\"");
+        if (!it->is_array()) throw DomainError("rrt rows must be arrays");
+        if (static_cast<int64_t>(it->size()) > n.cycles)
+          throw DomainError("node \"" + n.id + "\" rrt row for \"" + it.key() + "\" is longer than cycles");
+        for (size_t c = 0; c < it->size(); ++c) {
+          const json& cell = (*it)[c];
+          if (!cell.is_number_integer()) throw DomainError("rrt entries must be integers");
+          const int64_t v = cell.get<int64_t>();
+          if (v < 0) throw DomainError("rrt entries must be >= 0");
+          n.rrt[static_cast<size_t>(f)][c] = v;
+        }
+      }
+    }
+    n.regs = get_int(nj, "node", "regs", false, 0);
+    if (n.regs < 0) throw DomainError("node \"" + n.id + "\" regs must be >= 0");
+    n.footprint.assign(s.memories.size(), 0);
+    if (nj.contains("footprint")) {
+      if (!nj["footprint"].is_object()) throw DomainError("node \"" + n.id + "\" footprint must be an object");
+      for (auto it = nj["footprint"].begin(); it != nj["footprint"].end(); ++it) {
+        const int mi = index_of(s.memories, it.key());
+        if (mi < 0)
+          throw DomainError("node \"" + n.id + "\" footprint names undeclared memory \"" + it.key() + "\"");
+        if (!it->is_number_integer()) throw DomainError("footprint entries must be integers");
+        const int64_t v = it->get<int64_t>();
+        if (v < 0) throw DomainError("footprint entries must be >= 0");
+        n.footprint[static_cast<size_t>(mi)] = v;
+      }
+    }
     n.spill_cost = get_int(nj, "node", "spill_cost", false, 0);
+    if (n.spill_cost < 0) throw DomainError("spill_cost must be >= 0");
     if (nj.contains("variable_latency")) {
       if (!nj["variable_latency"].is_boolean()) throw DomainError("variable_latency must be a boolean");
       n.variable_latency = nj["variable_latency"].get<bool>();
     }
+    n.warps_required = static_cast<int>(get_int(nj, "node", "warps_required", false, 1));
+    if (n.warps_required < 1) throw DomainError("warps_required must be >= 1");
     index[n.id] = static_cast<int>(s.nodes.size());
     s.nodes.push_back(n);
   }
@@ -89,18 +154,25 @@ void parse_problem(const std::string& text, LoweredSchedule& s) {
         throw DomainError("edge requires string \"src\" and \"dst\"");
       auto si = index.find(ej["src"].get<std::string>());
       auto di = index.find(ej["dst"].get<std::string>());
-      if (si == index.end() || di == index.end()) throw DomainError("edge references an undeclared node");
+      if (si == index.end())
+        throw DomainError("edge references undeclared node \"" + ej["src"].get<std::string>() + "\"");
+      if (di == index.end())
+        throw DomainError("edge references undeclared node \"" + ej["dst"].get<std::string>() + "\"");
       e.src = si->second;
       e.dst = di->second;
       e.d = get_int(ej, "edge", "d", true, 0);
+      if (e.d < 0) throw DomainError("edge d must be >= 0");
       e.delta = static_cast<int>(get_int(ej, "edge", "delta", false, 0));
-      if (e.d < 0 || e.delta < 0) throw DomainError("edge d and delta must be >= 0");
-      if (ej.contains("blocking")) e.blocking = ej["blocking"].get<bool>();
+      if (e.delta < 0) throw DomainError("edge delta must be >= 0");
+      if (ej.contains("blocking")) {
+        if (!ej["blocking"].is_boolean()) throw DomainError("edge \"blocking\" must be a boolean");
+        e.blocking = ej["blocking"].get<bool>();
+      }
       s.edges.push_back(e);
     }
   }
-  for (const LNode& n : s.nodes)
-    if (n.warps_required > s.num_warps) throw DomainError("node \"" + n.id + "\" needs more warps than the machine has");
+  const std::vector<Violation> diags = validate_graph(s);
+  if (!diags.empty()) throw DomainError("invalid loop graph (" + diags[0].family + "): " + diags[0].message);
 }
 
 // ---- solution: solution_from_json (cli.cpp:96-155) + reconstruct (:161-168)
@@ -112,7 +184,11 @@ void parse_solution(const std::string& text, LoweredSchedule& s) {
     throw DomainError(std::string("invalid solution JSON: ") + e.what());
   }
   if (!j.is_object()) throw DomainError("solution JSON must be an object");
-  require_keys(j, "solution", {"I", "L", "M", "A", "streaming_depths", "search_report"});
+  for (auto it = j.begin(); it != j.end(); ++it) {
+    const std::string& k = it.key();
+    if (k != "I" && k != "L" && k != "M" && k != "A" && k != "streaming_depths" && k != "search_report")
+      throw DomainError("unknown solution key: " + k);
+  }
   if (!j.contains("I") || !j["I"].is_number_integer() || j["I"].get<int64_t>() < 1)
     throw DomainError("solution needs a positive integer I");
   if (!j.contains("L") || !j["L"].is_number_integer() || j["L"].get<int64_t>() < 1)
@@ -135,6 +211,13 @@ void parse_solution(const std::string& text, LoweredSchedule& s) {
     s.m[static_cast<size_t>(v)] = it.value().get<int64_t>();
   }
   if (j["M"].size() != n) throw DomainError("M must cover every node exactly once");
+  // fit in L against the graph as parsed (before the streaming rewrite), as
+  // solution_from_json does (cli.cpp:130-137)
+  for (size_t v = 0; v < n; ++v) {
+    const int64_t eff = std::max<int64_t>(1, s.nodes[v].cycles);
+    if (s.m[v] < 0 || s.m[v] > s.length - eff)
+      throw DomainError("M[" + s.nodes[v].id + "] = " + std::to_string(s.m[v]) + " does not fit in L");
+  }
   if (j.contains("A")) {
     if (!j["A"].is_object()) throw DomainError("A must be an object");
     for (auto it = j["A"].begin(); it != j["A"].end(); ++it) {
@@ -147,7 +230,7 @@ void parse_solution(const std::string& text, LoweredSchedule& s) {
   if (j.contains("streaming_depths")) {
     if (!j["streaming_depths"].is_object()) throw DomainError("streaming_depths must be an object");
     for (auto it = j["streaming_depths"].begin(); it != j["streaming_depths"].end(); ++it) {
-      if (!it.value().is_number_integer()) throw DomainError("streaming depth must be an integer");
+      if (!it.value().is_number_integer()) throw DomainError("streaming_depths entries must be integers");
       s.streaming_depths[it.key()] = it.value().get<int64_t>();
     }
   }
@@ -158,16 +241,13 @@ void parse_solution(const std::string& text, LoweredSchedule& s) {
     std::vector<int> indeg(n, 0);
     for (const LEdge& e : s.edges) ++indeg[static_cast<size_t>(e.dst)];
     for (size_t v = 0; v < n; ++v)
-      if (s.nodes[v].variable_latency && indeg[v] == 0) s.nodes[v].cycles = 0;
+      if (s.nodes[v].variable_latency && indeg[v] == 0) {
+        s.nodes[v].cycles = 0;
+        for (auto& row : s.nodes[v].rrt) row.clear();
+      }
   }
-  for (size_t v = 0; v < n; ++v) {
-    const int64_t eff = std::max<int64_t>(1, s.nodes[v].cycles);
-    if (s.m[v] < 0 || s.m[v] > s.length - eff)
-      throw DomainError("M[" + s.nodes[v].id + "] = " + std::to_string(s.m[v]) + " does not fit in L");
-    const int wr = std::max(1, s.nodes[v].warps_required);
-    if (s.a[v] < 0 || s.a[v] + wr > s.num_warps || s.a[v] % wr != 0)
-      throw DomainError("A[" + s.nodes[v].id + "] is not an aligned warp range of the machine");
-  }
+  // A's alignment and range are checked with the other families by
+  // validate_schedule (warp_uniqueness), which runs before anything indexes A
   s.copies = (s.length + s.ii - 1) / s.ii;
 }
 
@@ -590,12 +670,253 @@ void derive(LoweredSchedule& s) {
 
 }  // namespace
 
+LoweredSchedule parse(const std::string& problem_json, const std::string& solution_json) {
+  LoweredSchedule s;
+  parse_problem(problem_json, s);
+  parse_solution(solution_json, s);
+  return s;
+}
+
+std::string violations_json(const std::vector<Violation>& v) {
+  json arr = json::array();
+  for (const Violation& x : v) arr.push_back(json::array({x.family, x.message}));
+  return arr.dump();
+}
+
 LoweredSchedule lower(const std::string& problem_json, const std::string& solution_json) {
   LoweredSchedule s;
   parse_problem(problem_json, s);
   parse_solution(solution_json, s);
+  const std::vector<Violation> bad = validate_schedule(s);
+  if (!bad.empty()) {
+    std::string fams;
+    for (const Violation& v : bad)
+      if (fams.find(v.family) == std::string::npos) fams += (fams.empty() ? "" : ", ") + v.family;
+    throw DomainError("schedule rejected by validate_program (" + std::to_string(bad.size()) + " violation" +
+                      (bad.size() > 1 ? "s" : "") + " in " + fams + "; first: " + bad[0].family + ": " +
+                      bad[0].message + ")");
+  }
   derive(s);
   return s;
+}
+
+std::vector<Violation> validate_graph(const LoweredSchedule& s) {
+  std::vector<Violation> out;
+  const int n = static_cast<int>(s.nodes.size());
+  // the delta = 0 subgraph must be a DAG (iterative DFS, 0 new / 1 open / 2 done)
+  std::vector<std::vector<int>> adj(static_cast<size_t>(n));
+  for (const LEdge& e : s.edges)
+    if (e.delta == 0) adj[static_cast<size_t>(e.src)].push_back(e.dst);
+  std::vector<int> state(static_cast<size_t>(n), 0);
+  bool cycle = false;
+  for (int root = 0; root < n && !cycle; ++root) {
+    if (state[static_cast<size_t>(root)]) continue;
+    std::vector<std::pair<int, size_t>> stack{{root, 0}};
+    state[static_cast<size_t>(root)] = 1;
+    while (!stack.empty() && !cycle) {
+      auto& [v, i] = stack.back();
+      if (i < adj[static_cast<size_t>(v)].size()) {
+        const int w = adj[static_cast<size_t>(v)][i++];
+        if (state[static_cast<size_t>(w)] == 1) cycle = true;
+        else if (state[static_cast<size_t>(w)] == 0) {
+          state[static_cast<size_t>(w)] = 1;
+          stack.push_back({w, 0});
+        }
+      } else {
+        state[static_cast<size_t>(v)] = 2;
+        stack.pop_back();
+      }
+    }
+  }
+  if (cycle) out.push_back({"zero-delta-cycle", "dependence cycle with zero total iteration distance"});
+  for (const LNode& node : s.nodes) {
+    for (size_t f = 0; f < node.rrt.size(); ++f)
+      for (size_t c = 0; c < node.rrt[f].size(); ++c)
+        if (node.rrt[f][c] > s.units[f].capacity)
+          out.push_back({"rrt-exceeds-capacity", "node \"" + node.id + "\" reserves " +
+                                                     std::to_string(node.rrt[f][c]) + " of unit \"" + s.units[f].name +
+                                                     "\" (capacity " + std::to_string(s.units[f].capacity) + ")"});
+    if (node.warps_required > s.num_warps)
+      out.push_back({"warps-required-too-large", "node \"" + node.id + "\" requires " +
+                                                     std::to_string(node.warps_required) +
+                                                     " warps but the machine has " + std::to_string(s.num_warps)});
+  }
+  return out;
+}
+
+std::vector<Violation> validate_schedule(const LoweredSchedule& s) {
+  std::vector<Violation> out;
+  const size_t n = s.nodes.size();
+  const int64_t ii = s.ii, len = s.length;
+  const int64_t copies = std::max<int64_t>(1, (len + ii - 1) / ii);
+  const int64_t horizon = (copies - 1) * ii + len;
+  auto fmt = [](int64_t x) { return std::to_string(x); };
+  auto eff = [&](size_t v) { return std::max<int64_t>(1, s.nodes[v].cycles); };
+  auto wreq = [&](size_t v) { return std::max(1, s.nodes[v].warps_required); };
+  // expand_solution (sim.cpp:57-77): copy c of v issues at M(v) + c I
+  std::vector<std::vector<int64_t>> issue(n, std::vector<int64_t>(static_cast<size_t>(copies), -1));
+  std::vector<std::vector<std::vector<char>>> op(n);
+  for (size_t v = 0; v < n; ++v) {
+    op[v].assign(static_cast<size_t>(copies), std::vector<char>(static_cast<size_t>(horizon), 0));
+    for (int64_t c = 0; c < copies; ++c) {
+      const int64_t t = s.m[v] + c * ii;
+      if (t >= 0 && t < horizon) {
+        op[v][static_cast<size_t>(c)][static_cast<size_t>(t)] = 1;
+        issue[v][static_cast<size_t>(c)] = t;
+      }
+    }
+  }
+  // compute_live_tables (sim.cpp:29-55): backward fixed point
+  std::vector<std::vector<std::vector<char>>> live(n);
+  for (size_t v = 0; v < n; ++v) {
+    bool carries = false;
+    for (const LEdge& e : s.edges)
+      if (e.src == static_cast<int>(v) && e.delta > 0) carries = true;
+    live[v].assign(static_cast<size_t>(copies), std::vector<char>(static_cast<size_t>(horizon) + 1, 0));
+    for (int64_t c = 0; c < copies; ++c) {
+      auto& lv = live[v][static_cast<size_t>(c)];
+      lv[static_cast<size_t>(horizon)] = carries && c == copies - 1;
+      for (int64_t t = horizon; t >= 1; --t) {
+        const bool op_t = t < horizon && op[v][static_cast<size_t>(c)][static_cast<size_t>(t)];
+        bool use_t = false;
+        if (t < horizon)
+          for (const LEdge& e : s.edges) {
+            if (e.src != static_cast<int>(v)) continue;
+            const int64_t cc = c + e.delta;
+            if (cc < copies && op[static_cast<size_t>(e.dst)][static_cast<size_t>(cc)][static_cast<size_t>(t)])
+              use_t = true;
+          }
+        lv[static_cast<size_t>(t) - 1] = lv[static_cast<size_t>(t)] ? !op_t : use_t;
+      }
+    }
+  }
+  for (size_t v = 0; v < n; ++v)
+    for (int64_t c = 0; c < copies; ++c) {
+      const int64_t t = issue[v][static_cast<size_t>(c)];
+      if (t < 0) {
+        out.push_back({"uniqueness", "node " + s.nodes[v].id + " copy " + fmt(c) + " issues 0 times"});
+        continue;
+      }
+      const int64_t lo = c * ii, hi = c * ii + len - eff(v);
+      if (t < lo || t > hi)
+        out.push_back({"completion", "node " + s.nodes[v].id + " copy " + fmt(c) + " issues at " + fmt(t) +
+                                         " outside [" + fmt(lo) + ", " + fmt(hi) + "]"});
+    }
+  for (const LEdge& e : s.edges)
+    for (int64_t c = 0; c + e.delta < copies; ++c) {
+      const int64_t tu = issue[static_cast<size_t>(e.src)][static_cast<size_t>(c)];
+      const int64_t tv = issue[static_cast<size_t>(e.dst)][static_cast<size_t>(c + e.delta)];
+      if (tu < 0 || tv < 0) continue;
+      if (tv < tu + e.d)
+        out.push_back({"dependence", "edge " + s.nodes[static_cast<size_t>(e.src)].id + "->" +
+                                         s.nodes[static_cast<size_t>(e.dst)].id + ": consumer copy " +
+                                         fmt(c + e.delta) + " at " + fmt(tv) + " before " + fmt(tu) + "+" + fmt(e.d)});
+    }
+  // unit capacity over the whole horizon
+  std::vector<std::vector<int64_t>> occ(static_cast<size_t>(horizon), std::vector<int64_t>(s.units.size(), 0));
+  for (size_t v = 0; v < n; ++v)
+    for (int64_t c = 0; c < copies; ++c) {
+      const int64_t t = issue[v][static_cast<size_t>(c)];
+      if (t < 0) continue;
+      for (size_t f = 0; f < s.nodes[v].rrt.size() && f < s.units.size(); ++f)
+        for (size_t cyc = 0; cyc < s.nodes[v].rrt[f].size(); ++cyc)
+          if (t + static_cast<int64_t>(cyc) < horizon) occ[static_cast<size_t>(t) + cyc][f] += s.nodes[v].rrt[f][cyc];
+    }
+  for (int64_t t = 0; t < horizon; ++t)
+    for (size_t f = 0; f < s.units.size(); ++f)
+      if (occ[static_cast<size_t>(t)][f] > s.units[f].capacity)
+        out.push_back({"capacity", "unit " + s.units[f].name + " oversubscribed at cycle " + fmt(t) + ": " +
+                                       fmt(occ[static_cast<size_t>(t)][f]) + " > " + fmt(s.units[f].capacity)});
+  // memory footprints of live values
+  for (size_t mem = 0; mem < s.memories.size(); ++mem)
+    for (int64_t t = 0; t <= horizon; ++t) {
+      int64_t used = 0;
+      for (size_t v = 0; v < n; ++v) {
+        if (mem >= s.nodes[v].footprint.size()) continue;
+        for (int64_t c = 0; c < copies; ++c)
+          if (live[v][static_cast<size_t>(c)][static_cast<size_t>(t)]) used += s.nodes[v].footprint[mem];
+      }
+      if (used > s.memories[mem].capacity)
+        out.push_back({"memory", "memory " + s.memories[mem].name + " oversubscribed at cycle " + fmt(t) + ": " +
+                                     fmt(used) + " > " + fmt(s.memories[mem].capacity)});
+    }
+  // warp slots and the variable-latency warp
+  bool any_vl = false;
+  for (const LNode& nd : s.nodes) any_vl = any_vl || nd.variable_latency;
+  for (size_t v = 0; v < n; ++v) {
+    const int st = s.a[v], wr = wreq(v);
+    if (st < 0 || st % wr != 0 || st + wr > s.num_warps) {
+      out.push_back({"warp_uniqueness", "node " + s.nodes[v].id + " warp start " + fmt(st) +
+                                            " is not an aligned slot of width " + fmt(wr)});
+      continue;
+    }
+    if (!any_vl) continue;
+    const bool covers_vl = st <= s.vl_warp && s.vl_warp < st + wr;
+    if (s.nodes[v].variable_latency && st != s.vl_warp)
+      out.push_back({"variable_latency", "node " + s.nodes[v].id + " must issue from warp " + fmt(s.vl_warp)});
+    if (!s.nodes[v].variable_latency && covers_vl)
+      out.push_back({"variable_latency", "node " + s.nodes[v].id + " overlaps the reserved warp " + fmt(s.vl_warp)});
+  }
+  // per-warp register limit over live values
+  if (s.reg_limit > 0)
+    for (int w = 0; w < s.num_warps; ++w)
+      for (int64_t t = 0; t <= horizon; ++t) {
+        int64_t used = 0;
+        for (size_t v = 0; v < n; ++v) {
+          if (s.nodes[v].regs <= 0 || !(s.a[v] <= w && w < s.a[v] + wreq(v))) continue;
+          for (int64_t c = 0; c < copies; ++c)
+            if (live[v][static_cast<size_t>(c)][static_cast<size_t>(t)]) used += s.nodes[v].regs;
+        }
+        if (used > s.reg_limit)
+          out.push_back({"register_limit", "warp " + fmt(w) + " over the register limit at cycle " + fmt(t) + ": " +
+                                               fmt(used) + " > " + fmt(s.reg_limit)});
+      }
+  // cross-warp transfers and blocking waits: nothing else may occupy the
+  // consumer's warps at the receive / wait point
+  auto overlap = [](int a, int wa, int b, int wb) { return a < b + wb && b < a + wa; };
+  auto isolated = [&](size_t v, int64_t at, const std::string& family, const std::string& why) {
+    for (size_t o = 0; o < n; ++o) {
+      if (o == v || s.nodes[o].cycles <= 0) continue;
+      if (!overlap(s.a[v], wreq(v), s.a[o], wreq(o))) continue;
+      const int64_t lo = std::max<int64_t>(0, at - s.nodes[o].cycles + 1), hi = std::min(at, horizon - 1);
+      for (int64_t c = 0; c < copies; ++c) {
+        const int64_t to = issue[o][static_cast<size_t>(c)];
+        if (to >= lo && to <= hi)
+          out.push_back({family, "node " + s.nodes[o].id + " occupies the warps of " + s.nodes[v].id + " at cycle " +
+                                     fmt(at) + " " + why});
+      }
+    }
+  };
+  for (const LEdge& e : s.edges) {
+    if (e.src == e.dst) continue;
+    const size_t u = static_cast<size_t>(e.src), v = static_cast<size_t>(e.dst);
+    const bool cross = s.a[u] != s.a[v] || wreq(u) != wreq(v);
+    const int64_t spill = s.nodes[u].spill_cost;
+    if (cross && spill > 0) {
+      for (int64_t c = 0; c + e.delta < copies; ++c) {
+        const int64_t tu = issue[u][static_cast<size_t>(c)], tv = issue[v][static_cast<size_t>(c + e.delta)];
+        if (tu < 0 || tv < 0) continue;
+        if (tv >= tu + e.d && tv < tu + e.d + spill)
+          out.push_back({"spill", "edge " + s.nodes[u].id + "->" + s.nodes[v].id + ": consumer copy " +
+                                      fmt(c + e.delta) + " at " + fmt(tv) + " inside the transfer window [" +
+                                      fmt(tu + e.d) + ", " + fmt(tu + e.d + spill) + ")"});
+      }
+      for (int64_t c = 0; c + e.delta < copies; ++c) {
+        const int64_t tu = issue[u][static_cast<size_t>(c)];
+        if (tu < 0) continue;
+        const int64_t recv = tu + e.d + spill - 1;
+        if (recv >= horizon) continue;
+        isolated(v, recv, "spill_sync", "(transfer receive point)");
+      }
+    }
+    if (e.blocking)
+      for (int64_t c = 0; c + e.delta < copies; ++c) {
+        const int64_t tv = issue[v][static_cast<size_t>(c + e.delta)];
+        if (tv < 0) continue;
+        isolated(v, tv, "concurrency", "(blocked on " + s.nodes[u].id + ")");
+      }
+  }
+  return out;
 }
 
 std::string describe(const LoweredSchedule& s) {

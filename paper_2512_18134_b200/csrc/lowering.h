@@ -40,6 +40,14 @@ struct LNode {
   int warps_required = 1;
   bool variable_latency = false;
   int64_t spill_cost = 0;
+  int64_t regs = 0;
+  std::vector<std::vector<int64_t>> rrt;  // [unit][cycle], dense (empty rows once streamed)
+  std::vector<int64_t> footprint;         // by memory index, dense
+};
+
+struct LResource {
+  std::string name;
+  int64_t capacity = 0;
 };
 
 struct LEdge {
@@ -53,8 +61,10 @@ struct LoweredSchedule {
   // problem
   std::vector<LNode> nodes;
   std::vector<LEdge> edges;
+  std::vector<LResource> units, memories;
   int num_warps = 1;
   int vl_warp = 0;
+  int64_t reg_limit = 0;
   // solution
   int64_t ii = 1, length = 1, copies = 1;
   std::vector<int64_t> m;      // M by node
@@ -67,9 +77,36 @@ struct LoweredSchedule {
   TwfaDevicePlan plan{};
 };
 
-// Parses and lowers. Throws DomainError on malformed documents or schedules
-// the B200 executor cannot realize.
+// One violated constraint family of the reference's checker.
+struct Violation {
+  std::string family, message;
+};
+
+// validate_graph (ir.cpp:231-276) restated: zero-delta cycles, RRT rows over
+// a unit's capacity, warps_required over the machine.
+std::vector<Violation> validate_graph(const LoweredSchedule& s);
+
+// validate_program (sim.cpp:79-311) restated over the tables the solution
+// expands to (expand_solution, sim.cpp:57-77): completion window,
+// dependence, unit capacity, memory footprint of live values, aligned warp
+// slots, the variable-latency warp, the per-warp register limit, spill
+// windows, spill receive isolation and blocking isolation. Empty = valid.
+std::vector<Violation> validate_schedule(const LoweredSchedule& s);
+
+// Parses and lowers. Throws DomainError on malformed documents, on any
+// violation validate_graph / validate_schedule report (the reference's
+// checker must accept the schedule), and on schedules the B200 executor
+// cannot realize.
 LoweredSchedule lower(const std::string& problem_json, const std::string& solution_json);
+
+// Parses both documents (the problem through validate_graph, the solution
+// through solution_from_json + reconstruct) without validating the schedule
+// or lowering it.
+LoweredSchedule parse(const std::string& problem_json, const std::string& solution_json);
+
+// validate_schedule as the JSON list [[family, message], ...] the
+// reference's Python binding returns (bindings/module.cpp:176-184).
+std::string violations_json(const std::vector<Violation>& v);
 
 // JSON description of the plan: I, L, copies, per-node stage/slot/warp,
 // per-warp programs, ring depths.

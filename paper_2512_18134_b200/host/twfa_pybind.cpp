@@ -105,4 +105,20 @@ PYBIND11_MODULE(_twfa, m) {
       "describe",
       [](const std::string& problem, const std::string& solution) { return Plan(problem, solution).describe(); },
       py::arg("problem"), py::arg("solution"));
+  // same signature and result as _weftsched.validate (module.cpp:176-184,
+  // 241-243): a list of (family, message) tuples, empty when exact
+  m.def(
+      "validate",
+      [](const std::string& problem, const std::string& solution) {
+        size_t need = 0;
+        check(twfa_schedule_validate(problem.c_str(), solution.c_str(), nullptr, 0, &need));
+        std::string buf(need, '\0');
+        check(twfa_schedule_validate(problem.c_str(), solution.c_str(), buf.data(), buf.size(), &need));
+        py::list out;
+        for (auto v : py::module_::import("json").attr("loads")(py::str(buf.c_str())))
+          out.append(py::make_tuple(v[py::int_(0)], v[py::int_(1)]));
+        return out;
+      },
+      py::arg("problem"), py::arg("solution"),
+      "List of (family, message) violations; empty when the solution is exact.");
 }

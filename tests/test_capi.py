@@ -40,7 +40,7 @@ def test_error_codes_and_messages(twfa):
     need = ctypes.c_size_t()
     assert L.twfa_plan_raw(h, None, 0, ctypes.byref(need)) == 0 and need.value > 0
     L.twfa_plan_destroy(h)
-    assert L.twfa_abi_version() == 1
+    assert L.twfa_abi_version() == 2
 
 
 def test_plan_survives_threads(twfa):
@@ -105,8 +105,12 @@ def test_pybind_module_mirrors_reference_conventions(twfa):
     assert d["I"] == json.loads(sol)["I"] and d == twfa.Plan(prob, sol).describe()
     with pytest.raises(ValueError, match="machine"):
         m.Plan("{}", "{}")
-    with pytest.raises(ValueError, match="unknown key"):
+    with pytest.raises(ValueError, match="unknown solution key"):
         m.Plan(prob, json.dumps(dict(json.loads(sol), bogus=1)))
+    assert m.validate(prob, sol) == []
+    bad = json.loads(sol)
+    bad["A"]["S0"] = 3
+    assert [f for f, _ in m.validate(prob, json.dumps(bad))] == ["variable_latency"]
 
 
 def test_fa_bwd_entry_points_check_arguments_without_a_gpu(twfa):

@@ -104,12 +104,12 @@ def test_fa_ring_depth_follows_solution(twfa):
 
 @pytest.mark.parametrize("mutate,msg", [
     (lambda s: s.update(I=0), "positive integer I"),
-    (lambda s: s.update(bogus=1), "unknown key"),
+    (lambda s: s.update(bogus=1), "unknown solution key"),
     (lambda s: s["M"].pop("S0"), "cover every node"),
     (lambda s: s["M"].update(S0=99), "does not fit in L"),
-    (lambda s: s["A"].update(MX0=3), "aligned warp range"),
-    (lambda s: s["A"].update(EX0=8, MX0=4), "share a warpgroup"),
-    (lambda s: s["A"].update(S0=16), "aligned warp range"),
+    (lambda s: s["A"].update(MX0=3), "warp_uniqueness.*aligned slot"),
+    (lambda s: s["A"].update(EX0=8, MX0=4), "register_limit|share a warpgroup"),
+    (lambda s: s["A"].update(S0=16), "warp_uniqueness.*aligned slot"),
     (lambda s: s.update(streaming_depths={"LDK": 1, "LDV": 1}), "shallower than its consumer lag|cannot run ahead"),
 ])
 def test_bad_or_unrealizable_solutions_are_rejected(twfa, mutate, msg):
@@ -180,10 +180,10 @@ def test_fa_bwd_plan_roles_follow_the_solver(twfa):
 
 
 @pytest.mark.parametrize("mutate,msg", [
-    (lambda s: s["A"].update(DS=s["A"]["RD"]), "own warpgroup"),
-    (lambda s: s["A"].update(DQ=14), "issue from one warp"),
-    (lambda s: s["A"].update(RD=12), "cannot be inside"),
-    (lambda s: s["M"].update(DS=s["M"]["EXB"]), "violates dependence"),
+    (lambda s: s["A"].update(DS=s["A"]["RD"]), "spill|own warpgroup"),
+    (lambda s: s["A"].update(DQ=14), "variable_latency|issue from one warp"),
+    (lambda s: s["A"].update(RD=12), "variable_latency|cannot be inside"),
+    (lambda s: s["M"].update(DS=s["M"]["EXB"]), "dependence"),
 ])
 def test_fa_bwd_unrealizable_solutions_are_rejected(twfa, mutate, msg):
     prob, sol = twfa.load_schedule("fa_bwd")
