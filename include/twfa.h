@@ -93,8 +93,13 @@ int twfa_fa_fwd_traced(const twfa_plan* plan, const void* q, const void* k, cons
                        uint32_t* trace, uint32_t cap, void* stream);
 
 /* Host-buffer form of twfa_fa_fwd for CPU callers (the reference's C++ host,
- * the CLI): copies Q, K, V to the device, runs, copies O (and lse) back,
- * synchronously. Device staging buffers are cached per thread. */
+ * the CLI, ctypes): synchronous; on return O (and lse) are in the caller's
+ * buffers. The (b, h) pairs are streamed in chunks through a pipeline: host
+ * -> device copies of chunk i + 1 and device -> host copies of chunk i - 1
+ * overlap the kernel on chunk i (three CUDA streams). Page-locked caller
+ * buffers (cudaMallocHost / cudaHostRegister) are DMA'd directly; pageable
+ * ones are staged through pinned slots by host threads. Device buffers,
+ * pinned slots and streams are cached per calling thread. */
 int twfa_fa_fwd_host(const twfa_plan* plan, const uint16_t* q, const uint16_t* k, const uint16_t* v,
                      uint16_t* o, float* lse, int B, int H, int S, int D, int causal, float softmax_scale);
 

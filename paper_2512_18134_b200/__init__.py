@@ -188,18 +188,29 @@ def fa_fwd(plan, q, k, v, causal=False, softmax_scale=None, return_lse=False, ou
     return (o, lse) if return_lse else o
 
 
-def fa_fwd_host(plan, q, k, v, causal=False, softmax_scale=None, return_lse=False):
-    """Host-buffer form (numpy uint16 bf16 bit patterns, [B, H, S, 128])."""
+def fa_fwd_host(plan, q, k, v, causal=False, softmax_scale=None, return_lse=False, out=None, lse_out=None):
+    """Host-buffer form (twfa_fa_fwd_host): numpy uint16 arrays of bf16 bit
+    patterns, [B, H, S, 128]. Synchronous; the pairs stream through the
+    library's chunked copy/compute pipeline. Page-locked buffers (e.g. numpy
+    views of torch pin_memory tensors) are DMA'd directly -- pass `out` (and
+    `lse_out`) page-locked too to keep the whole call on that path."""
     import numpy as np
     q, k, v = (np.ascontiguousarray(x, dtype=np.uint16) for x in (q, k, v))
+    if q.shape != k.shape or q.shape != v.shape or q.ndim != 4:
+        raise ValueError("q, k, v must share shape [B, H, S, D]")
     B, H, S, D = q.shape
     scale = float(softmax_scale) if softmax_scale is not None else 1.0 / math.sqrt(D)
-    o = np.empty_like(q)
-    lse = np.empty((B, H, S), dtype=np.float32) if return_lse else None
+    if out is not None and (out.shape != q.shape or out.dtype != np.uint16 or not out.flags.c_contiguous):
+        raise ValueError("out must be a contiguous uint16 array of q's shape")
+    o = out if out is not None else np.empty_like(q)
+    if lse_out is not None and (lse_out.shape != (B, H, S) or lse_out.dtype != np.float32
+                                or not lse_out.flags.c_contiguous):
+        raise ValueError("lse_out must be a contiguous float32 [B, H, S] array")
+    lse = lse_out if lse_out is not None else (np.empty((B, H, S), dtype=np.float32) if return_lse else None)
     p = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
     _check(lib().twfa_fa_fwd_host(plan.handle, p(q), p(k), p(v), p(o), p(lse) if lse is not None else None,
                                   B, H, S, D, int(bool(causal)), scale))
-    return (o, lse) if return_lse else o
+    return (o, lse) if (return_lse or lse_out is not None) else o
 
 
 def fa_bwd(plan, q, k, v, o, dout, lse, causal=False, softmax_scale=None, workspace=None):

@@ -11,6 +11,7 @@
 #include <mutex>
 #include <queue>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <vector>
 
@@ -350,22 +351,175 @@ int fa_bwd_impl(const twfa_plan* plan, const void* q, const void* k, const void*
   return TWFA_OK;
 }
 
-struct HostStaging {
-  void* buf = nullptr;
-  size_t bytes = 0;
-  ~HostStaging() {
-    if (buf) cudaFree(buf);
+// Host-buffer pipeline of twfa_fa_fwd_host. The (b, h) pairs are
+// independent, so the call streams them in chunks: the caller's (pageable)
+// Q, K, V of chunk i are copied by host threads into a pinned staging slot,
+// DMA'd to the device on a copy stream, computed on a compute stream, and O
+// returns through a pinned slot on a third stream while chunk i + 1 is being
+// staged, so host copies, PCIe transfers in both directions and the kernel
+// overlap. Resources (device buffers for the whole problem, kStages pinned
+// slots, streams, events) are cached per calling thread and grow on demand.
+constexpr int kStages = 3;
+constexpr size_t kChunkBytes = 64u << 20;  // per tensor per chunk
+
+// memcpy split over host threads (the pageable <-> pinned copies are the
+// host-side bound of the pipeline)
+void parallel_copy(void* dst, const void* src, size_t bytes) {
+  const size_t kMin = 4u << 20;
+  unsigned nt = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  nt = static_cast<unsigned>(std::min<size_t>(nt, std::max<size_t>(1, bytes / kMin)));
+  if (nt <= 1) {
+    std::memcpy(dst, src, bytes);
+    return;
   }
-  void* get(size_t n) {
-    if (n > bytes) {
-      if (buf) cudaFree(buf);
-      buf = nullptr;
-      check(cudaMalloc(&buf, n), "cudaMalloc");
-      bytes = n;
+  std::vector<std::thread> ts;
+  const size_t part = (bytes + nt - 1) / nt;
+  for (unsigned t = 0; t < nt; ++t) {
+    const size_t a = t * part, b = std::min(bytes, a + part);
+    if (a >= b) break;
+    ts.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, b - a); });
+  }
+  for (auto& t : ts) t.join();
+}
+
+struct HostPipeline {
+  int dev = -1;
+  void* dbuf = nullptr;  // q, k, v, o (+ lse) of the whole problem
+  size_t dbytes = 0;
+  void* pin[kStages] = {};  // per slot: q, k, v chunk in, o chunk out, lse chunk out
+  size_t pin_bytes = 0;
+  cudaStream_t s_h2d = nullptr, s_cmp = nullptr, s_d2h = nullptr;
+  cudaEvent_t ev_in[kStages] = {}, ev_done[kStages] = {}, ev_out[kStages] = {};
+  ~HostPipeline() { release(); }
+  void release() {
+    if (dev < 0) return;
+    cudaSetDevice(dev);
+    cudaDeviceSynchronize();
+    if (dbuf) cudaFree(dbuf);
+    for (int i = 0; i < kStages; ++i) {
+      if (pin[i]) cudaFreeHost(pin[i]);
+      if (ev_in[i]) cudaEventDestroy(ev_in[i]);
+      if (ev_done[i]) cudaEventDestroy(ev_done[i]);
+      if (ev_out[i]) cudaEventDestroy(ev_out[i]);
+      pin[i] = nullptr;
+      ev_in[i] = ev_done[i] = ev_out[i] = nullptr;
     }
-    return buf;
+    for (cudaStream_t st : {s_h2d, s_cmp, s_d2h})
+      if (st) cudaStreamDestroy(st);
+    s_h2d = s_cmp = s_d2h = nullptr;
+    dbuf = nullptr;
+    dbytes = pin_bytes = 0;
+    dev = -1;
+  }
+  void prepare(size_t need_dev, size_t need_pin) {
+    int cur = 0;
+    check(cudaGetDevice(&cur), "cudaGetDevice");
+    if (dev != cur) {
+      release();
+      dev = cur;
+      check(cudaStreamCreateWithFlags(&s_h2d, cudaStreamNonBlocking), "cudaStreamCreate");
+      check(cudaStreamCreateWithFlags(&s_cmp, cudaStreamNonBlocking), "cudaStreamCreate");
+      check(cudaStreamCreateWithFlags(&s_d2h, cudaStreamNonBlocking), "cudaStreamCreate");
+      for (int i = 0; i < kStages; ++i) {
+        check(cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming), "cudaEventCreate");
+        check(cudaEventCreateWithFlags(&ev_done[i], cudaEventDisableTiming), "cudaEventCreate");
+        check(cudaEventCreateWithFlags(&ev_out[i], cudaEventDisableTiming), "cudaEventCreate");
+      }
+    }
+    if (need_dev > dbytes) {
+      if (dbuf) cudaFree(dbuf);
+      dbuf = nullptr;
+      dbytes = 0;
+      check(cudaMalloc(&dbuf, need_dev), "cudaMalloc");
+      dbytes = need_dev;
+    }
+    if (need_pin > pin_bytes) {
+      for (int i = 0; i < kStages; ++i) {
+        if (pin[i]) cudaFreeHost(pin[i]);
+        pin[i] = nullptr;
+      }
+      pin_bytes = 0;
+      for (int i = 0; i < kStages; ++i) check(cudaMallocHost(&pin[i], need_pin), "cudaMallocHost");
+      pin_bytes = need_pin;
+    }
   }
 };
+
+int fa_fwd_host_impl(const twfa_plan* plan, const uint16_t* q, const uint16_t* k, const uint16_t* v, uint16_t* o,
+                     float* lse, int B, int H, int S, int D, int causal, float scale) {
+  if (!q || !k || !v || !o) throw twfa::UsageError("NULL host buffer");
+  if (B < 1 || H < 1 || S < 1 || D != 128) throw twfa::UsageError("unsupported shape");
+  thread_local HostPipeline hp;
+  // page-locked caller buffers (cudaMallocHost / cudaHostRegister, e.g.
+  // torch pin_memory) are DMA'd directly; pageable ones go through the
+  // pinned staging slots
+  auto pinned = [](const void* p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+  };
+  const bool direct = pinned(q) && pinned(k) && pinned(v) && pinned(o) && (!lse || pinned(lse));
+  const size_t pairs = static_cast<size_t>(B) * H;
+  const size_t pb = static_cast<size_t>(S) * D * 2;  // bytes of one pair of one tensor
+  const size_t lb = static_cast<size_t>(S) * 4;      // lse bytes of one pair
+  const size_t chunk = std::max<size_t>(1, std::min(pairs, kChunkBytes / pb));
+  const size_t tb = pairs * pb;
+  // device layout: q | k | v | o | lse, each 256-byte aligned (TMA needs 16)
+  auto up = [](size_t x) { return (x + 255) & ~static_cast<size_t>(255); };
+  const size_t off_k = up(tb), off_v = off_k + up(tb), off_o = off_v + up(tb), off_l = off_o + up(tb);
+  const size_t need_dev = off_l + (lse ? up(pairs * lb) : 0);
+  // pinned slot layout: q | k | v | o | lse of one chunk
+  const size_t cb = chunk * pb, cl = chunk * lb;
+  const size_t need_pin = direct ? 0 : 4 * cb + (lse ? cl : 0);
+  hp.prepare(need_dev, need_pin);
+  uint8_t* d = static_cast<uint8_t*>(hp.dbuf);
+  const size_t nchunks = (pairs + chunk - 1) / chunk;
+  const uint8_t* src[3] = {reinterpret_cast<const uint8_t*>(q), reinterpret_cast<const uint8_t*>(k),
+                           reinterpret_cast<const uint8_t*>(v)};
+  const size_t doff[3] = {0, off_k, off_v};
+  auto drain = [&](size_t j) {  // chunk j's O (and lse) from its pinned slot to the caller
+    const int sl = static_cast<int>(j % kStages);
+    const size_t p0 = j * chunk, np = std::min(chunk, pairs - p0);
+    check(cudaEventSynchronize(hp.ev_out[sl]), "D2H o");
+    if (direct) return;
+    uint8_t* pin = static_cast<uint8_t*>(hp.pin[sl]);
+    parallel_copy(reinterpret_cast<uint8_t*>(o) + p0 * pb, pin + 3 * cb, np * pb);
+    if (lse) std::memcpy(reinterpret_cast<uint8_t*>(lse) + p0 * lb, pin + 4 * cb, np * lb);
+  };
+  for (size_t i = 0; i < nchunks; ++i) {
+    const int sl = static_cast<int>(i % kStages);
+    const size_t p0 = i * chunk, np = std::min(chunk, pairs - p0);
+    // the slot's previous chunk (i - kStages) has returned its O and left
+    // the slot's inputs (its H2D completed before its kernel ran)
+    if (i >= static_cast<size_t>(kStages)) drain(i - kStages);
+    uint8_t* pin = static_cast<uint8_t*>(hp.pin[sl]);
+    if (!direct)
+      for (int t = 0; t < 3; ++t) parallel_copy(pin + t * cb, src[t] + p0 * pb, np * pb);
+    for (int t = 0; t < 3; ++t)
+      check(cudaMemcpyAsync(d + doff[t] + p0 * pb, direct ? src[t] + p0 * pb : pin + t * cb, np * pb,
+                            cudaMemcpyHostToDevice, hp.s_h2d),
+            "H2D");
+    check(cudaEventRecord(hp.ev_in[sl], hp.s_h2d), "cudaEventRecord");
+    check(cudaStreamWaitEvent(hp.s_cmp, hp.ev_in[sl], 0), "cudaStreamWaitEvent");
+    // chunk i as a [1, np, S, 128] problem: the pairs are independent
+    const int rc = fa_fwd_impl(plan, d + p0 * pb, d + off_k + p0 * pb, d + off_v + p0 * pb, d + off_o + p0 * pb,
+                               lse ? reinterpret_cast<float*>(d + off_l + p0 * lb) : nullptr, 1, static_cast<int>(np),
+                               S, D, causal, scale, nullptr, 0, hp.s_cmp);
+    if (rc != TWFA_OK) return rc;
+    check(cudaEventRecord(hp.ev_done[sl], hp.s_cmp), "cudaEventRecord");
+    check(cudaStreamWaitEvent(hp.s_d2h, hp.ev_done[sl], 0), "cudaStreamWaitEvent");
+    uint8_t* o_dst = direct ? reinterpret_cast<uint8_t*>(o) + p0 * pb : pin + 3 * cb;
+    uint8_t* l_dst = direct ? reinterpret_cast<uint8_t*>(lse) + p0 * lb : pin + 4 * cb;
+    check(cudaMemcpyAsync(o_dst, d + off_o + p0 * pb, np * pb, cudaMemcpyDeviceToHost, hp.s_d2h), "D2H o");
+    if (lse) check(cudaMemcpyAsync(l_dst, d + off_l + p0 * lb, np * lb, cudaMemcpyDeviceToHost, hp.s_d2h), "D2H lse");
+    check(cudaEventRecord(hp.ev_out[sl], hp.s_d2h), "cudaEventRecord");
+  }
+  for (size_t j = nchunks > static_cast<size_t>(kStages) ? nchunks - kStages : 0; j < nchunks; ++j) drain(j);
+  return TWFA_OK;
+}
 
 }  // namespace
 
@@ -452,28 +606,7 @@ int twfa_fa_fwd_traced(const twfa_plan* plan, const void* q, const void* k, cons
 
 int twfa_fa_fwd_host(const twfa_plan* plan, const uint16_t* q, const uint16_t* k, const uint16_t* v, uint16_t* o,
                      float* lse, int B, int H, int S, int D, int causal, float softmax_scale) {
-  return guarded([&] {
-    if (!q || !k || !v || !o) throw twfa::UsageError("NULL host buffer");
-    if (B < 1 || H < 1 || S < 1 || D != 128) throw twfa::UsageError("unsupported shape");
-    thread_local HostStaging staging;
-    const size_t elems = static_cast<size_t>(B) * H * S * D;
-    const size_t tb = elems * 2;
-    const size_t lb = lse ? static_cast<size_t>(B) * H * S * 4 : 0;
-    uint8_t* base = static_cast<uint8_t*>(staging.get(4 * tb + lb + 64));
-    void* dq = base;
-    void* dk = base + tb;
-    void* dv = base + 2 * tb;
-    void* dout = base + 3 * tb;
-    float* dl = lse ? reinterpret_cast<float*>(base + 4 * tb) : nullptr;
-    check(cudaMemcpy(dq, q, tb, cudaMemcpyHostToDevice), "H2D q");
-    check(cudaMemcpy(dk, k, tb, cudaMemcpyHostToDevice), "H2D k");
-    check(cudaMemcpy(dv, v, tb, cudaMemcpyHostToDevice), "H2D v");
-    int rc = fa_fwd_impl(plan, dq, dk, dv, dout, dl, B, H, S, D, causal, softmax_scale, nullptr, 0, nullptr);
-    if (rc != TWFA_OK) return rc;
-    check(cudaMemcpy(o, dout, tb, cudaMemcpyDeviceToHost), "D2H o");
-    if (lse) check(cudaMemcpy(lse, dl, lb, cudaMemcpyDeviceToHost), "D2H lse");
-    return TWFA_OK;
-  });
+  return guarded([&] { return fa_fwd_host_impl(plan, q, k, v, o, lse, B, H, S, D, causal, softmax_scale); });
 }
 
 int twfa_fa_bwd_workspace_size(int B, int H, int S, int D, size_t* bytes) {

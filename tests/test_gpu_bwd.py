@@ -3,8 +3,9 @@ against the fp64-accumulated CPU oracle (oracle_attention_bwd) on the same
 bf16-rounded inputs and the kernel's own forward O and LSE.
 
 Tolerance: bf16 gradients of an fp32-accumulated backward whose P^T and dS^T
-enter the GEMMs in bf16 (N(0,1) inputs, d = 128): max |err| <= 2e-2 x max|ref|
-and mean |err| <= 2e-3 x max|ref| per gradient. The bf16 rounding of the
+enter the GEMMs in bf16 (N(0,1) inputs, d = 128): max |err| <= 1.5e-2 x max|ref|
+and mean |err| <= 1e-3 x max|ref| per gradient, about 3x the observed errors
+(tools/gpu/observed_errors.py: 4.8e-3, 2.8e-4). The bf16 rounding of the
 result alone is 2^-9 relative; bf16 P and dS add a comparable relative error
 per term, averaged over >= 128 terms."""
 import numpy as np
@@ -15,7 +16,7 @@ from tests import oracle_lib
 
 pytestmark = pytest.mark.gpu
 
-TOL_MAX, TOL_MEAN = 2e-2, 2e-3
+TOL_MAX, TOL_MEAN = 1.5e-2, 1e-3  # ~3x observed (tools/gpu/observed_errors.py: 4.8e-3, 2.8e-4)
 
 
 @pytest.fixture(scope="module")

@@ -1,11 +1,20 @@
 """FA-forward parity on the B200: the sm_100a kernel (through the C ABI) against
 the fp32 CPU oracle on the same bf16-rounded inputs.
 
-Tolerance (bf16 output of an fp32-accumulated attention with P rounded to bf16
-before the PV GEMM, N(0,1) inputs, d = 128): max |err| <= 2e-2 and mean |err|
-<= 2e-3 on O; |err| <= 1e-2 on the natural-log LSE. The bf16 rounding of O
-alone contributes up to 2^-9 relative (~4e-3 at |O| ~ 1) and the bf16 P adds
-a comparable relative error per term, averaged over >= 128 keys.
+Tolerances (bf16 output of an fp32-accumulated attention with P rounded to
+bf16 before the PV GEMM, d = 128), relative to max(1, max |O_ref|):
+max |err| <= 5e-3, mean |err| <= 5e-4 on O; |err| <= 2e-5 on the natural-log
+LSE (the row sum is accumulated in fp32 from the unrounded P). These are about
+3x the errors observed on N(0, 1) inputs (tools/gpu/observed_errors.py: O
+relative max 2.0e-3, mean 1.9e-4; LSE 1.9e-6, 10x on LSE): the
+bf16 rounding of O alone contributes up to 2^-9 relative, and the bf16 P a
+comparable relative error per term, averaged over >= 128 keys.
+
+The adversarial cases drive the conditional rescale of the online softmax
+(the running max only moves when a row's max grows by more than 2^8,
+fa_fwd_kernel.cuh kRescaleLog2): a late jump of the row max far above that
+threshold, a large softmax scale (the max moves on most K/V tiles), constant
+rows (every score equal), and rows whose max sits in the first key.
 """
 import numpy as np
 import pytest
@@ -15,7 +24,7 @@ from tests import oracle_lib
 
 pytestmark = pytest.mark.gpu
 
-TOL_MAX, TOL_MEAN, TOL_LSE = 2e-2, 2e-3, 1e-2
+TOL_MAX, TOL_MEAN, TOL_LSE = 5e-3, 5e-4, 2e-5
 
 
 @pytest.fixture(scope="module")
@@ -28,20 +37,72 @@ def _inputs(B, H, S, D, seed):
     return [torch.randn(B, H, S, D, generator=g).to(torch.bfloat16) for _ in range(3)]
 
 
-def _check(twfa, plan, B, H, S, causal, seed, scale=None):
-    q, k, v = _inputs(B, H, S, 128, seed)
+def _check_qkv(twfa, plan, q, k, v, causal, scale=None):
     dev = torch.device("cuda:0")
     o, lse = twfa.fa_fwd(plan, q.to(dev), k.to(dev), v.to(dev), causal=causal, softmax_scale=scale,
                          return_lse=True)
     torch.cuda.synchronize()
     ro, rl = oracle_lib.attention(q.float().numpy(), k.float().numpy(), v.float().numpy(), causal=causal,
                                   scale=scale)
-    err = np.abs(o.float().cpu().numpy() - ro)
+    of = o.float().cpu().numpy()
+    assert np.isfinite(of).all()
+    mag = max(1.0, float(np.abs(ro).max()))
+    err = np.abs(of - ro) / mag
     lerr = np.abs(lse.cpu().numpy() - rl)
-    assert np.isfinite(o.float().cpu().numpy()).all()
     assert err.max() <= TOL_MAX, f"max err {err.max()}"
     assert err.mean() <= TOL_MEAN, f"mean err {err.mean()}"
-    assert lerr.max() <= TOL_LSE, f"lse err {lerr.max()}"
+    assert lerr.max() <= TOL_LSE * max(1.0, float(np.abs(rl).max())), f"lse err {lerr.max()}"
+    return err, lerr
+
+
+def _check(twfa, plan, B, H, S, causal, seed, scale=None):
+    q, k, v = _inputs(B, H, S, 128, seed)
+    return _check_qkv(twfa, plan, q, k, v, causal, scale)
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_late_row_max_jump_far_above_rescale_threshold(twfa, plan, causal):
+    # keys in the last K/V tiles score ~10x higher: every row's max jumps by
+    # far more than 2^8 (log2 units) long after the running max settled, so
+    # the correction warpgroup must rescale O and l exactly once, late
+    q, k, v = _inputs(1, 2, 1024, 128, 21)
+    k[:, :, 900:] *= 10.0
+    _check_qkv(twfa, plan, q, k, v, causal)
+
+
+def test_large_softmax_scale_moves_the_max_every_tile(twfa, plan):
+    # scale 2.0: scores ~ N(0, 2 sqrt(128)), the row max moves past the
+    # threshold on many K/V tiles (many corrections per row)
+    q, k, v = _inputs(1, 2, 1024, 128, 22)
+    _check_qkv(twfa, plan, q, k, v, False, scale=2.0)
+
+
+def test_rising_scores_rescale_on_every_tile(twfa, plan):
+    # keys whose scores rise tile by tile: every K/V tile moves every row's max
+    q, k, v = _inputs(1, 1, 1024, 128, 23)
+    ramp = torch.linspace(0.2, 6.0, 1024).view(1, 1, 1024, 1)
+    k = (k.float() * ramp).to(torch.bfloat16)
+    _check_qkv(twfa, plan, q, k, v, False)
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_constant_rows(twfa, plan, causal):
+    # Q = 0: every score is 0, P = 1 everywhere, O = mean of the visible V rows
+    q, k, v = _inputs(1, 2, 640, 128, 24)
+    q.zero_()
+    _check_qkv(twfa, plan, q, k, v, causal)
+    # constant K and V rows: O = that row for every query
+    q, k, v = _inputs(1, 2, 384, 128, 25)
+    k[:] = k[:, :, :1]
+    v[:] = v[:, :, :1]
+    _check_qkv(twfa, plan, q, k, v, causal)
+
+
+def test_row_max_in_the_first_key(twfa, plan):
+    # key 0 dominates every row by a wide margin: later P underflow toward 0
+    q, k, v = _inputs(1, 2, 768, 128, 26)
+    k[:, :, 0] = q.float().mean(dim=2).to(torch.bfloat16) * 40.0
+    _check_qkv(twfa, plan, q, k, v, False)
 
 
 @pytest.mark.parametrize("S", [128, 256, 512, 1024])
@@ -84,9 +145,30 @@ def test_host_buffer_entry_point(twfa, plan):
     bits = [x.view(torch.int16).numpy().view(np.uint16) for x in (q, k, v)]
     o, lse = twfa.fa_fwd_host(plan, *bits, return_lse=True)
     ro, rl = oracle_lib.attention(q.float().numpy(), k.float().numpy(), v.float().numpy())
-    err = np.abs(oracle_lib.from_bf16_bits(o) - ro)
+    err = np.abs(oracle_lib.from_bf16_bits(o) - ro) / max(1.0, float(np.abs(ro).max()))
     assert err.max() <= TOL_MAX and err.mean() <= TOL_MEAN
-    assert np.abs(lse - rl).max() <= TOL_LSE
+    assert np.abs(lse - rl).max() <= TOL_LSE * max(1.0, float(np.abs(rl).max()))
+
+
+@pytest.mark.parametrize("pinned,causal", [(False, False), (True, False), (True, True)])
+def test_host_buffer_pipeline_matches_device_call(twfa, plan, pinned, causal):
+    """twfa_fa_fwd_host streams the (b, h) pairs in 64 MiB chunks (here 3
+    chunks: 32 + 32 + 6 pairs at S = 8192) through staged (pageable) or
+    direct (page-locked) copies: O and LSE bit-identical to the device call."""
+    B, H, S = 1, 70, 8192
+    g = torch.Generator(device="cuda").manual_seed(31)
+    q, k, v = (torch.randn(B, H, S, 128, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
+    o_dev, l_dev = twfa.fa_fwd(plan, q, k, v, causal=causal, return_lse=True)
+    hs = [x.cpu() for x in (q, k, v)]
+    ho = torch.empty_like(hs[0])
+    hl = torch.empty(B, H, S, dtype=torch.float32)
+    if pinned:
+        hs, ho, hl = [x.pin_memory() for x in hs], ho.pin_memory(), hl.pin_memory()
+    bits = [x.view(torch.int16).numpy().view(np.uint16) for x in (*hs, ho)]
+    twfa.fa_fwd_host(plan, *bits[:3], causal=causal, out=bits[3], lse_out=hl.numpy())
+    torch.cuda.synchronize()
+    assert torch.equal(ho, o_dev.cpu())
+    assert torch.equal(hl, l_dev.cpu())
 
 
 def test_full_size_against_cudnn_sdpa(twfa, plan):
@@ -100,15 +182,15 @@ def test_full_size_against_cudnn_sdpa(twfa, plan):
     o, lse = twfa.fa_fwd(plan, q, k, v, return_lse=True)
     ref = torch.nn.functional.scaled_dot_product_attention(q, k, v)
     d = (o.float() - ref.float()).abs()
-    assert d.max().item() <= 2.5e-2 and d.mean().item() <= 2e-3
+    assert d.max().item() <= 2e-3 and d.mean().item() <= 2e-5  # observed 4.9e-4 / 3.6e-6
     for b, h in [(0, 0), (3, 31)]:
         # first 512 query rows of the pair against all 8192 keys
         ro, rl = oracle_lib.attention(q[b:b + 1, h:h + 1, :512].float().cpu().numpy(),
                                       k[b:b + 1, h:h + 1].float().cpu().numpy(),
                                       v[b:b + 1, h:h + 1].float().cpu().numpy())
         err = np.abs(o[b, h, :512].float().cpu().numpy() - ro[0, 0])
-        assert err.max() <= TOL_MAX
-        assert np.abs(lse[b, h, :512].cpu().numpy() - rl[0, 0]).max() <= TOL_LSE
+        assert err.max() <= TOL_MAX * max(1.0, float(np.abs(ro).max()))
+        assert np.abs(lse[b, h, :512].cpu().numpy() - rl[0, 0]).max() <= TOL_LSE * max(1.0, float(np.abs(rl).max()))
 
 
 def test_full_size_causal_against_cudnn_sdpa(twfa, plan):
@@ -120,7 +202,7 @@ def test_full_size_causal_against_cudnn_sdpa(twfa, plan):
     o = twfa.fa_fwd(plan, q, k, v, causal=True)
     ref = torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True)
     d = (o.float() - ref.float()).abs()
-    assert d.max().item() <= 2.5e-2 and d.mean().item() <= 2e-3
+    assert d.max().item() <= 2e-2 and d.mean().item() <= 2e-5  # observed 7.8e-3 / 4.3e-6 (rows near the diagonal)
 
 
 def test_host_tool_runs_through_c_abi(twfa):
