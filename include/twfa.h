@@ -85,9 +85,9 @@ int twfa_fa_fwd(const twfa_plan* plan, const void* q, const void* k, const void*
 
 /* Same as twfa_fa_fwd, additionally recording the issue trace of CTA 0:
  * per warp w, trace[w * cap * 8] = number of records n, followed by n records
- * of 8 uint32 {node, iteration, trip, t_issue, t_ready, t_done, 0, 0}
- * (clock64 low words; device buffer of num_warps * cap * 8 uint32, zeroed by
- * the caller). */
+ * of 8 uint32 {node, iteration, trip, t_issue, t_ready, t_done, work tile
+ * ordinal, iterations of that work tile} (clock64 low words; device buffer of
+ * num_warps * cap * 8 uint32, zeroed by the caller). */
 int twfa_fa_fwd_traced(const twfa_plan* plan, const void* q, const void* k, const void* v, void* o,
                        float* lse, int B, int H, int S, int D, int causal, float softmax_scale,
                        uint32_t* trace, uint32_t cap, void* stream);
@@ -117,6 +117,14 @@ int twfa_fa_bwd(const twfa_plan* plan, const void* q, const void* k, const void*
                 const void* dout, const float* lse, void* dq, void* dk, void* dv, void* workspace,
                 size_t workspace_bytes, int B, int H, int S, int D, int causal, float softmax_scale,
                 void* stream);
+
+/* Same as twfa_fa_bwd, additionally recording the issue trace of CTA 0 in
+ * the layout of twfa_fa_fwd_traced (records {node, iteration, trip, t_issue,
+ * 0, t_done, work item ordinal, Q iterations of that item}). */
+int twfa_fa_bwd_traced(const twfa_plan* plan, const void* q, const void* k, const void* v, const void* o,
+                       const void* dout, const float* lse, void* dq, void* dk, void* dv, void* workspace,
+                       size_t workspace_bytes, int B, int H, int S, int D, int causal, float softmax_scale,
+                       uint32_t* trace, uint32_t cap, void* stream);
 
 /* GEMM mainloop plan: C[M,N] = A[M,K] * B[N,K]^T, bf16 in/out, fp32 accumulate.
  * M % 128 == 0, N % 256 == 0, K % 64 == 0. */

@@ -66,9 +66,11 @@ def lib():
         L.twfa_grid_size.argtypes = [ctypes.POINTER(i32)]
         L.twfa_fa_bwd_workspace_size.argtypes = [i32, i32, i32, i32, ctypes.POINTER(sz)]
         L.twfa_fa_bwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, i32, i32, i32, i32, i32, f32, vp]
+        L.twfa_fa_bwd_traced.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, i32, i32, i32, i32, i32, f32,
+                                         vp, ctypes.c_uint32, vp]
         for name in ("twfa_schedule_validate", "twfa_plan_create", "twfa_plan_describe", "twfa_plan_raw", "twfa_fa_fwd",
                      "twfa_fa_fwd_traced", "twfa_fa_fwd_host", "twfa_gemm", "twfa_grid_size",
-                     "twfa_fa_bwd_workspace_size", "twfa_fa_bwd"):
+                     "twfa_fa_bwd_workspace_size", "twfa_fa_bwd", "twfa_fa_bwd_traced"):
             getattr(L, name).restype = i32
         _lib = L
     return _lib
@@ -213,7 +215,8 @@ def fa_fwd_host(plan, q, k, v, causal=False, softmax_scale=None, return_lse=Fals
     return (o, lse) if (return_lse or lse_out is not None) else o
 
 
-def fa_bwd(plan, q, k, v, o, dout, lse, causal=False, softmax_scale=None, workspace=None):
+def fa_bwd(plan, q, k, v, o, dout, lse, causal=False, softmax_scale=None, workspace=None, trace=None,
+           trace_cap=0):
     """FA backward on the current CUDA stream (plan from an FA-backward
     schedule, e.g. load_schedule("fa_bwd")). q, k, v, o, dout: [B, H, S, 128]
     bf16 CUDA tensors; lse: [B, H, S] fp32 from fa_fwd(..., return_lse=True).
@@ -241,9 +244,15 @@ def fa_bwd(plan, q, k, v, o, dout, lse, causal=False, softmax_scale=None, worksp
         raise ValueError("inputs must be on one device")
     ptr = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
     with torch.cuda.device(q.device):
-        _check(lib().twfa_fa_bwd(plan.handle, ptr(q), ptr(k), ptr(v), ptr(o), ptr(dout), ptr(lse), ptr(dq), ptr(dk),
-                                 ptr(dv), ptr(workspace), need.value, B, H, S, D, int(bool(causal)), scale,
-                                 _stream_ptr(q)))
+        args = (plan.handle, ptr(q), ptr(k), ptr(v), ptr(o), ptr(dout), ptr(lse), ptr(dq), ptr(dk), ptr(dv),
+                ptr(workspace), need.value, B, H, S, D, int(bool(causal)), scale)
+        if trace is not None:
+            nw = plan.describe()["num_warps"]
+            if trace.dtype != torch.int32 or not trace.is_contiguous() or trace.numel() < nw * int(trace_cap) * 8:
+                raise ValueError("trace must be a contiguous int32 tensor of >= num_warps * trace_cap * 8 elements")
+            _check(lib().twfa_fa_bwd_traced(*args, ptr(trace), trace_cap, _stream_ptr(q)))
+        else:
+            _check(lib().twfa_fa_bwd(*args, _stream_ptr(q)))
     return dq, dk, dv
 
 

@@ -298,7 +298,8 @@ int fa_fwd_impl(const twfa_plan* plan, const void* q, const void* k, const void*
 
 int fa_bwd_impl(const twfa_plan* plan, const void* q, const void* k, const void* v, const void* o,
                 const void* dout, const float* lse, void* dq, void* dk, void* dv, void* ws, size_t ws_bytes, int B,
-                int H, int S, int D, int causal, float scale, void* stream) {
+                int H, int S, int D, int causal, float scale, void* stream, uint32_t* trace = nullptr,
+                uint32_t cap = 0) {
   if (!plan) throw twfa::UsageError("plan is NULL");
   const TwfaDevicePlan& p = plan->sched.plan;
   if (p.family != TWFA_FAMILY_FA_BWD) throw twfa::UsageError("plan is not an FA-backward plan");
@@ -336,6 +337,8 @@ int fa_bwd_impl(const twfa_plan* plan, const void* q, const void* k, const void*
   a.causal = causal ? 1 : 0;
   a.scale = scale;
   a.scale_log2 = scale * 1.4426950408889634f;
+  a.trace = trace;
+  a.trace_cap = cap;
   const long long work = static_cast<long long>(bh) * ((S + 127) / 128);
   const int grid = static_cast<int>(std::min<long long>(work, sm_count()));
   a.work_list = nullptr;
@@ -624,6 +627,17 @@ int twfa_fa_bwd(const twfa_plan* plan, const void* q, const void* k, const void*
   return guarded([&] {
     return fa_bwd_impl(plan, q, k, v, o, dout, lse, dq, dk, dv, workspace, workspace_bytes, B, H, S, D, causal,
                        softmax_scale, stream);
+  });
+}
+
+int twfa_fa_bwd_traced(const twfa_plan* plan, const void* q, const void* k, const void* v, const void* o,
+                       const void* dout, const float* lse, void* dq, void* dk, void* dv, void* workspace,
+                       size_t workspace_bytes, int B, int H, int S, int D, int causal, float softmax_scale,
+                       uint32_t* trace, uint32_t cap, void* stream) {
+  return guarded([&] {
+    if (!trace || cap < 2) throw twfa::UsageError("trace buffer missing");
+    return fa_bwd_impl(plan, q, k, v, o, dout, lse, dq, dk, dv, workspace, workspace_bytes, B, H, S, D, causal,
+                       softmax_scale, stream, trace, cap);
   });
 }
 

@@ -31,6 +31,11 @@ struct FaBwdArgs {
   // .. work_off[x + 1]) in order; nullptr = round-robin over the CTAs
   const int* work_list;
   const int* work_off;
+  // optional issue trace of CTA 0 (twfa_fa_bwd_traced): per warp, word 0 =
+  // record count, then 8-word records {node, iteration, trip, t_issue, 0,
+  // t_done, work item ordinal, iterations of that item}
+  uint32_t* trace;
+  uint32_t trace_cap;
 };
 
 size_t fa_bwd_smem_bytes(const TwfaDevicePlan& plan);

@@ -129,7 +129,25 @@ __device__ __forceinline__ BwdItem bwd_item(const BwdCtx& c, const FaBwdArgs& a,
 struct BwdState {
   int q_next, o_next;      // next Q / dO iteration to load (TMA warp)
   int q_target, o_target;  // loads the trip program has asked for so far
+  uint32_t trace_n;        // records of this warp in the issue trace
 };
+
+// Issue trace (CTA 0, lane 0 of every warp): one record per op instance,
+// the same layout as the forward's (fa_fwd_kernel.cuh)
+__device__ __forceinline__ uint32_t* bwd_trace(const FaBwdArgs& a, const BwdCtx& c, BwdState& st, int node, int it,
+                                               int trip, const BwdItem& t) {
+  if (a.trace == nullptr || blockIdx.x != 0 || c.lane != 0 || st.trace_n + 1 >= a.trace_cap) return nullptr;
+  uint32_t* base = a.trace + static_cast<size_t>(c.warp) * a.trace_cap * 8;
+  uint32_t* e = base + (st.trace_n + 1) * 8;
+  e[0] = static_cast<uint32_t>(node);
+  e[1] = static_cast<uint32_t>(it);
+  e[2] = static_cast<uint32_t>(trip);
+  e[3] = static_cast<uint32_t>(clock64());
+  e[6] = t.icount;
+  e[7] = static_cast<uint32_t>(t.N);
+  base[0] = ++st.trace_n;
+  return e;
+}
 
 // Streamed Q / dO loads (LDQ / LDO). A load issues at its trip-program
 // position if its ring slot is already free; otherwise it is deferred
@@ -458,7 +476,13 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
       const bool is_q = op.kind == TWFA_OP_LDQ;
       const int target = min(t.N - 1, r - static_cast<int>(op.stage) + (is_q ? plan.k_prefetch : plan.v_prefetch));
       (is_q ? st.q_target : st.o_target) = target;
+      const int before = is_q ? st.q_next : st.o_next;
       bwd_top_up(c, a, t, st, plan, is_q, target, !TWFA_BWD_LAZY_LOADS);
+      if (a.trace != nullptr)
+        for (int lit = before; lit < (is_q ? st.q_next : st.o_next); ++lit) {
+          uint32_t* e = bwd_trace(a, c, st, op.node, lit, r, t);
+          if (e) e[5] = e[3];
+        }
     }
     return;
   }
@@ -471,6 +495,13 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
   const int it = r - static_cast<int>(op.stage);
   if (it < 0 || it >= t.N) return;
   const uint32_t g = t.gbase + static_cast<uint32_t>(it);
+  // one record per op instance; t_done stamped when the op body returns
+  struct TraceDone {
+    uint32_t* e;
+    __device__ ~TraceDone() {
+      if (e) e[5] = static_cast<uint32_t>(clock64());
+    }
+  } trace_done_{a.trace != nullptr ? bwd_trace(a, c, st, op.node, it, r, t) : nullptr};
 #if TWFA_BWD_PROF
   const bool prof = blockIdx.x == 0 && c.lane == 0 && (c.warp & 3u) == 3 && t.icount == 0 && (it == 20 || it == 21);
   struct Out {
@@ -606,7 +637,7 @@ __device__ __forceinline__ void bwd_run(const BwdCtx& c, const TwfaDevicePlan& p
   const int plen = plan.prog_len[c.warp];
   const bool is_load = c.warp == static_cast<uint32_t>(plan.load_warp);
   const bool is_mma = c.warp == static_cast<uint32_t>(plan.mma_warp);
-  BwdState st{0, 0, -1, -1};
+  BwdState st{0, 0, -1, -1, 0};
   uint32_t gbase = 0, icount = 0;
   for (int i = 0;; ++i, ++icount) {
     int work;

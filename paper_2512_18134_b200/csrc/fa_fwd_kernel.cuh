@@ -95,6 +95,15 @@ constexpr float kRescaleLog2 = 8.0f;
 #endif
 constexpr int kPParts = TWFA_P_PARTS;
 static_assert(kPParts == 2 || kPParts == 4 || kPParts == 8, "P parts");
+// MMA-warp input waits: probe all inputs of a PV op at once (1) instead of
+// waiting for them one after the other (0); skip a second wait on a K / V
+// tile this warp already saw land (TWFA_MEMO_WAITS)
+#ifndef TWFA_PROBE_PARTS
+#define TWFA_PROBE_PARTS 1
+#endif
+#ifndef TWFA_MEMO_WAITS
+#define TWFA_MEMO_WAITS 1
+#endif
 #ifndef TWFA_SOFTMAX_TOKEN
 #define TWFA_SOFTMAX_TOKEN 0  // measured: serializing MX+EX of the two tiles is 12% slower (C3)
 #endif
@@ -135,12 +144,14 @@ __shared__ FaShared g_sh;
 
 // Issue trace of CTA 0 (debug / schedule-realization evidence). Per warp:
 // word 0 = record count, then records of kTraceWords uint32:
-// {node, iteration, trip, t_issue, t_ready (inputs waited), t_done}.
+// {node, iteration, trip, t_issue, t_ready (inputs waited), t_done, work tile
+// ordinal of the CTA, K/V iterations of that tile}. A streamed load that
+// runs ahead into the next work tile records that tile and its iteration.
 constexpr int kTraceWords = 8;
 
 template <bool kTrace>
 __device__ __forceinline__ uint32_t* trace_begin(const FaArgs& a, uint32_t warp, uint32_t& n, int node, int it,
-                                                 int trip) {
+                                                 int trip, uint32_t tile, int tile_n) {
   if (!kTrace || blockIdx.x != 0 || lane_id() != 0) return nullptr;
   uint32_t* base = a.trace + static_cast<size_t>(warp) * a.trace_cap * kTraceWords;
   if (n + 1 >= a.trace_cap) return nullptr;
@@ -149,6 +160,8 @@ __device__ __forceinline__ uint32_t* trace_begin(const FaArgs& a, uint32_t warp,
   e[1] = static_cast<uint32_t>(it);
   e[2] = static_cast<uint32_t>(trip);
   e[3] = static_cast<uint32_t>(clock64());
+  e[6] = tile;
+  e[7] = static_cast<uint32_t>(tile_n);
   base[0] = ++n;  // count kept in a register; the store is fire-and-forget
   return e;
 }
@@ -370,6 +383,9 @@ __device__ __forceinline__ int valid_keys(const FaArgs& a, int row, int key0) {
 struct WarpState {
   float m_run[TWFA_MAX_TILES], l_run[TWFA_MAX_TILES], alpha[TWFA_MAX_TILES];
   int k_next, v_next;  // next K / V iteration to load (TMA warp); may run into the next tile
+  // MMA warp: the last global iteration whose K (V) tile this warp already
+  // saw land; a second tensor-core op on the same tile skips the wait
+  uint32_t k_seen, v_seen;
   uint32_t trace_n;
   // TMA warp: the CTA's next work tile (its first K / V iterations are
   // prefetched while this tile's pipeline drains)
@@ -427,7 +443,8 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
         const int lit = next++;
         const bool cross = lit >= N;
         const int key0 = (cross ? lit - N : lit) * KV, bh = cross ? st.next_bh : t.bh;
-        uint32_t* tr = trace_begin<kTrace>(args, warp, st.trace_n, op.node, lit, r);
+        uint32_t* tr = trace_begin<kTrace>(args, warp, st.trace_n, op.node, cross ? lit - N : lit, r,
+                                           t.tcount + (cross ? 1u : 0u), cross ? st.next_N : N);
         const uint32_t g = t.gbase + static_cast<uint32_t>(lit);
         const int depth = is_k ? rg.kd : rg.vd;
         const uint32_t s = g % depth, ph = (g / depth) & 1;
@@ -454,7 +471,7 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
   const uint32_t g = t.gbase + static_cast<uint32_t>(it);
   const int k = op.tile;
   const uint32_t b = g % G::depth, pb = (g / G::depth) & 1;  // S buffer of this iteration, its phase
-  uint32_t* tr = trace_begin<kTrace>(args, warp, st.trace_n, op.node, it, r);
+  uint32_t* tr = trace_begin<kTrace>(args, warp, st.trace_n, op.node, it, r, t.tcount, N);
 
   if (op.kind == TWFA_OP_SA || op.kind == TWFA_OP_SB) {
     // split S_k (single 128-key S tile): SA_k = keys 0-63 into columns 0-63,
@@ -493,8 +510,9 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
     if (it == 0) mbar_wait(&bar.q_full[k], t.tcount & 1);
     if (g >= G::depth && !(op.flags & TWFA_OPF_INORDER))  // K landed; P_k(g-depth) consumed by PV_k
       mbar_wait_all(&bar.k_full[s], (g / rg.kd) & 1, &bar.o_done[k][b], pb ^ 1);
-    else
+    else if (!TWFA_MEMO_WAITS || st.k_seen != g + 1)  // (the other sub-tile's S on this warp saw K(g) land)
       mbar_wait(&bar.k_full[s], (g / rg.kd) & 1);
+    st.k_seen = g + 1;
     trace_mark<kTrace>(tr, 4);
     tc_fence_after();
     const uint32_t qd = sdesc_lo(smem_u32(c.q_smem + k * kTileBytes), 16);
@@ -530,7 +548,26 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
     // K-steps of PV_k overlap the exponentials of the second half
     constexpr int kParts = KV == 128 ? kPParts : 2;
     constexpr int kSteps = KV / 16 / kParts;  // K-steps (16 keys) per part
+    // probe every input of the op at once (non-blocking test_wait: the
+    // round trips overlap), then block only on what had not landed: a wait
+    // on this warp costs a ~160-clk shared-memory round trip even when the
+    // phase completed long ago, and the parts arriving one by one would
+    // otherwise serialize four of them into PV's issue
+    bool part_ready[kParts];
+#if TWFA_PROBE_PARTS
+    const bool v_ok = TWFA_MEMO_WAITS && st.v_seen == g + 1 ? true : mbar_test(&bar.v_full[s], (g / rg.vd) & 1);
+    const bool o_ok = mbar_test(&bar.o_ready[k][b], pb);
+#pragma unroll
+    for (int j = 0; j < kParts; ++j) part_ready[j] = mbar_test(&bar.p_part[k][b][j], pb);
+    if (!v_ok) mbar_wait(&bar.v_full[s], (g / rg.vd) & 1);
+    if (!o_ok) mbar_wait(&bar.o_ready[k][b], pb);
+    if (!part_ready[0]) mbar_wait(&bar.p_part[k][b][0], pb);
+#else
+#pragma unroll
+    for (int j = 0; j < kParts; ++j) part_ready[j] = false;
     mbar_wait_all(&bar.v_full[s], (g / rg.vd) & 1, &bar.p_part[k][b][0], pb, &bar.o_ready[k][b], pb);
+#endif
+    st.v_seen = g + 1;
     trace_mark<kTrace>(tr, 4);
     tc_fence_after();
     const uint32_t vd = sdesc_lo(smem_u32(c.v_smem + s * G::tile), G::half);
@@ -538,7 +575,7 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
     const uint32_t acc0 = it > 0 ? 1u : 0u;
 #pragma unroll
     for (int j = 0; j < kParts; ++j) {
-      if (j > 0) {
+      if (j > 0 && !part_ready[j]) {
         mbar_wait(&bar.p_part[k][b][j], pb);
         tc_fence_after();
       }
@@ -632,7 +669,7 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
             }
             // the trace keeps one record per op: EX_k ran inside this MX_k
             trace_mark<kTrace>(tr, 5);
-            uint32_t* tr_ex = trace_begin<kTrace>(args, warp, st.trace_n, op.node + 1, it, r);
+            uint32_t* tr_ex = trace_begin<kTrace>(args, warp, st.trace_n, op.node + 1, it, r, t.tcount, N);
             trace_mark<kTrace>(tr_ex, 4);
             trace_mark<kTrace>(tr_ex, 5);
             return;
@@ -667,7 +704,7 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
         trace_mark<kTrace>(tr, 5);
         if (!(op.flags & TWFA_OPF_FUSE_NEXT)) return;
         // EX_k is this warp's next op: run it on the resident S row
-        tr = trace_begin<kTrace>(args, warp, st.trace_n, op.node + 1, it, r);
+        tr = trace_begin<kTrace>(args, warp, st.trace_n, op.node + 1, it, r, t.tcount, N);
         trace_mark<kTrace>(tr, 4);
       } else {
         // unfused EX (other ops run between MX_k and EX_k on this warp):
@@ -812,6 +849,7 @@ __device__ __forceinline__ void work_loop(const FaCtx& c, const FaArgs& args, co
                                           Trip&& trip) {
   uint32_t gbase = 0, tcount = 0;
   st.k_next = st.v_next = 0;
+  st.k_seen = st.v_seen = 0;
   for (int round = 0;; ++round, ++tcount) {
     const int work = work_of<KV>(c, args, round);
     if (work >= c.num_work) break;
