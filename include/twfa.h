@@ -127,7 +127,7 @@ int twfa_fa_bwd_traced(const twfa_plan* plan, const void* q, const void* k, cons
                        uint32_t* trace, uint32_t cap, void* stream);
 
 /* GEMM mainloop plan: C[M,N] = A[M,K] * B[N,K]^T, bf16 in/out, fp32 accumulate.
- * M % 128 == 0, N % 256 == 0, K % 64 == 0. */
+ * M % 256 == 0, N % 256 == 0, K % 64 == 0 (one CTA pair per 256 x 256 output tile). */
 int twfa_gemm(const twfa_plan* plan, const void* a, const void* b, void* c, int M, int N, int K,
               void* stream);
 

@@ -3,6 +3,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -646,24 +647,32 @@ int twfa_gemm(const twfa_plan* plan, const void* a, const void* b, void* c, int 
     if (!plan) throw twfa::UsageError("plan is NULL");
     const TwfaDevicePlan& p = plan->sched.plan;
     if (p.family != TWFA_FAMILY_GEMM) throw twfa::UsageError("plan is not a GEMM plan");
-    if (M <= 0 || N <= 0 || K <= 0 || M % 128 || N % 256 || K % 64)
-      throw twfa::UsageError("GEMM needs M % 128 == 0, N % 256 == 0, K % 64 == 0");
-    if (p.k_depth < 1 || p.k_depth > 4) throw twfa::UsageError("GEMM ring depth must be 1..4");
+    if (M <= 0 || N <= 0 || K <= 0 || M % 256 || N % 256 || K % 64)
+      throw twfa::UsageError("GEMM needs M % 256 == 0, N % 256 == 0, K % 64 == 0");
+    if (p.k_depth < 1 || p.k_depth > 6) throw twfa::UsageError("GEMM ring depth must be 1..6");
     require_aligned(a, "a");
     require_aligned(b, "b");
     require_aligned(c, "c");
     DeviceGuard guard(a, "a");
     const cuuint64_t da[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(M)};
     const cuuint64_t db[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(N)};
+    const cuuint64_t dc[2] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(M)};
     const cuuint64_t st[1] = {static_cast<cuuint64_t>(K) * 2};
-    const cuuint32_t ba[2] = {64, 128};
-    const cuuint32_t bb[2] = {64, 256};
-    const CUtensorMap ta = make_map(a, 2, da, st, ba);
-    const CUtensorMap tb = make_map(b, 2, db, st, bb);
-    twfa::GemmArgs ga{static_cast<__nv_bfloat16*>(c), M, N, K};
-    const int tiles = (M / 128) * (N / 256);
-    const int grid = std::min(tiles, sm_count());
-    check(twfa::gemm_launch(ta, tb, p, ga, grid, static_cast<cudaStream_t>(stream)), "gemm launch");
+    const cuuint64_t stc[1] = {static_cast<cuuint64_t>(N) * 2};
+    const cuuint32_t box[2] = {64, 128};  // A, B: 128 rows x 64 k per CTA; C: 128 rows x 64 columns per store
+    const CUtensorMap ta = make_map(a, 2, da, st, box);
+    const CUtensorMap tb = make_map(b, 2, db, st, box);
+    const CUtensorMap tc = make_map(c, 2, dc, stc, box);
+    // raster group (pair-tile rows whose A panel stays in L2); TWFA_GEMM_GROUP overrides
+    int group_m = 8;
+    if (const char* e = std::getenv("TWFA_GEMM_GROUP")) group_m = std::max(1, std::atoi(e));
+    int pol_mode = 2;  // A and B evict_last (gemm_sm100.cu)
+    if (const char* e = std::getenv("TWFA_GEMM_POL")) pol_mode = std::atoi(e);
+    twfa::GemmArgs ga{static_cast<__nv_bfloat16*>(c), M, N, K, group_m, pol_mode};
+    // one CTA pair (cluster of 2) per 256 x 256 output tile, persistent
+    const int pair_tiles = (M / 256) * (N / 256);
+    const int grid = 2 * std::min(pair_tiles, sm_count() / 2);
+    check(twfa::gemm_launch(ta, tb, tc, p, ga, grid, static_cast<cudaStream_t>(stream)), "gemm launch");
     return TWFA_OK;
   });
 }

@@ -38,12 +38,14 @@ cudaError_t fa_fwd_launch(const CUtensorMap& tq, const CUtensorMap& tk, const CU
 const char* fa_fwd_kernel_name(const TwfaDevicePlan& plan);
 
 struct GemmArgs {
-  __nv_bfloat16* c;  // [M, N] row-major
+  __nv_bfloat16* c;  // [M, N] row-major (written through the tm_c tensor map)
   int M, N, K;
+  int group_m;       // raster: pair-tile rows per group (A panel kept in L2); <= 0: default
+  int pol_mode;      // L2 cache policies of the A / B loads (gemm_sm100.cu)
 };
 
 size_t gemm_smem_bytes(const TwfaDevicePlan& plan);
-cudaError_t gemm_launch(const CUtensorMap& ta, const CUtensorMap& tb, const TwfaDevicePlan& plan,
-                        const GemmArgs& args, int grid, cudaStream_t stream);
+cudaError_t gemm_launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
+                        const TwfaDevicePlan& plan, const GemmArgs& args, int grid, cudaStream_t stream);
 
 }  // namespace twfa

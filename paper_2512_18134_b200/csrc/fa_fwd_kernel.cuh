@@ -455,9 +455,13 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
         mbar_wait(empty, ph ^ 1);
         trace_mark<kTrace>(tr, 4);
         if (elect_one()) {
-          mbar_arrive_expect_tx(full, G::tile);
-          tma_load_3d(dst, map, full, 0, key0, bh, c.pol_kv);
-          tma_load_3d(dst + G::half, map, full, 64, key0, bh, c.pol_kv);
+          if (TWFA_WHATIF == 4 && g >= static_cast<uint32_t>(depth)) {
+            mbar_arrive(full);  // what-if: the tile is already resident (no L2 -> SM traffic)
+          } else {
+            mbar_arrive_expect_tx(full, G::tile);
+            tma_load_3d(dst, map, full, 0, key0, bh, c.pol_kv);
+            tma_load_3d(dst + G::half, map, full, 64, key0, bh, c.pol_kv);
+          }
         }
         __syncwarp();
         trace_mark<kTrace>(tr, 5);

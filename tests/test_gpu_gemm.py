@@ -16,7 +16,10 @@ def plan(twfa):
     return twfa.Plan(*twfa.load_schedule("gemm_mainloop"))
 
 
-@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (256, 512, 192), (384, 256, 1024), (1024, 1024, 512)])
+# one CTA pair per 256 x 256 tile: fewer tiles than pairs, several tiles per
+# pair (both TMEM accumulators, the staging double buffer), a ragged raster group
+@pytest.mark.parametrize("M,N,K", [(256, 256, 64), (256, 512, 192), (512, 256, 1024), (1024, 1024, 512),
+                                   (2560, 4608, 256)])
 def test_gemm_matches_oracle(twfa, plan, M, N, K):
     g = torch.Generator(device="cpu").manual_seed(1234)
     a = (torch.randn(M, K, generator=g) / K ** 0.5).to(torch.bfloat16)
@@ -39,8 +42,22 @@ def test_gemm_full_size(twfa, plan):
     assert d.max().item() <= 3e-2 and d.mean().item() <= 2e-3
 
 
-def test_gemm_rejects_unaligned_shapes(twfa, plan):
-    a = torch.zeros(100, 64, device="cuda", dtype=torch.bfloat16)
-    b = torch.zeros(256, 64, device="cuda", dtype=torch.bfloat16)
+def test_gemm_raster_groups_agree(twfa, plan, monkeypatch):
+    """The raster group only reorders tiles: bit-identical C for every group."""
+    g = torch.Generator(device="cuda").manual_seed(5)
+    a = (torch.randn(2048, 512, device="cuda", generator=g) / 512 ** 0.5).to(torch.bfloat16)
+    b = torch.randn(3072, 512, device="cuda", generator=g).to(torch.bfloat16)
+    outs = []
+    for grp in ("1", "3", "8", "64"):
+        monkeypatch.setenv("TWFA_GEMM_GROUP", grp)
+        outs.append(twfa.gemm(plan, a, b))
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0])
+
+
+@pytest.mark.parametrize("M,N,K", [(100, 256, 64), (128, 256, 64), (256, 384, 64), (256, 256, 48)])
+def test_gemm_rejects_unaligned_shapes(twfa, plan, M, N, K):
+    a = torch.zeros(M, K, device="cuda", dtype=torch.bfloat16)
+    b = torch.zeros(N, K, device="cuda", dtype=torch.bfloat16)
     with pytest.raises(ValueError):
         twfa.gemm(plan, a, b)

@@ -285,12 +285,14 @@ def fa_backward_problem(calibrated=False, fused=False, exb_spill=16, q_staging=F
 
 def gemm_problem():
     """GEMM mainloop (BASELINE config 2): per k-block, TMA loads of the A and B
-    tiles feed one 128x256x64 tcgen05 MMA chain into a TMEM accumulator.
-    128x256x64 = 2 MMAC = 512 clk on TC; TMA of 48 KiB = 512 clk."""
+    tiles feed one 256x256x64 tcgen05 MMA chain (cta_group::2: a CTA pair on
+    two SMs, each holding 128 rows of A and 128 rows of B) into a TMEM
+    accumulator. Per SM 128x256x64 = 2 MMAC = 512 clk on TC; TMA of 32 KiB
+    per SM per k-block."""
     T = 512
     machine = {
         "units": [{"name": "TC", "capacity": 1}, {"name": "TMA", "capacity": 1}],
-        "memories": [{"name": "smem", "capacity": 4}],
+        "memories": [{"name": "smem", "capacity": 6}],
         "num_warps": 2,
         "reg_limit": 0,
         "vl_warp": 1,
@@ -379,7 +381,7 @@ def main():
     args = ap.parse_args()
     # name: (raw problem, stream depth, normalization resolution U or None = --resolution)
     probs = {
-        "gemm_mainloop": (gemm_problem(), 4, None),
+        "gemm_mainloop": (gemm_problem(), 6, None),  # 32 KiB stages per SM (CTA pair)
         # production: tcgen05.mma modeled as variable latency (see
         # fa_forward_problem) with the B200-calibrated costs (EX 6, MX 2
         # units of 256 clk, measured by the in-kernel trace); U = 9 normalizes
