@@ -139,8 +139,9 @@ long long work_list_budget() {
 }
 
 // kind 0: forward (tile = 256 queries; causal work index w = (qbl-1-qb)*bh + b,
-// 2 (qb + 1) K/V iterations); kind 1: backward (tile = 128 keys; causal work
-// index w = j*bh + b, nq - j Q iterations). The group bound applies to the
+// 2 (qb + 1) K/V iterations); kind 2: forward on CTA pairs (tile = 512
+// queries, 4 (qb + 1) iterations, one list per pair); kind 1: backward (tile =
+// 128 keys; causal work index w = j*bh + b, nq - j Q iterations). The group bound applies to the
 // streamed operands of one (b, h): K, V (forward) or Q, dO (backward).
 WorkLists causal_work_lists(int kind, int bh, int S, int grid, cudaStream_t stream) {
   using Key = std::tuple<int, int, int, int, int, long long>;
@@ -154,7 +155,7 @@ WorkLists causal_work_lists(int kind, int bh, int S, int grid, cudaStream_t stre
   const Key key = std::make_tuple(kind, dev, bh, S, grid, budget);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
-  const int tile = kind == 0 ? 256 : 128;
+  const int tile = kind == 0 ? 256 : kind == 2 ? 512 : 128;
   const int nt = (S + tile - 1) / tile;  // tiles per (b, h)
   const int num = bh * nt;
   const long long stream_bytes = 2LL * S * 128 * 2;  // the two streamed operands of one (b, h)
@@ -172,9 +173,9 @@ WorkLists causal_work_lists(int kind, int bh, int S, int grid, cudaStream_t stre
   for (int w : order) {
     const int rank = w / bh;
     long long iters;
-    if (kind == 0) {
+    if (kind != 1) {
       const int qb = nt - 1 - rank;
-      iters = (std::min<long long>(S, 256LL * (qb + 1)) + 127) / 128;
+      iters = (std::min<long long>(S, static_cast<long long>(tile) * (qb + 1)) + 127) / 128;
     } else {
       iters = nt - rank;  // K/V tile j = rank sees Q tiles j .. nt-1
     }
@@ -243,6 +244,13 @@ struct DeviceGuard {
   DeviceGuard& operator=(const DeviceGuard&) = delete;
 };
 
+// CTA pairs (cta_group::2) for the forward when the plan allows them;
+// TWFA_PAIR=0 keeps one CTA per work tile (comparison runs)
+bool use_pairs(const TwfaDevicePlan& p) {
+  const char* e = std::getenv("TWFA_PAIR");
+  return twfa::fa_fwd_pair_capable(p) && !(e && std::strcmp(e, "0") == 0);
+}
+
 // TWFA_WORK_LISTS=0 keeps the arithmetic causal order (comparison runs)
 bool use_work_lists() {
   const char* e = std::getenv("TWFA_WORK_LISTS");
@@ -266,10 +274,13 @@ int fa_fwd_impl(const twfa_plan* plan, const void* q, const void* k, const void*
   const cuuint64_t bh = static_cast<cuuint64_t>(B) * H;
   const cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(S), bh};
   const cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 2, static_cast<cuuint64_t>(S) * D * 2};
+  const bool pair = use_pairs(p);
   const cuuint32_t box_q[3] = {64, 128, 1};
   const cuuint32_t box_kv[3] = {64, static_cast<cuuint32_t>(p.kv_tile), 1};
+  // a CTA of a pair loads half the keys of a K tile (per head-dim half)
+  const cuuint32_t box_k[3] = {64, static_cast<cuuint32_t>(pair ? p.kv_tile / 2 : p.kv_tile), 1};
   const CUtensorMap tq = make_map(q, 3, dims, strides, box_q);
-  const CUtensorMap tk = make_map(k, 3, dims, strides, box_kv);
+  const CUtensorMap tk = make_map(k, 3, dims, strides, box_k);
   const CUtensorMap tv = make_map(v, 3, dims, strides, box_kv);
   const CUtensorMap to = make_map(o, 3, dims, strides, box_q);
   twfa::FaArgs a{};
@@ -283,16 +294,20 @@ int fa_fwd_impl(const twfa_plan* plan, const void* q, const void* k, const void*
   a.S = S;
   a.causal = causal ? 1 : 0;
   a.scale_log2 = scale * 1.4426950408889634f;
-  const long long work = static_cast<long long>(bh) * ((S + 255) / 256);
-  const int grid = static_cast<int>(std::min<long long>(work, sm_count()));
+  // persistent: one work unit (CTA, or CTA pair of 512 query rows) per SM (pair)
+  const int unit_rows = pair ? 512 : 256, cta_per_unit = pair ? 2 : 1;
+  const long long work = static_cast<long long>(bh) * ((S + unit_rows - 1) / unit_rows);
+  const int units = static_cast<int>(std::min<long long>(work, sm_count() / cta_per_unit));
+  const int grid = units * cta_per_unit;
   a.work_list = nullptr;
   a.work_off = nullptr;
   if (causal && use_work_lists()) {
-    const WorkLists wl = causal_work_lists(0, static_cast<int>(bh), S, grid, static_cast<cudaStream_t>(stream));
+    const WorkLists wl =
+        causal_work_lists(pair ? 2 : 0, static_cast<int>(bh), S, units, static_cast<cudaStream_t>(stream));
     a.work_list = wl.list;
     a.work_off = wl.off;
   }
-  check(twfa::fa_fwd_launch(tq, tk, tv, p, a, grid, static_cast<cudaStream_t>(stream), allow_specialized()),
+  check(twfa::fa_fwd_launch(tq, tk, tv, p, a, grid, static_cast<cudaStream_t>(stream), allow_specialized(), pair),
         "fa_fwd launch");
   return TWFA_OK;
 }
@@ -542,7 +557,8 @@ int twfa_plan_create(const char* problem_json, const char* solution_json, twfa_p
       const std::string name = twfa::fa_fwd_kernel_name(p->sched.plan);
       const std::string kernel =
           allow_specialized() && name != "interpreter" ? "specialized:" + name : std::string("interpreter");
-      p->description.insert(p->description.size() - 1, ",\"kernel\":\"" + kernel + "\"");
+      p->description.insert(p->description.size() - 1, ",\"kernel\":\"" + kernel + "\",\"cta_pair\":" +
+                                                        (use_pairs(p->sched.plan) ? "true" : "false"));
     }
     *out = p;
     return TWFA_OK;

@@ -22,18 +22,23 @@ struct FaArgs {
   int B, H, S;
   int causal;
   float scale_log2;    // softmax_scale * log2(e)
-  // optional per-CTA work lists (causal): CTA x runs work_list[work_off[x]
-  // .. work_off[x + 1]) in order; nullptr = the arithmetic round order
+  // optional per-unit work lists (causal): unit x (a CTA, or a CTA pair)
+  // runs work_list[work_off[x] .. work_off[x + 1]) in order; nullptr = the
+  // arithmetic round order
   const int* work_list;
   const int* work_off;
 };
 
-size_t fa_fwd_smem_bytes(const TwfaDevicePlan& plan);
+// CTA-pair realization (cta_group::2, clusters of 2): 128-key K/V tiles,
+// unsplit S, two Q sub-tiles per CTA
+bool fa_fwd_pair_capable(const TwfaDevicePlan& plan);
+size_t fa_fwd_smem_bytes(const TwfaDevicePlan& plan, bool pair);
 // Runs the build-time specialized kernel of `plan` when one was generated
-// (gen/fa_plans.inc) and allow_specialized is set, else the interpreter.
+// (gen/fa_plans.inc) and allow_specialized is set, else the interpreter;
+// `pair`: as CTA pairs (grid even, work lists indexed by pair).
 cudaError_t fa_fwd_launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                           const TwfaDevicePlan& plan, const FaArgs& args, int grid, cudaStream_t stream,
-                          bool allow_specialized);
+                          bool allow_specialized, bool pair);
 // "specialized:<name>" or "interpreter"
 const char* fa_fwd_kernel_name(const TwfaDevicePlan& plan);
 

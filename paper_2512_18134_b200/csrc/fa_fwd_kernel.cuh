@@ -60,12 +60,24 @@ constexpr uint32_t kHalfBytes = kTileBytes / 2;
 // K/V tile of KV keys (128, or 64 when S is double-buffered in tensor memory:
 // the plan's S ring depth is 128 / KV). S_k's buffer b of iteration g is
 // g % depth at columns [128k + b*KV, ...); P_k (bf16) is aliased over it.
-template <int KV>
+//
+// CTA pair (P = true, cta_group::2): the two CTAs of a cluster run one work
+// tile of 2 x 256 query rows; sub-tile k of CTA r holds rows 256k + 128r of
+// it, and one M = 256 MMA computes S_k (PV_k) for both. Each CTA stages half
+// of every K tile (keys 64r .. 64r + 63, both head-dim halves) and half of
+// every V tile (head dims 64r .. 64r + 63, all keys), so the per-SM K/V ring
+// slots, the TMA traffic and the tensor core's shared-memory reads per FLOP
+// are halved.
+template <int KV, bool P = false>
 struct Kv {
   static constexpr int depth = 128 / KV;                        // S ring depth
-  static constexpr uint32_t tile = KV * kHeadDim * 2;           // K or V tile bytes
+  static constexpr uint32_t tile = KV * kHeadDim * 2;           // full K or V tile bytes
   static constexpr uint32_t half = tile / 2;                    // one 64-column SW128 half
-  static constexpr uint32_t idesc_s = idesc_bf16_f32(128, KV, 0);  // K-major Q, K-major K
+  static constexpr uint32_t slot = P ? tile / 2 : tile;         // this CTA's ring slot (K or V)
+  static constexpr uint32_t k_half = P ? half / 2 : half;       // K slot: one head-dim half of its keys
+  static constexpr int rows = P ? 2 : 1;                        // CTAs per work tile
+  static constexpr uint32_t idesc_s = idesc_bf16_f32(128 * rows, KV, 0);  // K-major Q, K-major K
+  static constexpr uint32_t idesc_pv = idesc_bf16_f32(128 * rows, kHeadDim, 1);  // TMEM P, MN-major V
 };
 constexpr int kMaxRing = 4;
 #ifndef TWFA_POLY_EVERY
@@ -82,7 +94,9 @@ constexpr float kRescaleLog2 = 8.0f;
 #endif
 // What-if knobs for sensitivity experiments (timing only; results are WRONG
 // when set): 1 = half the exponentials on MUFU (the rest reuse them),
-// 3 = MX reads half the row
+// 3 = MX reads half the row, 4 = no K/V loads after the first ring fill,
+// 5 = the MMA warp skips its steady-state waits on K, V and the correction
+// (only P and Q are awaited), 6 = 5 and the loads skip their empty-slot waits
 #ifndef TWFA_WHATIF
 #define TWFA_WHATIF 0
 #endif
@@ -95,6 +109,17 @@ constexpr float kRescaleLog2 = 8.0f;
 #endif
 constexpr int kPParts = TWFA_P_PARTS;
 static_assert(kPParts == 2 || kPParts == 4 || kPParts == 8, "P parts");
+// CTA pairs hand P over in halves (TWFA_PAIR_P_PARTS; measured under the
+// power cap, C3: 0.585 tensor-pipe fraction per clock with halves against
+// 0.564 with 4 parts)
+#ifndef TWFA_PAIR_P_PARTS
+#define TWFA_PAIR_P_PARTS 2
+#endif
+static_assert(TWFA_PAIR_P_PARTS <= kPParts || TWFA_PAIR_P_PARTS == 2, "pair P parts");
+template <bool P>
+__host__ __device__ constexpr int p_parts() {
+  return P ? (TWFA_PAIR_P_PARTS < kPParts ? TWFA_PAIR_P_PARTS : kPParts) : kPParts;
+}
 // MMA-warp input waits: probe all inputs of a PV op at once (1) instead of
 // waiting for them one after the other (0); skip a second wait on a K / V
 // tile this warp already saw land (TWFA_MEMO_WAITS)
@@ -170,6 +195,40 @@ __device__ __forceinline__ void trace_mark(uint32_t* e, int field) {
   if (kTrace && e != nullptr) e[field] = static_cast<uint32_t>(clock64());
 }
 
+// ---------------------------------------------------------------- barrier flavours
+// With CTA pairs (P) the MMA-side barriers of the leader also receive
+// arrivals from the peer CTA, and the tensor core reads and writes both
+// CTAs' memory: waits acquire at cluster scope, the softmax / correction
+// warps of both CTAs arrive on the leader's copy, commits multicast to both.
+template <bool P>
+__device__ __forceinline__ void wait_(uint64_t* b, uint32_t ph) {
+  if constexpr (P) mbar_wait_cluster(b, ph); else mbar_wait(b, ph);
+}
+template <bool P>
+__device__ __forceinline__ bool test_(uint64_t* b, uint32_t ph) {
+  if constexpr (P) return mbar_test_cluster(b, ph); else return mbar_test(b, ph);
+}
+template <bool P>
+__device__ __forceinline__ void wait_all_(uint64_t* b0, uint32_t p0, uint64_t* b1, uint32_t p1) {
+  if constexpr (P) {
+    bool d0 = mbar_try_wait_cluster(b0, p0);
+    bool d1 = mbar_try_wait_cluster(b1, p1);
+    while (!d0) d0 = mbar_try_wait_cluster(b0, p0);
+    while (!d1) d1 = mbar_try_wait_cluster(b1, p1);
+  } else {
+    mbar_wait_all(b0, p0, b1, p1);
+  }
+}
+// a warp's arrival on a barrier the MMA-issuing warp (of the leader) waits on
+template <bool P>
+__device__ __forceinline__ void arrive_mma_(uint64_t* b) {
+  if constexpr (P) warp_arrive_cluster(b, 0); else warp_arrive(b);
+}
+template <bool P>
+__device__ __forceinline__ void commit_(uint64_t* b) {
+  if constexpr (P) mma_commit_pair(b, 0x3); else mma_commit(b);
+}
+
 // ---------------------------------------------------------------- softmax pieces
 // all N scores of this thread's TMEM lane, one wait
 template <int N>
@@ -205,10 +264,10 @@ __device__ __forceinline__ float row_max(const uint32_t (&s)[N]) {
 // for the row sum, F2FP to bf16 pairs, stored as the TS-MMA A operand over
 // the first N/2 columns of the S tile. Part j of P is released to PV_k on
 // part_bar[j] (see kPParts). Returns the row sum.
-template <int N, bool kMask>
+template <int N, bool kMask, bool P>
 __device__ __forceinline__ float exp_store_row(const uint32_t (&s)[N], uint32_t taddr, float sl, float m,
                                                uint64_t* part_bar) {
-  constexpr int kParts = N == 128 ? kPParts : 2;  // 64-key tiles keep halves
+  constexpr int kParts = N == 128 ? p_parts<P>() : 2;  // 64-key tiles keep halves
   constexpr int kPartKeys = N / kParts;
   constexpr int kKeys = kPartKeys < 32 ? kPartKeys : 32;  // keys per tcgen05.st chunk
   constexpr int kRegs = kKeys / 2;
@@ -240,7 +299,7 @@ __device__ __forceinline__ float exp_store_row(const uint32_t (&s)[N], uint32_t 
       // work ago: release it
       tmem_st_wait();
       tc_fence_before();
-      warp_arrive(&part_bar[c * kKeys / kPartKeys - 1]);
+      arrive_mma_<P>(&part_bar[c * kKeys / kPartKeys - 1]);
     }
     tmem_st<kRegs>(taddr + c * kRegs, pk);
   }
@@ -266,10 +325,17 @@ __device__ __forceinline__ float exp_store_row(const uint32_t (&s)[N], uint32_t 
 #ifndef TWFA_S_HALVES
 #define TWFA_S_HALVES 0  // measured: -5 % C3 (twice the MMA issues for S outweigh the earlier start)
 #endif
-template <int N, class Handoff, class WaitRest>
+// TWFA_TRACE_SUB (diagnostic builds): the traced MX record's fields 6 / 7
+// hold the clock after the row max / handoff and after the last exponential
+// instead of the work tile
+#ifndef TWFA_TRACE_SUB
+#define TWFA_TRACE_SUB 0
+#endif
+template <int N, bool P, class Handoff, class WaitRest>
 __device__ __forceinline__ float mx_ex_spec(uint32_t (&s)[N], uint32_t taddr, float sl, float& m_io, float& alpha,
-                                            uint64_t* part_bar, Handoff&& handoff, WaitRest&& wait_rest) {
-  constexpr int kParts = kPParts;
+                                            uint64_t* part_bar, Handoff&& handoff, WaitRest&& wait_rest,
+                                            uint32_t* trm = nullptr) {
+  constexpr int kParts = p_parts<P>();
   constexpr int kPartKeys = N / kParts;
   constexpr int kKeys = kPartKeys < 32 ? kPartKeys : 32;
   constexpr int kRegs = kKeys / 2;
@@ -292,7 +358,9 @@ __device__ __forceinline__ float mx_ex_spec(uint32_t (&s)[N], uint32_t taddr, fl
       const int e = c * kKeys + i;
       const float2 x = ffma2(make_float2(__uint_as_float(s[e]), __uint_as_float(s[e + 1])), sl2, nm2);
       float2 p;
-      if (((e >> 1) % kPolyEvery) == kPolyEvery - 1) {  // unmasked rows only: x is finite
+      if (TWFA_WHATIF == 1 && e >= N / 2) {
+        p = x;
+      } else if (((e >> 1) % kPolyEvery) == kPolyEvery - 1) {  // unmasked rows only: x is finite
         p = poly_exp2x2(x);
       } else {
         p.x = fast_exp2(x.x);
@@ -314,6 +382,7 @@ __device__ __forceinline__ float mx_ex_spec(uint32_t (&s)[N], uint32_t taddr, fl
   alpha = m_new == m_old ? 1.f : fast_exp2(m_old - m_new);
   m_io = m_new;
   handoff(alpha);
+  if (TWFA_TRACE_SUB && trm != nullptr) trm[6] = static_cast<uint32_t>(clock64());
   tmem_st<kRegs>(taddr, pk0);
 #pragma unroll
   for (int c = 1; c < N / kKeys; ++c) {
@@ -322,10 +391,11 @@ __device__ __forceinline__ float mx_ex_spec(uint32_t (&s)[N], uint32_t taddr, fl
     if ((c * kKeys) % kPartKeys == 0) {
       tmem_st_wait();
       tc_fence_before();
-      warp_arrive(&part_bar[c * kKeys / kPartKeys - 1]);
+      arrive_mma_<P>(&part_bar[c * kKeys / kPartKeys - 1]);
     }
     tmem_st<kRegs>(taddr + c * kRegs, pk);
   }
+  if (TWFA_TRACE_SUB && trm != nullptr) trm[7] = static_cast<uint32_t>(clock64());
   tmem_st_wait();
   return (acc[0].x + acc[0].y) + (acc[1].x + acc[1].y);
 }
@@ -338,6 +408,8 @@ struct FaCtx {
   uint8_t* o_smem;  // 16 KiB epilogue staging (one 128 x 64 bf16 half-tile, SW128)
   uint32_t tmem;
   uint32_t warp, lane, quad, lane_off;
+  uint32_t rank;  // CTA rank in the pair (0 = leader, issues the MMAs); 0 without pairs
+  int unit, units;  // this CTA's work unit (CTA or CTA pair) and their number
   int S, BH, q_blocks, num_work;
   int q_warp;  // idle warp loading the Q tiles (-1: the load warp does)
   float scale_log2;
@@ -351,9 +423,10 @@ struct WorkTile {
   uint32_t tcount;  // work tiles done by this CTA (Q / LSE buffer phases)
 };
 
-template <int KV>
+template <int KV, bool P>
 __device__ __forceinline__ WorkTile work_tile(const FaCtx& c, const FaArgs& args, int work, uint32_t gbase,
                                               uint32_t tcount) {
+  constexpr int kRows = 2 * kBlockQ * Kv<KV, P>::rows;  // query rows of a work tile
   WorkTile t;
   int qb;
   if (args.causal) {  // longest-processing-time first
@@ -363,12 +436,18 @@ __device__ __forceinline__ WorkTile work_tile(const FaCtx& c, const FaArgs& args
     t.bh = work / c.q_blocks;
     qb = work % c.q_blocks;
   }
-  t.q0 = qb * 2 * kBlockQ;
-  const int kv_end = args.causal ? min(c.S, t.q0 + 2 * kBlockQ) : c.S;
+  t.q0 = qb * kRows;
+  const int kv_end = args.causal ? min(c.S, t.q0 + kRows) : c.S;
   t.N = (kv_end + KV - 1) / KV;
   t.gbase = gbase;
   t.tcount = tcount;
   return t;
+}
+
+// First query row of this CTA's sub-tile k of a work tile
+template <int KV, bool P>
+__device__ __forceinline__ int sub_tile_row(const FaCtx& c, const WorkTile& t, int k) {
+  return t.q0 + k * kBlockQ * Kv<KV, P>::rows + static_cast<int>(c.rank) * kBlockQ;
 }
 
 // Number of leading keys of this K/V tile that row `row` may attend to
@@ -419,14 +498,14 @@ struct Maps {
 // ---------------------------------------------------------------- op bodies
 // One op of the trip program on this warp, trip r. Shared by both kernels:
 // with a compile-time `op` and `rg` every branch below folds.
-template <int KV, bool kHeavy, bool kTrace>
+template <int KV, bool kHeavy, bool kTrace, bool P>
 __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const FaCtx& c, const WorkTile& t,
                                         WarpState& st, const Rings rg, const Maps& tm, const FaArgs& args) {
   FaBarriers& bar = g_sh.bar;
   const uint32_t warp = c.warp, lane = c.lane;
   const uint32_t tmem = c.tmem;
   const int N = t.N;
-  using G = Kv<KV>;
+  using G = Kv<KV, P>;
 
   if (op.kind == TWFA_OP_LDK || op.kind == TWFA_OP_LDV) {
     if constexpr (!kHeavy) {
@@ -450,12 +529,23 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
         const uint32_t s = g % depth, ph = (g / depth) & 1;
         uint64_t* full = is_k ? &bar.k_full[s] : &bar.v_full[s];
         uint64_t* empty = is_k ? &bar.k_empty[s] : &bar.v_empty[s];
-        uint8_t* dst = (is_k ? c.k_smem : c.v_smem) + s * G::tile;
+        uint8_t* dst = (is_k ? c.k_smem : c.v_smem) + s * G::slot;
         const CUtensorMap* map = is_k ? tm.k : tm.v;
-        mbar_wait(empty, ph ^ 1);
+        if (!(TWFA_WHATIF == 6 && g >= 8u)) wait_<P>(empty, ph ^ 1);
         trace_mark<kTrace>(tr, 4);
         if (elect_one()) {
-          if (TWFA_WHATIF == 4 && g >= static_cast<uint32_t>(depth)) {
+          if constexpr (P) {
+            // this CTA's half: K keys 64r.. (both head-dim halves), V head
+            // dims 64r.. (all keys); both halves land on the leader's barrier
+            if (c.rank == 0) mbar_arrive_expect_tx(full, 2 * G::slot);
+            const int r0 = static_cast<int>(c.rank);
+            if (is_k) {
+              tma_load_3d_pair(dst, map, full, 0, key0 + r0 * (KV / 2), bh, c.pol_kv);
+              tma_load_3d_pair(dst + G::k_half, map, full, 64, key0 + r0 * (KV / 2), bh, c.pol_kv);
+            } else {
+              tma_load_3d_pair(dst, map, full, r0 * 64, key0, bh, c.pol_kv);
+            }
+          } else if (TWFA_WHATIF == 4 && g >= static_cast<uint32_t>(depth)) {
             mbar_arrive(full);  // what-if: the tile is already resident (no L2 -> SM traffic)
           } else {
             mbar_arrive_expect_tx(full, G::tile);
@@ -472,6 +562,11 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
   const int it = r - static_cast<int>(op.stage);
   if (it < 0 || it >= N) return;
   if (op.kind == TWFA_OP_EX && (op.flags & TWFA_OPF_FUSED)) return;  // done by MX_k
+  // the leader issues the pair's tensor-core ops (its MMA warp is the peer's
+  // load warp too, which only runs the loads of the program)
+  if (P && c.rank != 0 && (op.kind == TWFA_OP_S || op.kind == TWFA_OP_PV || op.kind == TWFA_OP_SA ||
+                           op.kind == TWFA_OP_SB))
+    return;
   const uint32_t g = t.gbase + static_cast<uint32_t>(it);
   const int k = op.tile;
   const uint32_t b = g % G::depth, pb = (g / G::depth) & 1;  // S buffer of this iteration, its phase
@@ -511,18 +606,31 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
     // descriptors, so they live in uniform registers; one elected lane
     // issues the tcgen05.mma chain and the commits
     const uint32_t s = g % rg.kd;
-    if (it == 0) mbar_wait(&bar.q_full[k], t.tcount & 1);
-    if (g >= G::depth && !(op.flags & TWFA_OPF_INORDER))  // K landed; P_k(g-depth) consumed by PV_k
-      mbar_wait_all(&bar.k_full[s], (g / rg.kd) & 1, &bar.o_done[k][b], pb ^ 1);
+    if (it == 0) wait_<P>(&bar.q_full[k], t.tcount & 1);
+    if ((TWFA_WHATIF == 5 || TWFA_WHATIF == 6) && g >= 8u) {
+    } else if (g >= G::depth && !(op.flags & TWFA_OPF_INORDER))  // K landed; P_k(g-depth) consumed by PV_k
+      wait_all_<P>(&bar.k_full[s], (g / rg.kd) & 1, &bar.o_done[k][b], pb ^ 1);
     else if (!TWFA_MEMO_WAITS || st.k_seen != g + 1)  // (the other sub-tile's S on this warp saw K(g) land)
-      mbar_wait(&bar.k_full[s], (g / rg.kd) & 1);
+      wait_<P>(&bar.k_full[s], (g / rg.kd) & 1);
     st.k_seen = g + 1;
     trace_mark<kTrace>(tr, 4);
     tc_fence_after();
     const uint32_t qd = sdesc_lo(smem_u32(c.q_smem + k * kTileBytes), 16);
-    const uint32_t kd = sdesc_lo(smem_u32(c.k_smem + s * G::tile), 16);
+    const uint32_t kd = sdesc_lo(smem_u32(c.k_smem + s * G::slot), 16);
     const uint32_t d_s = tmem + k * 128 + b * KV;
-    if (elect_one()) {
+    if constexpr (P) {
+      // M = 256 (Q_k of both CTAs), N = 128 keys (64 from each CTA's half)
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < kHeadDim / 16; ++kk)
+          mma_ss_pair(d_s, sdesc_join(qd + ((kk >> 2) * kHalfBytes + (kk & 3) * 32) / 16, kSdescHi),
+                      sdesc_join(kd + ((kk >> 2) * G::k_half + (kk & 3) * 32) / 16, kSdescHi), G::idesc_s, kk > 0);
+        commit_<P>(&bar.s_full[k][b]);
+        commit_<P>(&bar.k_empty[s]);
+        if (it == N - 1) commit_<P>(&bar.q_empty[k]);
+      }
+      __syncwarp();
+    } else if (elect_one()) {
       if (TWFA_S_HALVES && KV == 128) {
         // keys 0-63, committed on their own, then keys 64-127: the softmax
         // starts on the first half while the second is computed
@@ -550,7 +658,7 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
     const uint32_t s = g % rg.vd;
     // P_k arrives in two halves (keys 0-63, 64-127): the first four
     // K-steps of PV_k overlap the exponentials of the second half
-    constexpr int kParts = KV == 128 ? kPParts : 2;
+    constexpr int kParts = KV == 128 ? p_parts<P>() : 2;
     constexpr int kSteps = KV / 16 / kParts;  // K-steps (16 keys) per part
     // probe every input of the op at once (non-blocking test_wait: the
     // round trips overlap), then block only on what had not landed: a wait
@@ -559,13 +667,14 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
     // otherwise serialize four of them into PV's issue
     bool part_ready[kParts];
 #if TWFA_PROBE_PARTS
-    const bool v_ok = TWFA_MEMO_WAITS && st.v_seen == g + 1 ? true : mbar_test(&bar.v_full[s], (g / rg.vd) & 1);
-    const bool o_ok = mbar_test(&bar.o_ready[k][b], pb);
+    const bool skip = (TWFA_WHATIF == 5 || TWFA_WHATIF == 6) && g >= 8u;
+    const bool v_ok = skip || (TWFA_MEMO_WAITS && st.v_seen == g + 1) ? true : test_<P>(&bar.v_full[s], (g / rg.vd) & 1);
+    const bool o_ok = skip || test_<P>(&bar.o_ready[k][b], pb);
 #pragma unroll
-    for (int j = 0; j < kParts; ++j) part_ready[j] = mbar_test(&bar.p_part[k][b][j], pb);
-    if (!v_ok) mbar_wait(&bar.v_full[s], (g / rg.vd) & 1);
-    if (!o_ok) mbar_wait(&bar.o_ready[k][b], pb);
-    if (!part_ready[0]) mbar_wait(&bar.p_part[k][b][0], pb);
+    for (int j = 0; j < kParts; ++j) part_ready[j] = test_<P>(&bar.p_part[k][b][j], pb);
+    if (!v_ok) wait_<P>(&bar.v_full[s], (g / rg.vd) & 1);
+    if (!o_ok) wait_<P>(&bar.o_ready[k][b], pb);
+    if (!part_ready[0]) wait_<P>(&bar.p_part[k][b][0], pb);
 #else
 #pragma unroll
     for (int j = 0; j < kParts; ++j) part_ready[j] = false;
@@ -574,22 +683,27 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
     st.v_seen = g + 1;
     trace_mark<kTrace>(tr, 4);
     tc_fence_after();
-    const uint32_t vd = sdesc_lo(smem_u32(c.v_smem + s * G::tile), G::half);
+    const uint32_t vd = sdesc_lo(smem_u32(c.v_smem + s * G::slot), G::half);
     const uint32_t d_o = tmem + 256 + k * 128, a_p = tmem + k * 128 + b * KV + (rg.split ? 64u : 0u);
     const uint32_t acc0 = it > 0 ? 1u : 0u;
 #pragma unroll
     for (int j = 0; j < kParts; ++j) {
       if (j > 0 && !part_ready[j]) {
-        mbar_wait(&bar.p_part[k][b][j], pb);
+        wait_<P>(&bar.p_part[k][b][j], pb);
         tc_fence_after();
       }
       if (elect_one()) {
 #pragma unroll
-        for (int kk = j * kSteps; kk < (j + 1) * kSteps; ++kk)  // V is MN-major: 16 keys = 16 rows of 128 B
-          mma_ts(d_o, a_p + kk * 8, sdesc_join(vd + kk * 2048 / 16, kSdescHi), kIdescPV, kk > 0 ? 1u : acc0);
+        for (int kk = j * kSteps; kk < (j + 1) * kSteps; ++kk) {  // V is MN-major: 16 keys = 16 rows of 128 B
+          if constexpr (P)  // M = 256 (P_k of both CTAs), N = 128 head dims (64 from each CTA's half)
+            mma_ts_pair(d_o, a_p + kk * 8, sdesc_join(vd + kk * 2048 / 16, kSdescHi), G::idesc_pv,
+                        kk > 0 ? 1u : acc0);
+          else
+            mma_ts(d_o, a_p + kk * 8, sdesc_join(vd + kk * 2048 / 16, kSdescHi), kIdescPV, kk > 0 ? 1u : acc0);
+        }
         if (j == kParts - 1) {
-          mma_commit(&bar.o_done[k][b]);
-          mma_commit(&bar.v_empty[s]);
+          commit_<P>(&bar.o_done[k][b]);
+          commit_<P>(&bar.v_empty[s]);
         }
       }
       __syncwarp();
@@ -603,7 +717,7 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
     // not touched and the correction only forwards the handoff
     if (it > 0 && !__all_sync(0xffffffffu, alpha == 1.f)) {
       // O is read-modified-written: PV_k(g - 1) must have completed
-      mbar_wait(&bar.o_done[k][(g - 1) % G::depth], ((g - 1) / G::depth) & 1);
+      wait_<P>(&bar.o_done[k][(g - 1) % G::depth], ((g - 1) / G::depth) & 1);
       trace_mark<kTrace>(tr, 4);
       tc_fence_after();
 #pragma unroll 1
@@ -624,11 +738,11 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
       tmem_st_wait();
     }
     tc_fence_before();
-    warp_arrive(&bar.o_ready[k][b]);
+    arrive_mma_<P>(&bar.o_ready[k][b]);
   } else if (op.kind == TWFA_OP_MX || op.kind == TWFA_OP_EX) {
     if constexpr (kHeavy) {
       const uint32_t taddr = tmem + c.lane_off + k * 128 + b * KV;
-      const int row = t.q0 + k * kBlockQ + c.quad * 32 + lane;
+      const int row = sub_tile_row<KV, P>(c, t, k) + c.quad * 32 + lane;
       const int limit = valid_keys<KV>(args, row, it * KV);
       const bool mask = !__all_sync(0xffffffffu, limit >= KV);
       uint32_t srow[KV];
@@ -642,7 +756,7 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
         else if (TWFA_S_HALVES && spec)
           mbar_wait(&bar.s_lo[k][b], pb);  // keys 0-63; the rest is awaited inside the speculative EX
         else
-          mbar_wait(&bar.s_full[k][b], pb);
+          wait_<P>(&bar.s_full[k][b], pb);
         trace_mark<kTrace>(tr, 4);
         tc_fence_after();
         if constexpr (KV == 128) {
@@ -650,7 +764,7 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
           if (spec) {
             float m = m_old, alpha = 1.f;
             const uint32_t sb = g & 1;
-            const float sum = mx_ex_spec<KV>(srow, taddr, c.scale_log2, m, alpha, bar.p_part[k][b], [&](float al) {
+            const float sum = mx_ex_spec<KV, P>(srow, taddr, c.scale_log2, m, alpha, bar.p_part[k][b], [&](float al) {
               mbar_wait(&bar.st_empty[k][sb], ((g >> 1) & 1) ^ 1);
               g_sh.stats[k][sb][c.quad * 32 + lane] = al;
               warp_arrive(&bar.st_full[k][sb]);
@@ -659,12 +773,12 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
                 mbar_wait(&bar.s_full[k][b], pb);
                 tc_fence_after();
               }
-            });
+            }, tr);
             wr(st.m_run, k, m);
             wr(st.alpha, k, alpha);
             wr(st.l_run, k, rd(st.l_run, k) * alpha + sum);
             tc_fence_before();
-            warp_arrive(&bar.p_part[k][b][kPParts - 1]);
+            arrive_mma_<P>(&bar.p_part[k][b][p_parts<P>() - 1]);
             if (it == N - 1) {
               mbar_wait(&bar.l_empty[k], (t.tcount & 1) ^ 1);
               g_sh.lbuf[k][0][c.quad * 32 + lane] = m;
@@ -720,11 +834,11 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
       const float m_run = rd(st.m_run, k);
       const float m_safe = m_run == -INFINITY ? 0.f : m_run;
       const uint32_t paddr = taddr + (rg.split ? 64u : 0u);  // P_k columns
-      const float sum = mask ? exp_store_row<KV, true>(srow, paddr, c.scale_log2, m_safe, bar.p_part[k][b])
-                             : exp_store_row<KV, false>(srow, paddr, c.scale_log2, m_safe, bar.p_part[k][b]);
+      const float sum = mask ? exp_store_row<KV, true, P>(srow, paddr, c.scale_log2, m_safe, bar.p_part[k][b])
+                             : exp_store_row<KV, false, P>(srow, paddr, c.scale_log2, m_safe, bar.p_part[k][b]);
       wr(st.l_run, k, rd(st.l_run, k) * rd(st.alpha, k) + sum);
       tc_fence_before();
-      warp_arrive(&bar.p_part[k][b][(KV == 128 ? kPParts : 2) - 1]);
+      arrive_mma_<P>(&bar.p_part[k][b][(KV == 128 ? p_parts<P>() : 2) - 1]);
       if (tok) warp_arrive(&bar.sm_tok[k == rg.ring0 ? rg.ring1 : rg.ring0]);
       if (it == N - 1) {
         mbar_wait(&bar.l_empty[k], (t.tcount & 1) ^ 1);
@@ -737,16 +851,25 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
   trace_mark<kTrace>(tr, 5);
 }
 
-// Q sub-tiles of a new work tile (TMA warp, before its trip loop)
+// Q sub-tiles of a new work tile (TMA warp, before its trip loop). With CTA
+// pairs each CTA loads its own sub-tile rows onto the leader's barrier.
+template <int KV, bool P>
 __device__ __forceinline__ void load_q(const FaCtx& c, const WorkTile& t, int tiles, const Maps& tm) {
   FaBarriers& bar = g_sh.bar;
   for (int k = 0; k < tiles; ++k) {
-    mbar_wait(&bar.q_empty[k], (t.tcount & 1) ^ 1);
+    wait_<P>(&bar.q_empty[k], (t.tcount & 1) ^ 1);
     uint8_t* dst = c.q_smem + k * kTileBytes;
+    const int row = sub_tile_row<KV, P>(c, t, k);
     if (elect_one()) {
-      mbar_arrive_expect_tx(&bar.q_full[k], kTileBytes);
-      tma_load_3d(dst, tm.q, &bar.q_full[k], 0, t.q0 + k * kBlockQ, t.bh, c.pol_q);
-      tma_load_3d(dst + kHalfBytes, tm.q, &bar.q_full[k], 64, t.q0 + k * kBlockQ, t.bh, c.pol_q);
+      if constexpr (P) {
+        if (c.rank == 0) mbar_arrive_expect_tx(&bar.q_full[k], 2 * kTileBytes);
+        tma_load_3d_pair(dst, tm.q, &bar.q_full[k], 0, row, t.bh, c.pol_q);
+        tma_load_3d_pair(dst + kHalfBytes, tm.q, &bar.q_full[k], 64, row, t.bh, c.pol_q);
+      } else {
+        mbar_arrive_expect_tx(&bar.q_full[k], kTileBytes);
+        tma_load_3d(dst, tm.q, &bar.q_full[k], 0, row, t.bh, c.pol_q);
+        tma_load_3d(dst + kHalfBytes, tm.q, &bar.q_full[k], 64, row, t.bh, c.pol_q);
+      }
     }
     __syncwarp();
   }
@@ -754,18 +877,19 @@ __device__ __forceinline__ void load_q(const FaCtx& c, const WorkTile& t, int ti
 
 // Epilogue of sub-tile k on its correction warpgroup: O / l -> bf16 -> global,
 // LSE (the accumulator is final after the last PV_k).
-template <int KV>
+template <int KV, bool P>
 __device__ __forceinline__ void epilogue(const FaCtx& c, const WorkTile& t, int k, const FaArgs& args) {
   FaBarriers& bar = g_sh.bar;
   const uint32_t lane = c.lane;
   const uint32_t g_last = t.gbase + static_cast<uint32_t>(t.N - 1);
-  mbar_wait(&bar.o_done[k][g_last % Kv<KV>::depth], (g_last / Kv<KV>::depth) & 1);
+  wait_<P>(&bar.o_done[k][g_last % Kv<KV>::depth], (g_last / Kv<KV>::depth) & 1);
   mbar_wait(&bar.l_full[k], t.tcount & 1);
   const float m = g_sh.lbuf[k][0][c.quad * 32 + lane];
   const float l = g_sh.lbuf[k][1][c.quad * 32 + lane];
   warp_arrive(&bar.l_empty[k]);
   tc_fence_after();
-  const int row = t.q0 + k * kBlockQ + c.quad * 32 + lane;
+  const int row0 = sub_tile_row<KV, P>(c, t, k);
+  const int row = row0 + c.quad * 32 + lane;
   const float inv = l > 0.f ? 1.f / l : 0.f;
 #if TWFA_TMA_EPILOGUE
   // two 128 x 64 halves through the swizzled staging buffer and a bulk
@@ -794,7 +918,7 @@ __device__ __forceinline__ void epilogue(const FaCtx& c, const WorkTile& t, int 
     fence_proxy_async_shared();
     named_bar_sync(wg_bar, 128);
     if (leader) {
-      tma_store_3d(&args.tm_o, c.o_smem, h * 64, t.q0 + k * kBlockQ, t.bh);
+      tma_store_3d(&args.tm_o, c.o_smem, h * 64, row0, t.bh);
       bulk_commit();
       bulk_wait_read();  // the staging buffer is reusable
     }
@@ -830,16 +954,15 @@ __device__ __forceinline__ void epilogue(const FaCtx& c, const WorkTile& t, int 
 // The i-th work tile of this CTA: from the host's per-CTA list (causal:
 // load-balanced, (b, h)-grouped for L2 reuse of K / V), else round-robin
 // over the persistent CTAs.
-template <int KV>
+// A work unit is one CTA, or one CTA pair (both CTAs walk the same list).
 __device__ __forceinline__ int work_of(const FaCtx& c, const FaArgs& args, int i) {
   if (args.work_list != nullptr) {
-    const int o = args.work_off[blockIdx.x] + i;
-    return o < args.work_off[blockIdx.x + 1] ? args.work_list[o] : c.num_work;
+    const int o = args.work_off[c.unit] + i;
+    return o < args.work_off[c.unit + 1] ? args.work_list[o] : c.num_work;
   }
   // causal without a list: longest first, alternating the direction of each
-  // round over the persistent CTAs ("snake") to balance their totals
-  return i * static_cast<int>(gridDim.x) +
-         ((args.causal && (i & 1)) ? static_cast<int>(gridDim.x - 1 - blockIdx.x) : static_cast<int>(blockIdx.x));
+  // round over the persistent units ("snake") to balance their totals
+  return i * c.units + ((args.causal && (i & 1)) ? c.units - 1 - c.unit : c.unit);
 }
 
 // cross-tile prefetch (Q on an idle warp, the next tile's first K / V
@@ -847,7 +970,7 @@ __device__ __forceinline__ int work_of(const FaCtx& c, const FaArgs& args, int i
 #ifndef TWFA_XTILE
 #define TWFA_XTILE 1
 #endif
-template <int KV, class Trip>
+template <int KV, bool P, class Trip>
 __device__ __forceinline__ void work_loop(const FaCtx& c, const FaArgs& args, const Maps& tm, int tiles, int max_stage,
                                           bool is_load_warp, bool is_q_warp, const int* cr_warp, WarpState& st,
                                           Trip&& trip) {
@@ -855,20 +978,20 @@ __device__ __forceinline__ void work_loop(const FaCtx& c, const FaArgs& args, co
   st.k_next = st.v_next = 0;
   st.k_seen = st.v_seen = 0;
   for (int round = 0;; ++round, ++tcount) {
-    const int work = work_of<KV>(c, args, round);
+    const int work = work_of(c, args, round);
     if (work >= c.num_work) break;
-    const WorkTile t = work_tile<KV>(c, args, work, gbase, tcount);
+    const WorkTile t = work_tile<KV, P>(c, args, work, gbase, tcount);
     if (TWFA_XTILE && is_q_warp) {  // Q of every tile, as soon as the previous tile's last S_k released it
-      load_q(c, t, tiles, tm);
+      load_q<KV, P>(c, t, tiles, tm);
       gbase += static_cast<uint32_t>(t.N);
       continue;
     }
     if (is_load_warp) {
-      if (!TWFA_XTILE || !(c.q_warp >= 0)) load_q(c, t, tiles, tm);
-      const int nwork = work_of<KV>(c, args, round + 1);
+      if (!TWFA_XTILE || !(c.q_warp >= 0)) load_q<KV, P>(c, t, tiles, tm);
+      const int nwork = work_of(c, args, round + 1);
       st.next_N = 0;
       if (TWFA_XTILE && nwork < c.num_work) {
-        const WorkTile nt = work_tile<KV>(c, args, nwork, gbase + static_cast<uint32_t>(t.N), tcount + 1);
+        const WorkTile nt = work_tile<KV, P>(c, args, nwork, gbase + static_cast<uint32_t>(t.N), tcount + 1);
         st.next_bh = nt.bh;
         st.next_N = nt.N;
       }
@@ -885,7 +1008,7 @@ __device__ __forceinline__ void work_loop(const FaCtx& c, const FaArgs& args, co
     const int trips = t.N + max_stage;
     for (int r = -1; r < trips; ++r) trip(r, t);
     for (int k = 0; k < tiles; ++k)
-      if (static_cast<int>(c.warp & ~3u) == cr_warp[k]) epilogue<KV>(c, t, k, args);
+      if (static_cast<int>(c.warp & ~3u) == cr_warp[k]) epilogue<KV, P>(c, t, k, args);
     // iterations of the next tile already in flight keep their count
     st.k_next = max(0, st.k_next - t.N);
     st.v_next = max(0, st.v_next - t.N);
@@ -894,7 +1017,7 @@ __device__ __forceinline__ void work_loop(const FaCtx& c, const FaArgs& args, co
 }
 
 // Shared prologue of both kernels: smem carve-up, barriers, TMEM allocation.
-template <int KV>
+template <int KV, bool P>
 __device__ __forceinline__ FaCtx fa_setup(int tiles, int kd, int vd, int load_warp, int q_warp, int split,
                                           const FaArgs& args, const Maps& tm, uint8_t* smem_raw) {
   // 1 KiB alignment of the tile buffers (SW128 atoms) by offset arithmetic on
@@ -903,8 +1026,8 @@ __device__ __forceinline__ FaCtx fa_setup(int tiles, int kd, int vd, int load_wa
   FaCtx c;
   c.q_smem = smem;
   c.k_smem = c.q_smem + tiles * kTileBytes;
-  c.v_smem = c.k_smem + kd * Kv<KV>::tile;
-  c.o_smem = c.v_smem + vd * Kv<KV>::tile;
+  c.v_smem = c.k_smem + kd * Kv<KV, P>::slot;
+  c.o_smem = c.v_smem + vd * Kv<KV, P>::slot;
   FaBarriers& bar = g_sh.bar;
   c.warp = warp_id();
   c.lane = lane_id();
@@ -915,8 +1038,9 @@ __device__ __forceinline__ FaCtx fa_setup(int tiles, int kd, int vd, int load_wa
       mbar_init(&bar.q_empty[k], split ? 2 : 1);  // the last S GEMM(s) of the tile read Q_k
       for (int b = 0; b < 2; ++b) {
         mbar_init(&bar.s_full[k][b], 1);
-        for (int j = 0; j < kPParts; ++j) mbar_init(&bar.p_part[k][b][j], 4);  // warp arrivals of a warpgroup
-        mbar_init(&bar.o_ready[k][b], 4);
+        // warp arrivals of a warpgroup (of both CTAs' warpgroups: the leader's copy)
+        for (int j = 0; j < kPParts; ++j) mbar_init(&bar.p_part[k][b][j], 4 * Kv<KV, P>::rows);
+        mbar_init(&bar.o_ready[k][b], 4 * Kv<KV, P>::rows);
         mbar_init(&bar.o_done[k][b], 1);
       }
       for (int j = 0; j < 2; ++j) {
@@ -946,9 +1070,15 @@ __device__ __forceinline__ FaCtx fa_setup(int tiles, int kd, int vd, int load_wa
     tma_prefetch_desc(tm.k);
     tma_prefetch_desc(tm.v);
   }
-  if (c.warp == 0) tmem_alloc<512>(&bar.tmem_base);
-  tc_fence_before();
-  __syncthreads();
+  if constexpr (P) {
+    if (c.warp == 0) tmem_alloc_pair<512>(&bar.tmem_base);
+    tc_fence_before();
+    cluster_sync();  // both CTAs' barriers initialised and tensor memory allocated
+  } else {
+    if (c.warp == 0) tmem_alloc<512>(&bar.tmem_base);
+    tc_fence_before();
+    __syncthreads();
+  }
   tc_fence_after();
   // the CTA owns all 512 columns (one CTA per SM): the allocation starts at
   // column 0, lane 0, so the base is the compile-time constant 0
@@ -957,7 +1087,11 @@ __device__ __forceinline__ FaCtx fa_setup(int tiles, int kd, int vd, int load_wa
   c.scale_log2 = args.scale_log2;
   c.S = args.S;
   c.BH = args.B * args.H;
-  c.q_blocks = (c.S + 2 * kBlockQ - 1) / (2 * kBlockQ);
+  c.rank = P ? cluster_ctarank() : 0u;
+  c.unit = static_cast<int>(blockIdx.x) / Kv<KV, P>::rows;
+  c.units = static_cast<int>(gridDim.x) / Kv<KV, P>::rows;
+  constexpr int kRows = 2 * kBlockQ * Kv<KV, P>::rows;
+  c.q_blocks = (c.S + kRows - 1) / kRows;
   c.num_work = c.BH * c.q_blocks;
   c.quad = c.warp & 3u;               // TMEM lane quadrant of this warp
   c.lane_off = (c.quad * 32u) << 16;  // TMEM address lane field
@@ -966,13 +1100,22 @@ __device__ __forceinline__ FaCtx fa_setup(int tiles, int kd, int vd, int load_wa
   return c;
 }
 
+template <bool P>
 __device__ __forceinline__ void fa_teardown(const FaCtx& c) {
   if (c.lane == 0) bulk_wait_all();  // epilogue bulk stores of this warp (if any) are complete
   tc_fence_before();
-  __syncthreads();
-  if (c.warp == 0) {
-    tc_fence_after();
-    tmem_dealloc<512>(c.tmem);
+  if constexpr (P) {
+    cluster_sync();  // neither CTA leaves while the pair's MMAs may touch its memory
+    if (c.warp == 0) {
+      tc_fence_after();
+      tmem_dealloc_pair<512>(c.tmem);
+    }
+  } else {
+    __syncthreads();
+    if (c.warp == 0) {
+      tc_fence_after();
+      tmem_dealloc<512>(c.tmem);
+    }
   }
 }
 
@@ -986,22 +1129,22 @@ __device__ __forceinline__ void set_register_class(int heavy_wgs) {
 }
 
 // ---------------------------------------------------------------- interpreter
-template <int KV, bool kHeavy, bool kTrace>
+template <int KV, bool kHeavy, bool kTrace, bool P>
 __device__ __forceinline__ void run_interp(const FaCtx& c, const Maps& tm, const FaArgs& args, int tiles,
                                            int max_stage, int load_warp, const int* cr_warp, const Rings rg) {
   WarpState st;
   st.trace_n = 0;
   int plen = 0;
   while (plen < TWFA_MAX_NODES && g_sh.prog_len[c.warp] > plen) ++plen;
-  work_loop<KV>(c, args, tm, tiles, max_stage, !kHeavy && c.warp == static_cast<uint32_t>(load_warp),
+  work_loop<KV, P>(c, args, tm, tiles, max_stage, !kHeavy && c.warp == static_cast<uint32_t>(load_warp),
                 !kHeavy && static_cast<int>(c.warp) == c.q_warp, cr_warp, st,
                 [&](int r, const WorkTile& t) {
                   for (int j = 0; j < plen; ++j)
-                    exec_op<KV, kHeavy, kTrace>(g_sh.prog[c.warp][j], r, c, t, st, rg, tm, args);
+                    exec_op<KV, kHeavy, kTrace, P>(g_sh.prog[c.warp][j], r, c, t, st, rg, tm, args);
             });
 }
 
-template <int KV, bool kTrace>
+template <int KV, bool kTrace, bool P>
 __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
     fa_fwd_interp(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                   const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ TwfaDevicePlan plan,
@@ -1013,20 +1156,20 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
     if (j < plan.prog_len[w]) g_sh.prog[w][j] = plan.ops[plan.prog[w][j]];
     if (j == 0) g_sh.prog_len[w] = plan.prog_len[w];
   }
-  const FaCtx c = fa_setup<KV>(plan.num_tiles, plan.k_depth, plan.v_depth, plan.load_warp, plan.q_warp, plan.s_split,
-                               args, tm, smem_raw);
+  const FaCtx c = fa_setup<KV, P>(plan.num_tiles, plan.k_depth, plan.v_depth, plan.load_warp, plan.q_warp,
+                                  plan.s_split, args, tm, smem_raw);
   const Rings rg{plan.k_depth,   plan.v_depth,    plan.k_prefetch, plan.v_prefetch,
                  plan.ex_ring_len, plan.ex_ring[0], plan.ex_ring[1], plan.s_split};
   const bool heavy = (plan.heavy_wg_mask >> (c.warp >> 2)) & 1;
   const int heavy_wgs = __popc(plan.heavy_wg_mask);
   if (heavy) {
     set_register_class<true>(heavy_wgs);
-    run_interp<KV, true, kTrace>(c, tm, args, plan.num_tiles, plan.max_stage, plan.load_warp, plan.cr_warp, rg);
+    run_interp<KV, true, kTrace, P>(c, tm, args, plan.num_tiles, plan.max_stage, plan.load_warp, plan.cr_warp, rg);
   } else {
     set_register_class<false>(heavy_wgs);
-    run_interp<KV, false, kTrace>(c, tm, args, plan.num_tiles, plan.max_stage, plan.load_warp, plan.cr_warp, rg);
+    run_interp<KV, false, kTrace, P>(c, tm, args, plan.num_tiles, plan.max_stage, plan.load_warp, plan.cr_warp, rg);
   }
-  fa_teardown(c);
+  fa_teardown<P>(c);
 }
 
 // ---------------------------------------------------------------- specialized
@@ -1061,17 +1204,17 @@ __device__ __forceinline__ void fill_progs(int w, int j, std::integer_sequence<i
   ((w == W ? fill_warp_prog<I, W>(j, std::make_integer_sequence<int, TWFA_PLAN(I).prog_len[W]>{}) : void()), ...);
 }
 
-template <int I, int W, bool kTrace, int... J>
+template <int I, int W, bool kTrace, bool P, int... J>
 __device__ __forceinline__ void spec_trip(int r, const FaCtx& c, const WorkTile& t, WarpState& st, const Maps& tm,
                                           const FaArgs& args, std::integer_sequence<int, J...>) {
   constexpr bool kHeavy = (TWFA_PLAN(I).heavy_wg_mask >> (W / 4)) & 1;
   constexpr Rings rg{TWFA_PLAN(I).k_depth,    TWFA_PLAN(I).v_depth,    TWFA_PLAN(I).k_prefetch,
                      TWFA_PLAN(I).v_prefetch, TWFA_PLAN(I).ex_ring_len, TWFA_PLAN(I).ex_ring[0],
                      TWFA_PLAN(I).ex_ring[1], TWFA_PLAN(I).s_split};
-  (exec_op<TWFA_PLAN(I).kv_tile, kHeavy, kTrace>(spec_op<I, W, J>(), r, c, t, st, rg, tm, args), ...);
+  (exec_op<TWFA_PLAN(I).kv_tile, kHeavy, kTrace, P>(spec_op<I, W, J>(), r, c, t, st, rg, tm, args), ...);
 }
 
-template <int I, int W, bool kTrace>
+template <int I, int W, bool kTrace, bool P>
 __device__ __forceinline__ void run_spec(const FaCtx& c, const Maps& tm, const FaArgs& args) {
   constexpr bool kHeavy = (TWFA_PLAN(I).heavy_wg_mask >> (W / 4)) & 1;
   constexpr int plen = TWFA_PLAN(I).prog_len[W];
@@ -1079,10 +1222,10 @@ __device__ __forceinline__ void run_spec(const FaCtx& c, const Maps& tm, const F
   constexpr int cr_warp[TWFA_MAX_TILES] = {TWFA_PLAN(I).cr_warp[0], TWFA_PLAN(I).cr_warp[1]};
   WarpState st;
   st.trace_n = 0;
-  work_loop<TWFA_PLAN(I).kv_tile>(c, args, tm, TWFA_PLAN(I).num_tiles, TWFA_PLAN(I).max_stage, kLoad,
+  work_loop<TWFA_PLAN(I).kv_tile, P>(c, args, tm, TWFA_PLAN(I).num_tiles, TWFA_PLAN(I).max_stage, kLoad,
                                   !kHeavy && static_cast<int>(c.warp) == c.q_warp, cr_warp, st,
             [&](int r, const WorkTile& t) {
-              spec_trip<I, W, kTrace>(r, c, t, st, tm, args, std::make_integer_sequence<int, plen>{});
+              spec_trip<I, W, kTrace, P>(r, c, t, st, tm, args, std::make_integer_sequence<int, plen>{});
             });
 }
 
@@ -1090,18 +1233,18 @@ __device__ __forceinline__ void run_spec(const FaCtx& c, const Maps& tm, const F
 // program, one instantiation per distinct role; softmax warpgroups run the
 // runtime interpreter over the same plan (a single shared copy of the large
 // MX/EX bodies keeps the kernel within the instruction cache).
-template <int I, bool kTrace, int... W>
+template <int I, bool kTrace, bool P, int... W>
 __device__ __forceinline__ void spec_dispatch_light(const FaCtx& c, const Maps& tm, const FaArgs& args,
                                                     std::integer_sequence<int, W...>) {
   int role = -1;
   ((c.warp == static_cast<uint32_t>(W) ? (void)(role = gen::PlanOf<I>::role[W]) : void()), ...);
   ((!((TWFA_PLAN(I).heavy_wg_mask >> (W / 4)) & 1) && gen::PlanOf<I>::role[W] == W && role == W
-        ? run_spec<I, W, kTrace>(c, tm, args)
+        ? run_spec<I, W, kTrace, P>(c, tm, args)
         : void()),
    ...);
 }
 
-template <int I, bool kTrace>
+template <int I, bool kTrace, bool P>
 __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
     fa_fwd_spec(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                 const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ FaArgs args) {
@@ -1111,7 +1254,7 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
     fill_progs<I>(i / TWFA_MAX_NODES, i % TWFA_MAX_NODES, std::make_integer_sequence<int, TWFA_MAX_WARPS>{});
   constexpr int cr_warp[TWFA_MAX_TILES] = {TWFA_PLAN(I).cr_warp[0], TWFA_PLAN(I).cr_warp[1]};
   constexpr int KV = TWFA_PLAN(I).kv_tile;
-  const FaCtx c = fa_setup<KV>(TWFA_PLAN(I).num_tiles, TWFA_PLAN(I).k_depth, TWFA_PLAN(I).v_depth,
+  const FaCtx c = fa_setup<KV, P>(TWFA_PLAN(I).num_tiles, TWFA_PLAN(I).k_depth, TWFA_PLAN(I).v_depth,
                                TWFA_PLAN(I).load_warp, TWFA_PLAN(I).q_warp, TWFA_PLAN(I).s_split, args, tm, smem_raw);
   // the register class is per warpgroup; the warp roles of each class are
   // dispatched inside its branch so ptxas allocates them under that budget
@@ -1120,16 +1263,16 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
   constexpr int nw = TWFA_PLAN(I).num_warps;
   if ((mask >> (c.warp >> 2)) & 1) {
     set_register_class<true>(heavy_wgs);
-    run_interp<KV, true, kTrace>(c, tm, args, TWFA_PLAN(I).num_tiles, TWFA_PLAN(I).max_stage, TWFA_PLAN(I).load_warp,
+    run_interp<KV, true, kTrace, P>(c, tm, args, TWFA_PLAN(I).num_tiles, TWFA_PLAN(I).max_stage, TWFA_PLAN(I).load_warp,
                              cr_warp, Rings{TWFA_PLAN(I).k_depth, TWFA_PLAN(I).v_depth, TWFA_PLAN(I).k_prefetch,
                                             TWFA_PLAN(I).v_prefetch, TWFA_PLAN(I).ex_ring_len,
                                             TWFA_PLAN(I).ex_ring[0], TWFA_PLAN(I).ex_ring[1],
                                             TWFA_PLAN(I).s_split});
   } else {
     set_register_class<false>(heavy_wgs);
-    spec_dispatch_light<I, kTrace>(c, tm, args, std::make_integer_sequence<int, nw>{});
+    spec_dispatch_light<I, kTrace, P>(c, tm, args, std::make_integer_sequence<int, nw>{});
   }
-  fa_teardown(c);
+  fa_teardown<P>(c);
 }
 
 bool same_plan(const TwfaDevicePlan& a, const TwfaDevicePlan& b) {
@@ -1156,12 +1299,29 @@ bool same_plan(const TwfaDevicePlan& a, const TwfaDevicePlan& b) {
   return true;
 }
 
+// `cluster` = 2 launches CTA pairs (clusters of two CTAs on one TPC)
 template <class Kernel, class... Args>
-cudaError_t launch(Kernel kernel, size_t smem, int grid, int threads, cudaStream_t stream, Args... args) {
+cudaError_t launch(Kernel kernel, size_t smem, int grid, int threads, cudaStream_t stream, int cluster,
+                   Args... args) {
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  kernel<<<grid, threads, smem, stream>>>(args...);
-  return cudaGetLastError();
+  if (cluster <= 1) {
+    kernel<<<grid, threads, smem, stream>>>(args...);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(static_cast<unsigned>(threads));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = static_cast<unsigned>(cluster);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
 }  // namespace

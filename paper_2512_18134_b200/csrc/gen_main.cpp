@@ -105,6 +105,7 @@ int main(int argc, char** argv) {
     return 2;
   }
   std::string body, list;
+  std::vector<bool> pair_capable;  // 128-key K/V tiles, unsplit S, two Q sub-tiles (fa_fwd_pair_capable)
   int id = 0;
   try {
     for (int i = 2; i + 2 < argc; i += 3) {
@@ -112,6 +113,7 @@ int main(int argc, char** argv) {
       const twfa::LoweredSchedule s = twfa::lower(slurp(argv[i + 1]), slurp(argv[i + 2]));
       if (s.plan.family != TWFA_FAMILY_FA_FWD) continue;  // the GEMM kernel has a single fixed role layout
       body += emit(id, name, s, std::string(argv[i + 2]).substr(std::string(argv[i + 2]).rfind('/') + 1));
+      pair_capable.push_back(s.plan.kv_tile == 128 && !s.plan.s_split && s.plan.num_tiles == 2);
       list += " X(" + std::to_string(id++) + ")";
     }
   } catch (const std::exception& e) {
@@ -128,15 +130,21 @@ int main(int argc, char** argv) {
   for (int i = 0; i < id; ++i) {
     decl << "cudaError_t launch_spec_" << i
          << "(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const FaArgs& args, size_t smem,\n"
-            "                          int grid, int threads, cudaStream_t stream, bool trace);\n";
+            "                          int grid, int threads, cudaStream_t stream, bool trace, bool pair);\n";
     std::ofstream tu(dir + "fa_spec_" + std::to_string(i) + ".cu");
     tu << "// GENERATED by twfa-gen: kernel specialization " << i << " (gen::PlanOf<" << i << ">).\n"
           "#include <fa_fwd_kernel.cuh>\n#include <gen/fa_spec_launch.h>\n\nnamespace twfa {\nnamespace gen {\n"
           "cudaError_t launch_spec_" << i
        << "(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const FaArgs& args, size_t smem,\n"
-          "                          int grid, int threads, cudaStream_t stream, bool trace) {\n"
-          "  return trace ? launch(fa_fwd_spec<" << i << ", true>, smem, grid, threads, stream, tq, tk, tv, args)\n"
-          "               : launch(fa_fwd_spec<" << i << ", false>, smem, grid, threads, stream, tq, tk, tv, args);\n"
+          "                          int grid, int threads, cudaStream_t stream, bool trace, bool pair) {\n";
+    if (pair_capable[i])
+      tu << "  if (pair)\n"
+            "    return trace ? launch(fa_fwd_spec<" << i << ", true, true>, smem, grid, threads, stream, 2, tq, tk, tv, args)\n"
+            "                 : launch(fa_fwd_spec<" << i << ", false, true>, smem, grid, threads, stream, 2, tq, tk, tv, args);\n";
+    else
+      tu << "  if (pair) return cudaErrorInvalidValue;  // no CTA-pair realization of this plan\n";
+    tu << "  return trace ? launch(fa_fwd_spec<" << i << ", true, false>, smem, grid, threads, stream, 1, tq, tk, tv, args)\n"
+          "               : launch(fa_fwd_spec<" << i << ", false, false>, smem, grid, threads, stream, 1, tq, tk, tv, args);\n"
           "}\n}  // namespace gen\n}  // namespace twfa\n";
   }
   decl << "}  // namespace gen\n}  // namespace twfa\n";

@@ -292,19 +292,43 @@ TWFA_DEV uint32_t mapa_rank(const void* p, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
   return r;
 }
-// release-arrive on a barrier of either CTA of the cluster (shared::cluster
-// address from mapa_rank)
+// arrive on a barrier of either CTA of the cluster (shared::cluster address
+// from mapa_rank). TWFA_REMOTE_SEM selects the semantics: 0 = release at
+// CTA scope (what the producer's own tcgen05 / shared writes need: they are
+// ordered by tcgen05.fence::before_thread_sync and read by the leader's
+// tensor core), 1 = release at cluster scope.
+#ifndef TWFA_REMOTE_SEM
+#define TWFA_REMOTE_SEM 0
+#endif
 TWFA_DEV void mbar_arrive_cluster(uint32_t cluster_addr) {
+#if TWFA_REMOTE_SEM == 1
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+#else
+  asm volatile("mbarrier.arrive.release.cta.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+#endif
 }
-// one arrival per warp on a barrier of CTA `rank` (see warp_arrive)
+// one arrival per warp on a barrier of CTA `rank` (see warp_arrive); a local
+// barrier takes the plain arrive
 TWFA_DEV void warp_arrive_cluster(uint64_t* bar, uint32_t rank) {
   __syncwarp();
-  if ((threadIdx.x & 31u) == 0) mbar_arrive_cluster(mapa_rank(bar, rank));
+  if ((threadIdx.x & 31u) == 0) {
+    if (cluster_ctarank() == rank)
+      mbar_arrive(bar);
+    else
+      mbar_arrive_cluster(mapa_rank(bar, rank));
+  }
 }
-// wait with cluster-scope acquire: the phase may complete through arrivals
-// from the peer CTA, whose prior writes must be visible here
+// Waits on a barrier that receives arrivals from the peer CTA. The data they
+// publish (tensor memory written by tcgen05.st, shared memory written by TMA
+// or read by the tensor core) is ordered by the tcgen05 fences and the
+// barrier itself, so acquire at CTA scope suffices (as CUTLASS's cluster
+// barriers do); TWFA_CLUSTER_ACQUIRE=1 acquires at cluster scope, which
+// ptxas lowers with an L1 invalidation (CCTL.IVALL) per wait.
+#ifndef TWFA_CLUSTER_ACQUIRE
+#define TWFA_CLUSTER_ACQUIRE 0
+#endif
 TWFA_DEV bool mbar_try_wait_cluster(uint64_t* bar, uint32_t parity) {
+#if TWFA_CLUSTER_ACQUIRE
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -314,8 +338,12 @@ TWFA_DEV bool mbar_try_wait_cluster(uint64_t* bar, uint32_t parity) {
       : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
   return ok != 0;
+#else
+  return mbar_try_wait(bar, parity);
+#endif
 }
 TWFA_DEV bool mbar_test_cluster(uint64_t* bar, uint32_t parity) {
+#if TWFA_CLUSTER_ACQUIRE
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -325,6 +353,9 @@ TWFA_DEV bool mbar_test_cluster(uint64_t* bar, uint32_t parity) {
       : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
   return ok != 0;
+#else
+  return mbar_test(bar, parity);
+#endif
 }
 TWFA_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait_cluster(bar, parity)) {

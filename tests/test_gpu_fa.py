@@ -289,3 +289,33 @@ def test_causal_work_lists_do_not_change_results(twfa, plan, monkeypatch):
     without = twfa.fa_fwd(plan, q, k, v, causal=True)
     torch.cuda.synchronize()
     assert torch.equal(with_lists, without)
+
+
+@pytest.mark.parametrize("B,H,S,causal", [(1, 2, 512, False), (1, 2, 640, True), (2, 3, 300, False),
+                                          (1, 1, 100, True), (2, 48, 1664, True), (4, 40, 1024, False)])
+@pytest.mark.parametrize("kernel", ["specialized", "interpreter"])
+def test_cta_pair_matches_single_cta(twfa, plan, B, H, S, causal, kernel, monkeypatch):
+    """The CTA-pair realization (cta_group::2: one M = 256 MMA covers sub-tile
+    k of both CTAs; each CTA stages half of every K tile and half of every V
+    tile; the softmax / correction warps of the peer arrive on the leader's
+    barriers) computes every product and sum in the same order as one CTA per
+    work tile: bit-identical O and LSE. Covers work tiles past the sequence
+    end (S < 512: the peer's rows are all out of range), ragged S, causal
+    work lists indexed by pair, and more pair tiles than pairs."""
+    if kernel == "interpreter":
+        monkeypatch.setenv("TWFA_KERNEL", "interpreter")
+    q, k, v = (x.cuda() for x in _inputs(B, H, S, 128, 31))
+    monkeypatch.setenv("TWFA_PAIR", "1")
+    o_pair, l_pair = twfa.fa_fwd(plan, q, k, v, causal=causal, return_lse=True)
+    torch.cuda.synchronize()
+    monkeypatch.setenv("TWFA_PAIR", "0")
+    o_one, l_one = twfa.fa_fwd(plan, q, k, v, causal=causal, return_lse=True)
+    torch.cuda.synchronize()
+    assert torch.equal(o_pair, o_one)
+    assert torch.equal(l_pair, l_one)
+
+
+def test_cta_pair_against_oracle(twfa, plan, monkeypatch):
+    monkeypatch.setenv("TWFA_PAIR", "1")
+    _check(twfa, plan, 1, 3, 1000, True, 32)
+    _check(twfa, plan, 1, 3, 768, False, 33)

@@ -90,8 +90,12 @@ def _validate(prob, sol, m_real, a_real):
     assert m_real == solution["M"] and a_real == solution["A"]
 
 
+@pytest.mark.parametrize("pair", ["0", "1"])
 @pytest.mark.parametrize("name", fwd_schedules())
-def test_realized_forward_schedule_is_the_solution(twfa, name):
+def test_realized_forward_schedule_is_the_solution(twfa, name, pair, monkeypatch):
+    """pair = 1: the CTA-pair realization where the plan allows it (CTA 0 is
+    the leader, which issues the pair's tensor-core ops)."""
+    monkeypatch.setenv("TWFA_PAIR", pair)
     prob, sol = twfa.load_schedule(name)
     plan = twfa.Plan(prob, sol)
     desc, per_warp = traced_fwd(twfa, plan, 1, 1, 2048, False)
@@ -100,12 +104,14 @@ def test_realized_forward_schedule_is_the_solution(twfa, name):
     _validate(prob, sol, m_real, a_real)
 
 
+@pytest.mark.parametrize("pair", ["0", "1"])
 @pytest.mark.parametrize("B,H,S,causal", [(1, 80, 1024, False), (2, 48, 2048, True), (1, 160, 1280, True)])
-def test_realized_forward_schedule_over_many_work_tiles(twfa, B, H, S, causal):
+def test_realized_forward_schedule_over_many_work_tiles(twfa, B, H, S, causal, pair, monkeypatch):
     """Several work tiles per CTA: the next tile's Q (idle-warp loader) and
     first K / V iterations stream in while the current one drains; causal
-    launches run the host's per-CTA work lists (tiles of different lengths,
-    longest first, (b, h)-grouped)."""
+    launches run the host's per-CTA (per-pair) work lists (tiles of different
+    lengths, longest first, (b, h)-grouped)."""
+    monkeypatch.setenv("TWFA_PAIR", pair)
     prob, sol = twfa.load_schedule("fa_fwd")
     plan = twfa.Plan(prob, sol)
     desc, per_warp = traced_fwd(twfa, plan, B, H, S, causal)
