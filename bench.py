@@ -76,6 +76,7 @@ class ClockSampler:
     def __init__(self, device):
         self.device = device
         self.samples = []
+        self.power = []
         self.reasons = set()
         self.max_mhz = None
         self._stop = threading.Event()
@@ -108,6 +109,7 @@ class ClockSampler:
                 while not self._stop.is_set():
                     try:
                         self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                        self.power.append(pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0)
                         r = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
                         for n, bit in names.items():
                             if r & bit:
@@ -130,8 +132,9 @@ class ClockSampler:
     def summary(self):
         s = sorted(self.samples)
         med = s[len(s) // 2] if s else None
+        pw = sorted(self.power)
         return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-                "samples": len(s)}
+                "samples": len(s), "power_w": round(pw[len(pw) // 2], 1) if pw else None}
 
 
 # ---------------------------------------------------------------- ranks
@@ -542,12 +545,17 @@ def run_ours(args, ranks):
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": None,
                      "peak_kind": f"{peak_kind} bf16 burst (MEASURED_PEAKS.json)",
-                     "kernel": "twfa::fa_fwd_spec (" + desc_plan.get("kernel", "?") + ")",
+                     "kernel": "twfa::fa_fwd_spec (" + desc_plan.get("kernel", "?") + ", "
+                               + ("CTA pairs, cta_group::2" if desc_plan.get("cta_pair") else "one CTA per tile")
+                               + ")",
                      "flops_per_launch": flops_local, "launch_ms": per_launch_ms,
                      "spec_peak_at_sampled_clock": sms * SM_FLOP_PER_CLK * sm_mhz * 1e6 / 1e12},
         "tensor_pipe": {"busy_frac_from_run": tensor_pipe_run, "sm_mhz": sm_mhz,
                         "how": "algorithmic flops per launch / (SMs x 8192 flop/clk x sampled SM clock x launch "
-                               "time), this run"},
+                               "time), this run (NVML median SM clock during the timed region)",
+                        "power_w": clocks.get("power_w"),
+                        "note": "under sustained load the 1000 W board limit (sw_power_cap) sets the SM clock; "
+                                "this per-clock fraction is the clock-independent figure (DESIGN.md 10)"},
         "clocks": clocks,
         "per_rank": per_rank,
         "job_checksum": {"digest": digest, "pairs": int(cks.numel()),

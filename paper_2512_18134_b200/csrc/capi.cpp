@@ -247,8 +247,11 @@ struct DeviceGuard {
 // CTA pairs (cta_group::2) for the forward when the plan allows them;
 // TWFA_PAIR=0 keeps one CTA per work tile (comparison runs)
 bool use_pairs(const TwfaDevicePlan& p) {
+  if (!twfa::fa_fwd_pair_capable(p)) return false;
+  // rings that only fit in shared memory with half K / V tiles per CTA
+  if (twfa::fa_fwd_smem_bytes(p, false) > 216 * 1024 + 1024 + 16384) return true;
   const char* e = std::getenv("TWFA_PAIR");
-  return twfa::fa_fwd_pair_capable(p) && !(e && std::strcmp(e, "0") == 0);
+  return !(e && std::strcmp(e, "0") == 0);
 }
 
 // TWFA_WORK_LISTS=0 keeps the arithmetic causal order (comparison runs)

@@ -32,6 +32,7 @@ cudaError_t fa_fwd_launch(const CUtensorMap& tq, const CUtensorMap& tk, const CU
                           bool allow_specialized, bool pair) {
   if (pair && (!fa_fwd_pair_capable(plan) || grid % 2 != 0)) return cudaErrorInvalidValue;
   const size_t smem = fa_fwd_smem_bytes(plan, pair);
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;  // deep rings need the CTA-pair realization
   const int threads = plan.num_warps * 32;
   const bool trace = args.trace != nullptr;
   if (allow_specialized) {

@@ -647,7 +647,11 @@ void derive(LoweredSchedule& s) {
   const int64_t kv_bytes = static_cast<int64_t>(p.kv_tile) * 256;
   // + 16 KiB epilogue staging; 227 KiB per CTA minus the static state
   // (barriers, row statistics, trip programs ~10 KiB) and alignment slack
-  const int64_t smem = 32768LL * tiles + kv_bytes * (p.k_depth + p.v_depth) + 16384;
+  // A plan the CTA-pair realization can run (128-key tiles, unsplit S, two
+  // sub-tiles) stages half of every K / V tile per CTA, so deeper rings fit
+  // there (the launch then requires pairs, capi.cpp use_pairs)
+  const bool pair_capable = p.kv_tile == 128 && !split && tiles == 2;
+  const int64_t smem = 32768LL * tiles + kv_bytes / (pair_capable ? 2 : 1) * (p.k_depth + p.v_depth) + 16384;
   if (p.k_depth > 4 || p.v_depth > 4) throw DomainError("ring depth above 4");
   if (smem > 216 * 1024) throw DomainError("ring depths exceed shared memory");
   // Q tiles are loaded once per work tile, outside the loop body: an idle

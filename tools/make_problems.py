@@ -387,6 +387,9 @@ def main():
         # units of 256 clk, measured by the in-kernel trace); U = 9 normalizes
         # {256, 512, 1536} exactly (F = 0)
         "fa_fwd": (fa_forward_problem(tc_variable_latency=True, calibrated=True), 2, 9),
+        # (stream_depth 3 and 4 give the same M / A with deeper K / V rings,
+        # which fit with the CTA-pair realization: measured equal, not kept;
+        # profiles/r02c_notes.md)
         # variable latency with the datasheet costs (EX 4, MX 1)
         "fa_fwd_vl": (fa_forward_problem(tc_variable_latency=True), 2, None),
         # comparison: MMAs as fixed-latency ops (the solver scatters them over warps)
