@@ -130,7 +130,12 @@ struct BwdState {
   int q_next, o_next;      // next Q / dO iteration to load (TMA warp)
   int q_target, o_target;  // loads the trip program has asked for so far
   uint32_t trace_n;        // records of this warp in the issue trace
+  uint32_t* rec;           // the current op's trace record (t_ready stamped after its waits)
 };
+// t_ready of the current op's trace record: its inputs have been awaited
+__device__ __forceinline__ void bwd_ready(BwdState& st) {
+  if (st.rec != nullptr) st.rec[4] = static_cast<uint32_t>(clock64());
+}
 
 // Issue trace (CTA 0, lane 0 of every warp): one record per op instance,
 // the same layout as the forward's (fa_fwd_kernel.cuh)
@@ -203,7 +208,7 @@ __device__ __forceinline__ void stage_tile_vec(float* dst, float v, uint32_t r, 
 // EXB: P^T row of this thread (key kv0 + r) for Q tile q0, stored to TMEM as
 // bf16 over S^T; the fp32 values stay in p[] for a fused DS.
 __device__ __forceinline__ void exb_part(const BwdCtx& c, const FaBwdArgs& a, const BwdItem& t, int it, uint32_t g,
-                                         uint32_t (&p)[kT]) {
+                                         uint32_t (&p)[kT], BwdState& st) {
   BwdBarriers& bar = g_bb;
   const int q0 = (t.q_first + it) * kT;
   const uint32_t r = c.quad * 32 + c.lane;
@@ -215,6 +220,7 @@ __device__ __forceinline__ void exb_part(const BwdCtx& c, const FaBwdArgs& a, co
   const float my_lse2 = qt < c.S ? a.lse[row0 + r] * kLog2e : INFINITY;  // rows past S: P = 0
   mbar_wait(&bar.s_full, g & 1);
   tc_fence_after();
+  bwd_ready(st);
   // chunk 0 of the S^T row first; the rest streams in from tensor memory
   // while chunk 0 is exponentiated (and while the LSE is staged)
   tmem_ld32(c.lane_off + kColS, *reinterpret_cast<uint32_t(*)[32]>(&p[0]));
@@ -331,7 +337,7 @@ __device__ __forceinline__ void ds_part(const BwdCtx& c, const FaBwdArgs& a, con
 // 128 rows x 32 columns) -> cp.reduce.async.bulk add into the fp32 dQ
 // accumulator (the atomic reduction of the paper's backward loop).
 __device__ __forceinline__ void rd_op(const BwdCtx& c, const FaBwdArgs& a, const BwdItem& t, int it, uint32_t g,
-                                      const TwfaDevicePlan& plan) {
+                                      const TwfaDevicePlan& plan, BwdState& st) {
   // staging buffer: Q_i's ring slot when the schedule says so (plan.s_split
   // for the backward family; DK_i is complete once DQ_i is), else dS's
   const bool q_stage = plan.s_split != 0;
@@ -344,6 +350,7 @@ __device__ __forceinline__ void rd_op(const BwdCtx& c, const FaBwdArgs& a, const
   const uint32_t nb = 1 + (c.warp >> 2);  // named barrier of this warpgroup
   mbar_wait(&bar.dq_full, g & 1);
   tc_fence_after();
+  bwd_ready(st);
   if (TWFA_BWD_RED) {
     // the dS buffer is not used for staging: DS(i+1) may proceed (with Q-slot
     // staging DQ's commit frees it, and RD releases the unused Q slot)
@@ -502,6 +509,7 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
       if (e) e[5] = static_cast<uint32_t>(clock64());
     }
   } trace_done_{a.trace != nullptr ? bwd_trace(a, c, st, op.node, it, r, t) : nullptr};
+  st.rec = trace_done_.e;
 #if TWFA_BWD_PROF
   const bool prof = blockIdx.x == 0 && c.lane == 0 && (c.warp & 3u) == 3 && t.icount == 0 && (it == 20 || it == 21);
   struct Out {
@@ -523,7 +531,7 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
     if constexpr (kRole == kExbDs || kRole == kExb || kRole == kDs) {
       uint32_t p[kT];
       if (op.kind == TWFA_OP_EXB) {
-        exb_part(c, a, t, it, g, p);
+        exb_part(c, a, t, it, g, p, st);
         if constexpr (kRole == kExbDs) ds_part<true>(c, a, t, it, g, p);  // fused (lowering guarantees)
       } else if constexpr (kRole == kDs) {
         ds_part<false>(c, a, t, it, g, p);
@@ -532,7 +540,7 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
     return;
   }
   if (op.kind == TWFA_OP_RD) {
-    if constexpr (kRole == kReduce) rd_op(c, a, t, it, g, plan);
+    if constexpr (kRole == kReduce) rd_op(c, a, t, it, g, plan, st);
     return;
   }
   if constexpr (kRole != kLight) return;
@@ -552,6 +560,7 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
     else
       mbar_wait(&bar.q_full[qs], (g / plan.k_depth) & 1);
     tc_fence_after();
+    bwd_ready(st);
 #if TWFA_BWD_PROF
     g_prof_ready = clock64();
 #endif
@@ -573,6 +582,7 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
     else
       mbar_wait(&bar.o_full[os], (g / plan.v_depth) & 1);
     tc_fence_after();
+    bwd_ready(st);
 #if TWFA_BWD_PROF
     g_prof_ready = clock64();
 #endif
@@ -597,6 +607,7 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
     else
       mbar_wait_all(&bar.ds_full, g & 1, &bar.q_full[qs], (g / plan.k_depth) & 1);
     tc_fence_after();
+    bwd_ready(st);
 #if TWFA_BWD_PROF
     g_prof_ready = clock64();
 #endif
@@ -613,6 +624,7 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
   } else if (op.kind == TWFA_OP_DQ) {
     mbar_wait(&bar.ds_full, g & 1);
     tc_fence_after();
+    bwd_ready(st);
 #if TWFA_BWD_PROF
     g_prof_ready = clock64();
 #endif
@@ -637,7 +649,7 @@ __device__ __forceinline__ void bwd_run(const BwdCtx& c, const TwfaDevicePlan& p
   const int plen = plan.prog_len[c.warp];
   const bool is_load = c.warp == static_cast<uint32_t>(plan.load_warp);
   const bool is_mma = c.warp == static_cast<uint32_t>(plan.mma_warp);
-  BwdState st{0, 0, -1, -1, 0};
+  BwdState st{0, 0, -1, -1, 0, nullptr};
   uint32_t gbase = 0, icount = 0;
   for (int i = 0;; ++i, ++icount) {
     int work;
