@@ -97,7 +97,8 @@ def sources(gen_root=CSRC):
     gen = os.path.join(gen_root, "gen")
     specs = sorted(os.path.join(gen, f) for f in os.listdir(gen) if f.startswith("fa_spec_") and f.endswith(".cu")) \
         if os.path.isdir(gen) else []
-    cu = [os.path.join(CSRC, f) for f in ("fa_fwd_sm100.cu", "fa_bwd_sm100.cu", "gemm_sm100.cu")] + specs
+    cu = [os.path.join(CSRC, f) for f in ("fa_fwd_sm100.cu", "fa_bwd_sm100.cu", "fa_bwd_pp_sm100.cu",
+                                          "gemm_sm100.cu")] + specs
     cpp = [os.path.join(CSRC, f) for f in ("lowering.cpp", "capi.cpp")]
     return cu, cpp
 

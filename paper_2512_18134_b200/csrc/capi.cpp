@@ -83,12 +83,13 @@ EncodeFn encode_fn() {
 
 // bf16 (or fp32) tensor of `rank` dims (innermost first), 128-byte swizzled boxes
 CUtensorMap make_map(const void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides_bytes,
-                     const cuuint32_t* box, CUtensorMapDataType dtype = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16) {
+                     const cuuint32_t* box, CUtensorMapDataType dtype = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                     CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_128B) {
   CUtensorMap m;
   cuuint32_t elem[3] = {1, 1, 1};
   CUresult r = encode_fn()(&m, dtype, static_cast<cuuint32_t>(rank),
                            const_cast<void*>(base), dims, strides_bytes, box, elem,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
   return m;
@@ -345,6 +346,9 @@ int fa_bwd_impl(const twfa_plan* plan, const void* q, const void* k, const void*
   a.tm_v = make_map(v, 3, dims, strides, box);
   a.tm_do = make_map(dout, 3, dims, strides, box);
   a.tm_dq = make_map(dq_acc, 3, dims, strides32, box32, CU_TENSOR_MAP_DATA_TYPE_FLOAT32);
+  const cuuint32_t box64[3] = {64, 64, 1};
+  a.tm_dq64 = make_map(dq_acc, 3, dims, strides32, box64, CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                       CU_TENSOR_MAP_SWIZZLE_NONE);
   a.lse = lse;
   a.dvec = dvec;
   a.dq_acc = dq_acc;

@@ -18,6 +18,9 @@ struct FaBwdArgs {
   alignas(64) CUtensorMap tm_v;
   alignas(64) CUtensorMap tm_do;
   alignas(64) CUtensorMap tm_dq;
+  // the fp32 dQ accumulator with 64 x 64 unswizzled boxes (the two-sub-tile
+  // kernel's reduce-add of a 64-query x 64-dim staging block)
+  alignas(64) CUtensorMap tm_dq64;
   const float* lse;   // [B, H, S] natural-log sum-exp of the forward
   float* dvec;        // [B, H, S] workspace: rowsum(dO * O)
   float* dq_acc;      // [B, H, S, 128] workspace: fp32 dQ accumulator
@@ -41,7 +44,10 @@ struct FaBwdArgs {
 size_t fa_bwd_smem_bytes(const TwfaDevicePlan& plan);
 size_t fa_bwd_workspace_bytes(int B, int H, int S);
 // pre-pass (D), zeroing of the accumulator, the main kernel, post-pass (dQ)
+// (num_tiles == 2 plans run the two-sub-tile kernel, fa_bwd_pp_sm100.cu)
 cudaError_t fa_bwd_launch(const TwfaDevicePlan& plan, const FaBwdArgs& args, const __nv_bfloat16* o,
                           const __nv_bfloat16* dout, __nv_bfloat16* dq, int grid, cudaStream_t stream);
+size_t fa_bwd_pp_smem_bytes(const TwfaDevicePlan& plan);
+cudaError_t fa_bwd_pp_main_launch(const TwfaDevicePlan& plan, const FaBwdArgs& args, int grid, cudaStream_t stream);
 
 }  // namespace twfa

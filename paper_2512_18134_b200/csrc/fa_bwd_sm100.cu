@@ -83,7 +83,8 @@ struct __align__(8) BwdBarriers {
 __shared__ BwdBarriers g_bb;
 // LSE * log2(e) and D of the current Q tile, broadcast to the EXB / DS
 // warpgroup (thread t stages query q0 + t)
-__shared__ float g_lse2[kT], g_dvec[kT];
+__shared__ __align__(16) float g_lse2[kT];
+__shared__ __align__(16) float g_dvec[kT];
 #if TWFA_BWD_PROF
 __shared__ int g_prof_n;
 __shared__ long long g_prof[24][4];
@@ -840,11 +841,15 @@ cudaError_t fa_bwd_launch(const TwfaDevicePlan& plan, const FaBwdArgs& args, con
   fa_bwd_pre<<<static_cast<unsigned>((rows + 15) / 16), 256, 0, stream>>>(o, dout, args.dvec, rows);
   cudaError_t e = cudaMemsetAsync(args.dq_acc, 0, static_cast<size_t>(rows) * 128 * sizeof(float), stream);
   if (e != cudaSuccess) return e;
-  const size_t smem = fa_bwd_smem_bytes(plan);
-  e = cudaFuncSetAttribute(fa_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
-  fa_bwd_kernel<<<grid, TWFA_MAX_WARPS * 32, smem, stream>>>(plan, args);
-  e = cudaGetLastError();
+  if (plan.num_tiles == 2) {
+    e = fa_bwd_pp_main_launch(plan, args, grid, stream);
+  } else {
+    const size_t smem = fa_bwd_smem_bytes(plan);
+    e = cudaFuncSetAttribute(fa_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    fa_bwd_kernel<<<grid, TWFA_MAX_WARPS * 32, smem, stream>>>(plan, args);
+    e = cudaGetLastError();
+  }
   if (e != cudaSuccess) return e;
   const int64_t n8 = rows * 16;
   fa_bwd_post<<<static_cast<unsigned>((n8 + 255) / 256), 256, 0, stream>>>(args.dq_acc, dq, args.scale, n8);

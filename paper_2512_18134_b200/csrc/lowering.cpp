@@ -262,8 +262,10 @@ bool classify(const std::string& id, uint8_t& kind, uint8_t& tile) {
                               {"DK", TWFA_OP_DK},   {"DQ", TWFA_OP_DQ},   {"RD", TWFA_OP_RD}};
   for (const Pfx& f : fixed)
     if (id == f.p) { kind = f.k; tile = 0; return true; }
-  static const Pfx tiled[] = {{"MX", TWFA_OP_MX}, {"EX", TWFA_OP_EX}, {"CR", TWFA_OP_CR}, {"PV", TWFA_OP_PV},
-                              {"SA", TWFA_OP_SA}, {"SB", TWFA_OP_SB}, {"S", TWFA_OP_S}};
+  static const Pfx tiled[] = {{"MX", TWFA_OP_MX},   {"EX", TWFA_OP_EX},  {"CR", TWFA_OP_CR},  {"PV", TWFA_OP_PV},
+                              {"SA", TWFA_OP_SA},   {"SB", TWFA_OP_SB},  {"S", TWFA_OP_S},    {"ST", TWFA_OP_ST},
+                              {"DP", TWFA_OP_DP},   {"EXB", TWFA_OP_EXB}, {"DS", TWFA_OP_DS}, {"DV", TWFA_OP_DV},
+                              {"DK", TWFA_OP_DK},   {"DQ", TWFA_OP_DQ},  {"RD", TWFA_OP_RD}};
   for (const Pfx& f : tiled) {
     const size_t l = std::strlen(f.p);
     if (id.size() == l + 1 && id.compare(0, l, f.p) == 0 && id[l] >= '0' && id[l] < '0' + TWFA_MAX_TILES) {
@@ -364,6 +366,104 @@ void derive_bwd(LoweredSchedule& s, NodeId&& node_id, DepthOf&& depth_of, Prefet
   // releases the ring slot with its commit
   p.ops[later("ST", "DK")].flags |= TWFA_OPF_RELEASE;
   p.ops[later("DP", "DV")].flags |= TWFA_OPF_RELEASE;
+}
+
+// FA backward with two 64-query sub-tiles per iteration (family FA_BWD,
+// num_tiles 2; tools/make_problems.py:fa_backward_pp_problem, realized by
+// fa_bwd_pp_sm100.cu): per sub-tile k the nodes ST_k, DP_k, EXB_k, DS_k,
+// DV_k, DK_k, DQ_k, RD_k, plus the streamed LDQ / LDO of the 128-row tiles.
+// All tensor-core ops issue from one thread (the in-order aliasing edges
+// DV_k -> DQ_k and DK_k -> DP_k); EXB_k and DS_k share a warpgroup with DS_k
+// right after EXB_k (P^T_k in registers); RD_k runs on a warpgroup of its own
+// register class. The later tensor-core reader of Q_i (dO_i) in issue order
+// releases its ring slot.
+template <class NodeId, class DepthOf, class PrefetchOf>
+void derive_bwd_pp(LoweredSchedule& s, NodeId&& node_id, DepthOf&& depth_of, PrefetchOf&& prefetch_of) {
+  TwfaDevicePlan& p = s.plan;
+  p.family = TWFA_FAMILY_FA_BWD;
+  p.num_tiles = 2;
+  static const char* per_tile[] = {"ST", "DP", "EXB", "DS", "DV", "DK", "DQ", "RD"};
+  for (const char* id : {"LDQ", "LDO"})
+    if (node_id(id) < 0) throw DomainError(std::string("FA-backward loop is missing ") + id);
+  for (int k = 0; k < 2; ++k)
+    for (const char* id : per_tile)
+      if (node_id(id + std::to_string(k)) < 0)
+        throw DomainError(std::string("two-sub-tile FA-backward loop is missing ") + id + std::to_string(k));
+  if (s.nodes.size() != 18) throw DomainError("two-sub-tile FA-backward loop has unexpected extra nodes");
+  const TwfaPlanOp &ldq = p.ops[node_id("LDQ")], &ldo = p.ops[node_id("LDO")];
+  if (ldq.warp_start != ldo.warp_start || ldq.warp_count != 1)
+    throw DomainError("LDQ and LDO must be issued by one TMA warp");
+  p.load_warp = ldq.warp_start;
+  p.k_depth = depth_of("LDQ");
+  p.v_depth = depth_of("LDO");
+  p.k_prefetch = prefetch_of(node_id("LDQ"), p.k_depth);
+  p.v_prefetch = prefetch_of(node_id("LDO"), p.v_depth);
+  if (p.k_depth > 2 || p.v_depth > 2) throw DomainError("Q / dO rings deeper than 2 exceed shared memory");
+  auto op = [&](const char* id, int k) -> TwfaPlanOp& { return p.ops[node_id(id + std::to_string(k))]; };
+  const int mma = op("ST", 0).warp_start;
+  for (int k = 0; k < 2; ++k)
+    for (const char* id : {"ST", "DP", "DV", "DK", "DQ"}) {
+      const TwfaPlanOp& o = op(id, k);
+      if (o.warp_count != 1 || o.warp_start != mma)
+        throw DomainError("tensor-core ops of the backward loop must issue from one warp");
+    }
+  p.mma_warp = mma;
+  int heavy = 0;
+  for (int k = 0; k < 2; ++k) {
+    const TwfaPlanOp &exb = op("EXB", k), &ds = op("DS", k), &rd = op("RD", k);
+    for (const TwfaPlanOp* o : {&exb, &ds, &rd})
+      if (o->warp_count != 4 || o->warp_start % 4 != 0)
+        throw DomainError("EXB, DS and RD are row-wise over 128 TMEM lanes: they need a warpgroup");
+    for (int w : {p.load_warp, p.mma_warp})
+      for (const TwfaPlanOp* o : {&exb, &ds, &rd})
+        if (w >= o->warp_start && w < o->warp_start + 4)
+          throw DomainError("the TMA / MMA warp cannot be inside an EXB, DS or RD warpgroup");
+    if (exb.warp_start != ds.warp_start)
+      throw DomainError("EXB_k and DS_k must share a warpgroup (P^T_k is carried in registers)");
+    const int exi = node_id("EXB" + std::to_string(k)), dsi = node_id("DS" + std::to_string(k));
+    for (int w = exb.warp_start; w < exb.warp_start + 4; ++w) {
+      const std::vector<int>& prog = s.warp_prog[static_cast<size_t>(w)];
+      auto it = std::find(prog.begin(), prog.end(), exi);
+      if (it == prog.end() || it + 1 == prog.end() || *(it + 1) != dsi ||
+          s.stage[static_cast<size_t>(exi)] != s.stage[static_cast<size_t>(dsi)])
+        throw DomainError("DS_k must directly follow EXB_k on its warpgroup (P is carried in registers)");
+    }
+    p.ops[exi].flags |= TWFA_OPF_FUSE_NEXT;
+    p.ops[dsi].flags |= TWFA_OPF_FUSED;
+    p.sm_warp[k] = exb.warp_start;
+    p.cr_warp[k] = rd.warp_start;
+    heavy |= 1 << (exb.warp_start / 4);
+  }
+  for (int k = 0; k < 2; ++k)
+    if (p.cr_warp[k] == p.sm_warp[0] || p.cr_warp[k] == p.sm_warp[1])
+      throw DomainError("RD needs a warpgroup of its own (register budget of the dQ staging)");
+  p.heavy_wg_mask = heavy;
+  // the graph's aliasing edges the kernel realizes by issue order on the MMA
+  // thread or by its barriers
+  auto has_edge = [&](const std::string& a, const std::string& b, int delta) {
+    for (const LEdge& e : s.edges)
+      if (e.src == node_id(a) && e.dst == node_id(b) && e.delta == delta) return true;
+    return false;
+  };
+  for (int k = 0; k < 2; ++k) {
+    const std::string K = std::to_string(k);
+    if (!has_edge("DV" + K, "DQ" + K, 0) || !has_edge("DK" + K, "DP" + K, 1) || !has_edge("RD" + K, "ST" + K, 1) ||
+        !has_edge("DQ" + K, "DS" + K, 1) || !has_edge("RD" + K, "DS" + K, 1))
+      throw DomainError("two-sub-tile FA-backward loop lacks a tensor-memory / shared-memory aliasing edge");
+  }
+  // ring slots: the last tensor-core reader of Q_i (of dO_i) in issue order
+  auto last = [&](std::initializer_list<std::string> ids) {
+    int best = -1;
+    for (const std::string& id : ids) {
+      const int v = node_id(id);
+      if (best < 0 || std::make_pair(s.stage[static_cast<size_t>(v)], p.ops[v].order) >
+                          std::make_pair(s.stage[static_cast<size_t>(best)], p.ops[best].order))
+        best = v;
+    }
+    return best;
+  };
+  p.ops[last({"ST0", "ST1", "DK0", "DK1"})].flags |= TWFA_OPF_RELEASE;
+  p.ops[last({"DP0", "DP1", "DV0", "DV1"})].flags |= TWFA_OPF_RELEASE;
 }
 
 void derive(LoweredSchedule& s) {
@@ -523,7 +623,10 @@ void derive(LoweredSchedule& s) {
   const bool is_bwd = kinds.count(TWFA_OP_ST) && kinds.count(TWFA_OP_DQ);
   if (is_fa + is_gemm + is_bwd != 1) throw DomainError("graph is neither the FA-forward, FA-backward nor GEMM loop");
   if (is_bwd) {
-    derive_bwd(s, node_id, depth_of, prefetch_of);
+    if (node_id("ST0") >= 0)
+      derive_bwd_pp(s, node_id, depth_of, prefetch_of);
+    else
+      derive_bwd(s, node_id, depth_of, prefetch_of);
     return;
   }
   if (is_gemm) {
@@ -984,14 +1087,28 @@ std::string describe(const LoweredSchedule& s) {
     rings["dO"] = p.v_depth;
     j["prefetch"] = {{"LDQ", p.k_prefetch}, {"LDO", p.v_prefetch}};
     j["mma_warp"] = p.mma_warp;
-    j["warpgroups"] = {{"exp", p.sm_warp[0]}, {"ds", p.sm_warp[1]}, {"dq_reduce", p.cr_warp[0]}};
-    j["p_transfer"] = p.sm_warp[0] == p.sm_warp[1] ? "registers (EXB and DS fused)" : "tensor memory (bf16 P^T re-read)";
+    j["num_tiles"] = p.num_tiles;
+    if (p.num_tiles == 2) {  // two 64-query sub-tiles (fa_bwd_pp_sm100.cu)
+      j["warpgroups"] = {{"exp_ds0", p.sm_warp[0]}, {"exp_ds1", p.sm_warp[1]},
+                         {"dq_reduce0", p.cr_warp[0]}, {"dq_reduce1", p.cr_warp[1]}};
+      j["p_transfer"] = "registers (EXB_k and DS_k fused)";
+    } else {
+      j["warpgroups"] = {{"exp", p.sm_warp[0]}, {"ds", p.sm_warp[1]}, {"dq_reduce", p.cr_warp[0]}};
+      j["p_transfer"] =
+          p.sm_warp[0] == p.sm_warp[1] ? "registers (EXB and DS fused)" : "tensor memory (bf16 P^T re-read)";
+    }
     json rel = json::array();
     for (int v = 0; v < p.num_nodes; ++v)
       if (p.ops[v].flags & TWFA_OPF_RELEASE) rel.push_back(s.nodes[static_cast<size_t>(v)].id);
     j["ring_release"] = rel;
-    j["dq_staging"] = p.s_split ? "Q ring slot" : "dS buffer";
-    j["tmem_columns"] = {{"dK", 0}, {"dV", 128}, {"S^T/P^T/dQ", 256}, {"dP^T/dS^T", 384}};
+    if (p.num_tiles == 2) {
+      j["dq_staging"] = "dS_k buffer, transposed, two 64-dim passes";
+      j["tmem_columns"] = {{"dK", 0},           {"dV", 128},           {"S^T_0/P^T_0/dQ^T_0", 256},
+                           {"dP^T_0/dS^T_0", 320}, {"S^T_1/P^T_1/dQ^T_1", 384}, {"dP^T_1/dS^T_1", 448}};
+    } else {
+      j["dq_staging"] = p.s_split ? "Q ring slot" : "dS buffer";
+      j["tmem_columns"] = {{"dK", 0}, {"dV", 128}, {"S^T/P^T/dQ", 256}, {"dP^T/dS^T", 384}};
+    }
   } else {
     rings["AB"] = p.k_depth;
     j["mma_warp"] = p.mma_warp;

@@ -13,7 +13,7 @@
 #pragma once
 #include <stdint.h>
 
-#define TWFA_MAX_NODES 16
+#define TWFA_MAX_NODES 20
 #define TWFA_MAX_WARPS 16
 #define TWFA_MAX_TILES 2
 

@@ -137,3 +137,21 @@ def test_causal_work_lists_keep_dk_dv(twfa, plans, monkeypatch):
     torch.cuda.synchronize()
     assert torch.equal(a[1], b[1]) and torch.equal(a[2], b[2])
     assert (a[0].float() - b[0].float()).abs().max().item() <= 1e-2 * b[0].float().abs().max().item()
+
+
+@pytest.fixture(scope="module")
+def pp_plans(twfa):
+    return twfa.Plan(*twfa.load_schedule("fa_fwd")), twfa.Plan(*twfa.load_schedule("fa_bwd_pp"))
+
+
+@pytest.mark.parametrize("B,H,S,causal", [(1, 2, 128, False), (1, 2, 640, False), (1, 2, 384, True),
+                                          (1, 1, 200, False), (1, 1, 77, True), (1, 1, 320, True),
+                                          (2, 96, 256, True), (2, 80, 512, False)])
+def test_two_subtile_schedule_matches_oracle(twfa, pp_plans, B, H, S, causal):
+    """fa_bwd_pp: two 64-query sub-tiles per Q tile with their own TMEM
+    buffers, EXB_k / DS_k on two warpgroups (the solver's assignment), dQ^T_k
+    = K^T dS^T_k reduced from a transposed shared-memory staging block.
+    Covers sequence tails (sub-tile 1 past S), causal diagonal tiles and more
+    work items than SMs (accumulator hand-off across items)."""
+    assert pp_plans[1].describe()["num_tiles"] == 2
+    _check(twfa, pp_plans, B, H, S, causal, 40)

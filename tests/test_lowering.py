@@ -95,10 +95,15 @@ def test_fa_ring_depth_follows_solution(twfa):
     prob, sol = twfa.load_schedule("fa_fwd")
     s = json.loads(sol)
     assert twfa.Plan(prob, sol).describe()["rings"] == {"K": 2, "V": 2, "S": 1}
-    # two 32 KiB Q tiles + 2 + 2 ring slots fill the 227 KiB of shared memory;
-    # a deeper ring than the solution's is not realizable and must say so
-    s["streaming_depths"] = {"LDK": 3, "LDV": 2}
-    with pytest.raises(ValueError, match="shared memory"):
+    # one CTA per tile: two 32 KiB Q tiles + 2 + 2 ring slots of 32 KiB fill
+    # the 227 KiB of shared memory. A deeper ring fits with the CTA-pair
+    # realization (16 KiB K / V slots per CTA), which the plan then requires;
+    # deeper than 4 is not realizable and must say so
+    s["streaming_depths"] = {"LDK": 3, "LDV": 3}
+    d = twfa.Plan(prob, json.dumps(s)).describe()
+    assert d["rings"] == {"K": 3, "V": 3, "S": 1} and d["cta_pair"] is True
+    s["streaming_depths"] = {"LDK": 5, "LDV": 2}
+    with pytest.raises(ValueError, match="ring depth above 4"):
         twfa.Plan(prob, json.dumps(s))
 
 

@@ -283,6 +283,81 @@ def fa_backward_problem(calibrated=False, fused=False, exb_spill=16, q_staging=F
     return {"machine": machine, "graph": {"nodes": nodes, "edges": edges}}
 
 
+def fa_backward_pp_problem():
+    """FA-backward loop body with two 64-query sub-tiles per iteration (the
+    paper's Blackwell strategy: two exponential
+    warpgroups ping-pong over alternating query tiles, a third stages the dQ
+    reduction). One CTA owns a 128-key K/V tile (K, V resident in shared
+    memory; dK, dV accumulated in tensor memory) and iterates over 128-row
+    Q / dO tiles (LDQ, LDO, streamed); sub-tile k = queries 64k .. 64k + 63:
+
+      ST_k   S^T_k  = K Q_k^T        M 128 keys, N 64 queries, K 128 d (SS)
+      EXB_k  P^T_k  = exp2(S^T_k - LSE)  -> bf16 over S^T_k        (MUFU)
+      DP_k   dP^T_k = V dO_k^T       M 128, N 64, K 128 (SS)
+      DS_k   dS^T_k = P^T_k (dP^T_k - D) -> bf16 over dP^T_k and to smem
+      DV_k   dV    += P^T_k dO_k     M 128 keys, N 128 d, K 64 (TS)
+      DK_k   dK    += dS^T_k Q_k     M 128, N 128, K 64 (TS)
+      DQ_k   dQ^T_k = K^T dS^T_k     M 128 d, N 64 queries, K 128 keys (SS)
+      RD_k   dQ^T_k -> smem (transposed) -> TMA reduce-add into fp32 dQ
+
+    Tensor memory (512 columns): dK 128, dV 128, and per sub-tile 128: S^T_k
+    (64, P^T_k over it, then dQ^T_k over it once DV_k has read P^T_k) and
+    dP^T_k (64, dS^T_k over it). Aliasing edges: DV_k -> DQ_k (in order on
+    the issuing thread), RD_k -> ST_k (delta 1: S^T_k(i+1) overwrites the
+    dQ^T_k RD_k(i) reads), DK_k -> DP_k (delta 1, in order), DQ_k -> DS_k
+    (delta 1: dS^T_k(i+1) overwrites the shared-memory operand DQ_k(i)
+    reads), RD_k -> DS_k (delta 1: RD_k stages dQ^T_k in that buffer).
+    EXB_k -> DS_k carries P^T_k in registers (a large spill cost keeps them
+    on one warpgroup); a 192-register budget per warp keeps the two sub-tiles'
+    EXB / DS on different warpgroups.
+    Raw costs (B200 clk, multiples of 256 so the normalization is exact at
+    U = 14): SS GEMMs with N = 64 read 6 KiB of shared memory per 32-clk
+    K-step (192 B/clk against 128): 384, priced 512; TS GEMMs 256; EXB 768
+    (8192 exp2 at 16/clk + the S^T read); DS 512; RD 512; spill 2048."""
+    ss, ts, ex, dsc, rd = 512, 256, 768, 512, 512
+    machine = {
+        "units": [{"name": "TC", "capacity": 1}, {"name": "TMA", "capacity": 1},
+                  {"name": "MUFU", "capacity": 1}, {"name": "ALU", "capacity": 1},
+                  {"name": "FMA", "capacity": 1}],
+        "memories": [{"name": "tmem", "capacity": 512}],
+        "num_warps": 16,
+        "reg_limit": 192,
+        "vl_warp": 15,
+    }
+    nodes = [node("LDQ", "TMA", 256, variable_latency=True), node("LDO", "TMA", 256, variable_latency=True)]
+    edges = []
+    for k in (0, 1):
+        nodes += [
+            node(f"ST{k}", "TC", ss, footprint={"tmem": 64}, variable_latency=True),
+            node(f"DP{k}", "TC", ss, footprint={"tmem": 64}, variable_latency=True),
+            node(f"EXB{k}", "MUFU", ex, regs=128, spill_cost=2048, warps_required=4),
+            node(f"DS{k}", "FMA", dsc, regs=64, warps_required=4),
+            node(f"DV{k}", "TC", ts, variable_latency=True),
+            node(f"DK{k}", "TC", ts, variable_latency=True),
+            node(f"DQ{k}", "TC", ss, variable_latency=True),
+            node(f"RD{k}", "ALU", rd, regs=64, warps_required=4),
+        ]
+        edges += [
+            edge("LDQ", f"ST{k}", 0, blocking=True), edge("LDQ", f"DK{k}", 0, blocking=True),
+            edge("LDO", f"DP{k}", 0, blocking=True), edge("LDO", f"DV{k}", 0, blocking=True),
+            edge(f"ST{k}", f"EXB{k}", ss, blocking=True),
+            edge(f"EXB{k}", f"DV{k}", ex, blocking=True), edge(f"EXB{k}", f"DS{k}", ex),
+            edge(f"DP{k}", f"DS{k}", ss, blocking=True),
+            edge(f"DS{k}", f"DK{k}", dsc, blocking=True), edge(f"DS{k}", f"DQ{k}", dsc, blocking=True),
+            edge(f"DQ{k}", f"RD{k}", ss, blocking=True),
+            edge(f"DV{k}", f"DQ{k}", 0),
+            edge(f"RD{k}", f"ST{k}", rd, delta=1, blocking=True),
+            edge(f"DK{k}", f"DP{k}", 0, delta=1),
+            edge(f"DQ{k}", f"DS{k}", ss, delta=1, blocking=True),
+            edge(f"RD{k}", f"DS{k}", rd, delta=1, blocking=True),
+            edge(f"EXB{k}", f"EXB{k}", ex, delta=1), edge(f"DS{k}", f"DS{k}", dsc, delta=1),
+            edge(f"RD{k}", f"RD{k}", rd, delta=1),
+        ]
+    for n in nodes:
+        n["rrt"] = {u: [1] * n["cycles"] for u in n["rrt"]}
+    return {"machine": machine, "graph": {"nodes": nodes, "edges": edges}}
+
+
 def gemm_problem():
     """GEMM mainloop (BASELINE config 2): per k-block, TMA loads of the A and B
     tiles feed one 256x256x64 tcgen05 MMA chain (cta_group::2: a CTA pair on
@@ -411,6 +486,8 @@ def main():
         # the split model with dQ staged in the Q ring slot (no RD -> DS chain)
         "fa_bwd_qstage": (fa_backward_problem(exb_spill=1, q_staging=True), 2, 13),
         "fa_bwd_cal": (fa_backward_problem(calibrated=True), 2, 14),
+        # two 64-query sub-tiles per iteration, ping-ponging EXB / DS warpgroups
+        "fa_bwd_pp": (fa_backward_pp_problem(), 2, 14),
     }
     for name, (raw, depth, res) in probs.items():
         if args.only and name != args.only:
