@@ -89,6 +89,9 @@ struct PpState {
   uint32_t trace_n;
   uint32_t* rec;       // current op's trace record
   bool dv_started, dk_started;  // the work item's first DV / DK MMA initialises the accumulator
+  // 1 + the last global iteration whose Q (dO) tile the MMA warp has seen
+  // land: later readers of the tile skip the wait
+  uint32_t q_seen, o_seen;
 };
 
 __device__ __forceinline__ PpItem pp_item(const PpCtx& c, const FaBwdArgs& a, int work, uint32_t gbase,
@@ -371,12 +374,16 @@ __device__ __forceinline__ void pp_exec(const TwfaPlanOp op, const int r, const 
     if (it == 0) mbar_wait(&bar.kv_full, t.icount & 1);
     if (is_s) {
       // S^T_k(g) overwrites dQ^T_k(g-1), which RD_k(g-1) must have read out
-      if (g > 0)
+      if (g > 0 && st.q_seen == g + 1)
+        mbar_wait(&bar.q_free[k], (g - 1) & 1);
+      else if (g > 0)
         mbar_wait_all(&bar.q_full[qs], (g / plan.k_depth) & 1, &bar.q_free[k], (g - 1) & 1);
       else
         mbar_wait(&bar.q_full[qs], (g / plan.k_depth) & 1);
+      st.q_seen = g + 1;
     } else {
-      mbar_wait(&bar.o_full[os], (g / plan.v_depth) & 1);
+      if (st.o_seen != g + 1) mbar_wait(&bar.o_full[os], (g / plan.v_depth) & 1);
+      st.o_seen = g + 1;
     }
     tc_fence_after();
     pp_ready(st);
@@ -398,10 +405,14 @@ __device__ __forceinline__ void pp_exec(const TwfaPlanOp op, const int r, const 
     // the accumulator is overwritten by the item's first MMA: the previous
     // work item's dK / dV must have been read out
     if (!started && t.icount > 0) mbar_wait(&bar.acc_free, (t.icount - 1) & 1);
-    if (dv)
-      mbar_wait_all(&bar.p_full[k], g & 1, &bar.o_full[os], (g / plan.v_depth) & 1);
+    uint32_t& seen = dv ? st.o_seen : st.q_seen;
+    uint64_t* tile_full = dv ? &bar.o_full[os] : &bar.q_full[qs];
+    const uint32_t tile_ph = dv ? (g / plan.v_depth) & 1 : (g / plan.k_depth) & 1;
+    if (seen == g + 1)
+      mbar_wait(dv ? &bar.p_full[k] : &bar.ds_full[k], g & 1);
     else
-      mbar_wait_all(&bar.ds_full[k], g & 1, &bar.q_full[qs], (g / plan.k_depth) & 1);
+      mbar_wait_all(dv ? &bar.p_full[k] : &bar.ds_full[k], g & 1, tile_full, tile_ph);
+    seen = g + 1;
     tc_fence_after();
     pp_ready(st);
     // B = dO_k / Q_k as [K = query][N = d], MN-major (the two 64-dim halves kHalf apart)
@@ -440,7 +451,7 @@ __device__ __forceinline__ void pp_run(const PpCtx& c, const TwfaDevicePlan& pla
   const int plen = plan.prog_len[c.warp];
   const bool is_load = c.warp == static_cast<uint32_t>(plan.load_warp);
   const bool is_mma = c.warp == static_cast<uint32_t>(plan.mma_warp);
-  PpState st{0, 0, 0, nullptr, false, false};
+  PpState st{0, 0, 0, nullptr, false, false, 0, 0};
   uint32_t gbase = 0, icount = 0;
   for (int i = 0;; ++i, ++icount) {
     int work;

@@ -106,9 +106,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     // L2 policies (TWFA_GEMM_POL): 0 normal / normal, 1 A evict_last / B
     // evict_first, 2 last / last (default: 1.07 GB DRAM reads per 8192^3
     // launch against 2.2 GB for 1 and 3; profiles/r02b_gemm_policy.txt),
-    // 3 normal / first
+    // 3 normal / first, 4 last / normal
     const int pm = args.pol_mode;
-    const uint64_t pol_a = (pm == 1 || pm == 2) ? policy_evict_last() : policy_evict_normal();
+    const uint64_t pol_a = (pm == 1 || pm == 2 || pm == 4) ? policy_evict_last() : policy_evict_normal();
     const uint64_t pol_b = pm == 2 ? policy_evict_last() : (pm == 1 || pm == 3) ? policy_evict_first()
                                                                                  : policy_evict_normal();
     uint32_t g = 0;
