@@ -331,6 +331,12 @@ __device__ __forceinline__ float exp_store_row(const uint32_t (&s)[N], uint32_t 
 #ifndef TWFA_TRACE_SUB
 #define TWFA_TRACE_SUB 0
 #endif
+// TWFA_LATE_SUM: the row sum of chunks 1.. is taken after the last P part is
+// released (the fp32 P overwrites the consumed S registers), so the FADD2s
+// leave the MUFU-bound path to PV
+#ifndef TWFA_LATE_SUM
+#define TWFA_LATE_SUM 1  // measured: +0.9 % (pair) / +1.4 % (one CTA) per clock under the power cap, +4 % burst
+#endif
 template <int N, bool P, class Handoff, class WaitRest>
 __device__ __forceinline__ float mx_ex_spec(uint32_t (&s)[N], uint32_t taddr, float sl, float& m_io, float& alpha,
                                             uint64_t* part_bar, Handoff&& handoff, WaitRest&& wait_rest,
@@ -366,7 +372,12 @@ __device__ __forceinline__ float mx_ex_spec(uint32_t (&s)[N], uint32_t taddr, fl
         p.x = fast_exp2(x.x);
         p.y = fast_exp2(x.y);
       }
-      acc[(i >> 1) & 1] = fadd2(acc[(i >> 1) & 1], p);
+      if (TWFA_LATE_SUM && c > 0) {  // S of chunk c is consumed: keep P there for the late row sum
+        s[e] = __float_as_uint(p.x);
+        s[e + 1] = __float_as_uint(p.y);
+      } else {
+        acc[(i >> 1) & 1] = fadd2(acc[(i >> 1) & 1], p);
+      }
       pk[i >> 1] = pack_bf16(p.x, p.y);
     }
   };
@@ -397,6 +408,15 @@ __device__ __forceinline__ float mx_ex_spec(uint32_t (&s)[N], uint32_t taddr, fl
   }
   if (TWFA_TRACE_SUB && trm != nullptr) trm[7] = static_cast<uint32_t>(clock64());
   tmem_st_wait();
+  if constexpr (TWFA_LATE_SUM) {
+    tc_fence_before();
+    arrive_mma_<P>(&part_bar[kParts - 1]);  // the last part, before the row sum
+#pragma unroll
+    for (int e = kKeys; e < N; e += 4) {
+      acc[0] = fadd2(acc[0], make_float2(__uint_as_float(s[e]), __uint_as_float(s[e + 1])));
+      acc[1] = fadd2(acc[1], make_float2(__uint_as_float(s[e + 2]), __uint_as_float(s[e + 3])));
+    }
+  }
   return (acc[0].x + acc[0].y) + (acc[1].x + acc[1].y);
 }
 
@@ -777,8 +797,10 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
             wr(st.m_run, k, m);
             wr(st.alpha, k, alpha);
             wr(st.l_run, k, rd(st.l_run, k) * alpha + sum);
-            tc_fence_before();
-            arrive_mma_<P>(&bar.p_part[k][b][p_parts<P>() - 1]);
+            if (!TWFA_LATE_SUM) {
+              tc_fence_before();
+              arrive_mma_<P>(&bar.p_part[k][b][p_parts<P>() - 1]);
+            }
             if (it == N - 1) {
               mbar_wait(&bar.l_empty[k], (t.tcount & 1) ^ 1);
               g_sh.lbuf[k][0][c.quad * 32 + lane] = m;
