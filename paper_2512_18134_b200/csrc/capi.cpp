@@ -278,13 +278,9 @@ int fa_fwd_impl(const twfa_plan* plan, const void* q, const void* k, const void*
   const cuuint64_t bh = static_cast<cuuint64_t>(B) * H;
   const cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(S), bh};
   const cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 2, static_cast<cuuint64_t>(S) * D * 2};
-  const bool pair = use_pairs(p);
   const cuuint32_t box_q[3] = {64, 128, 1};
   const cuuint32_t box_kv[3] = {64, static_cast<cuuint32_t>(p.kv_tile), 1};
-  // a CTA of a pair loads half the keys of a K tile (per head-dim half)
-  const cuuint32_t box_k[3] = {64, static_cast<cuuint32_t>(pair ? p.kv_tile / 2 : p.kv_tile), 1};
   const CUtensorMap tq = make_map(q, 3, dims, strides, box_q);
-  const CUtensorMap tk = make_map(k, 3, dims, strides, box_k);
   const CUtensorMap tv = make_map(v, 3, dims, strides, box_kv);
   const CUtensorMap to = make_map(o, 3, dims, strides, box_q);
   twfa::FaArgs a{};
@@ -298,21 +294,36 @@ int fa_fwd_impl(const twfa_plan* plan, const void* q, const void* k, const void*
   a.S = S;
   a.causal = causal ? 1 : 0;
   a.scale_log2 = scale * 1.4426950408889634f;
-  // persistent: one work unit (CTA, or CTA pair of 512 query rows) per SM (pair)
-  const int unit_rows = pair ? 512 : 256, cta_per_unit = pair ? 2 : 1;
-  const long long work = static_cast<long long>(bh) * ((S + unit_rows - 1) / unit_rows);
-  const int units = static_cast<int>(std::min<long long>(work, sm_count() / cta_per_unit));
-  const int grid = units * cta_per_unit;
-  a.work_list = nullptr;
-  a.work_off = nullptr;
-  if (causal && use_work_lists()) {
-    const WorkLists wl =
-        causal_work_lists(pair ? 2 : 0, static_cast<int>(bh), S, units, static_cast<cudaStream_t>(stream));
-    a.work_list = wl.list;
-    a.work_off = wl.off;
+  auto launch_as = [&](bool pair) {
+    // a CTA of a pair loads half the keys of a K tile (per head-dim half)
+    const cuuint32_t box_k[3] = {64, static_cast<cuuint32_t>(pair ? p.kv_tile / 2 : p.kv_tile), 1};
+    const CUtensorMap tk = make_map(k, 3, dims, strides, box_k);
+    // persistent: one work unit (CTA, or CTA pair of 512 query rows) per SM (pair)
+    const int unit_rows = pair ? 512 : 256, cta_per_unit = pair ? 2 : 1;
+    const long long work = static_cast<long long>(bh) * ((S + unit_rows - 1) / unit_rows);
+    const int units = static_cast<int>(std::min<long long>(work, std::max(1, sm_count() / cta_per_unit)));
+    const int grid = units * cta_per_unit;
+    a.work_list = nullptr;
+    a.work_off = nullptr;
+    if (causal && use_work_lists()) {
+      const WorkLists wl =
+          causal_work_lists(pair ? 2 : 0, static_cast<int>(bh), S, units, static_cast<cudaStream_t>(stream));
+      a.work_list = wl.list;
+      a.work_off = wl.off;
+    }
+    return twfa::fa_fwd_launch(tq, tk, tv, p, a, grid, static_cast<cudaStream_t>(stream), allow_specialized(),
+                               pair);
+  };
+  const bool pair = use_pairs(p);
+  cudaError_t e = launch_as(pair);
+  if (pair && (e == cudaErrorInvalidClusterSize || e == cudaErrorLaunchOutOfResources) &&
+      twfa::fa_fwd_smem_bytes(p, false) <= 227 * 1024) {
+    // the device cannot co-schedule the CTA pairs (e.g. a partitioned GPU):
+    // the same plan as one CTA per tile (bit-identical outputs)
+    cudaGetLastError();
+    e = launch_as(false);
   }
-  check(twfa::fa_fwd_launch(tq, tk, tv, p, a, grid, static_cast<cudaStream_t>(stream), allow_specialized(), pair),
-        "fa_fwd launch");
+  check(e, "fa_fwd launch");
   return TWFA_OK;
 }
 
