@@ -49,7 +49,7 @@ def edge(src, dst, d, delta=0, blocking=False):
     return e
 
 
-def fa_forward_problem(tc_variable_latency=False, calibrated=False, s_ring=1, split_s=False):
+def fa_forward_problem(tc_variable_latency=False, calibrated=False, s_ring=1, split_s=False, ex_split=False):
     """FA-forward loop body on sm_100a: two 128-row Q sub-tiles (k = 0, 1)
     share one 128-key K/V tile per iteration.
 
@@ -128,6 +128,28 @@ def fa_forward_problem(tc_variable_latency=False, calibrated=False, s_ring=1, sp
                       # S_k(i+1) overwrites the TMEM columns P_k(i) is read from: the
                       # calibrated model waits for PV_k's completion (cross-warp commit)
                       edge(f"PV{k}", f"S{k}", cost["PV"] if calibrated else 0, delta=s_ring)]
+        if ex_split:
+            # EX_k as its MUFU part (EXM_k: 16384 exp2 at 16/clk = 4 units)
+            # and its FMA part (EXF_k: scale-subtract, bf16 pack, row sum and
+            # the P stores, the rest of the calibrated EX); analysis only
+            # (the kernel realizes EX as one op)
+            exm = 4
+            exf = max(1, cost["EX"] - exm)
+            nodes += [node(f"MX{k}", "ALU", cost["MX"], regs=kv, spill_cost=spill, warps_required=4),
+                      # the exponentials' values stay in the warpgroup's registers
+                      # until EXF packs and stores them: a whole EX as spill cost
+                      node(f"EXM{k}", "MUFU", exm, regs=kv // 2, spill_cost=cost["EX"], warps_required=4),
+                      node(f"EXF{k}", "FMA", exf, regs=kv // 2, warps_required=4),
+                      node(f"CR{k}", "FMA", cost["CR"], regs=64, warps_required=4),
+                      node(f"PV{k}", "TC", cost["PV"], footprint={"tmem": 128})]
+            edges += [edge(f"MX{k}", f"EXM{k}", cost["MX"]), edge(f"EXM{k}", f"EXF{k}", exm),
+                      edge(f"MX{k}", f"MX{k}", cost["MX"], delta=1), edge(f"EXM{k}", f"EXM{k}", exm, delta=1),
+                      edge(f"EXF{k}", f"EXF{k}", exf, delta=1), edge(f"MX{k}", f"CR{k}", cost["MX"]),
+                      edge(f"EXF{k}", f"PV{k}", exf, blocking=True), edge("LDV", f"PV{k}", 0, blocking=True),
+                      edge(f"CR{k}", f"PV{k}", cost["CR"], blocking=True),
+                      edge(f"PV{k}", f"CR{k}", cost["PV"], delta=1, blocking=True),
+                      edge(f"PV{k}", f"PV{k}", cost["PV"], delta=1)]
+            continue
         nodes += [
             # split S: SA_k(i+1) overwrites S columns right after MX_k(i) read them,
             # so the S row (MX_k's value) cannot be re-read by a consumer on another
