@@ -49,7 +49,7 @@ def steady_programs_from_reference(ws, prob, sol):
     return prog, per_warp, stage, warp
 
 
-@pytest.mark.parametrize("name", ["fa_fwd", "gemm_mainloop", "fa_bwd"])
+@pytest.mark.parametrize("name", ["fa_fwd", "gemm_mainloop", "fa_bwd", "fa_bwd_pp"])
 def test_plan_equals_reference_program(twfa, ws, name):
     prob, sol = twfa.load_schedule(name)
     d = twfa.Plan(prob, sol).describe()
@@ -205,3 +205,47 @@ def test_tile_makespan_formula_matches_reference_simulate(twfa, ws):
     s = json.loads(sol)
     for n in (2, 3, 17, 64):  # the replay needs at least `copies` iterations
         assert ws.simulate(prob, sol, n)["cycles"] == (n - 1) * s["I"] + s["L"]
+
+
+def test_fa_bwd_pp_plan_roles_follow_the_solver(twfa):
+    """Two 64-query sub-tiles: EXB_k / DS_k fused on the solver's warpgroup of
+    sub-tile k, RD_k on its own, all tensor-core ops on one warp in slot
+    order, and the last reader of Q_i (dO_i) in issue order releases the slot."""
+    prob, sol = twfa.load_schedule("fa_bwd_pp")
+    s = json.loads(sol)
+    d = twfa.Plan(prob, sol).describe()
+    assert d["family"] == "fa_bwd" and d["num_tiles"] == 2
+    assert d["warpgroups"] == {"exp_ds0": s["A"]["EXB0"], "exp_ds1": s["A"]["EXB1"],
+                               "dq_reduce0": s["A"]["RD0"], "dq_reduce1": s["A"]["RD1"]}
+    for k in (0, 1):
+        assert s["A"][f"DS{k}"] == s["A"][f"EXB{k}"]
+    mma = d["warp_programs"][str(d["mma_warp"])]
+    tc = [v for v in mma if not v.startswith("LD")]
+    assert sorted(tc) == sorted(f"{op}{k}" for op in ("ST", "DP", "DV", "DK", "DQ") for k in (0, 1))
+    assert tc == sorted(tc, key=lambda v: (s["M"][v] // s["I"], s["M"][v] % s["I"]))
+    last = lambda ids: max(ids, key=lambda v: (s["M"][v] // s["I"], mma.index(v)))  # noqa: E731
+    assert sorted(d["ring_release"]) == sorted([last(["ST0", "ST1", "DK0", "DK1"]),
+                                                last(["DP0", "DP1", "DV0", "DV1"])])
+
+
+@pytest.mark.parametrize("mutate,msg", [
+    (lambda s: s["A"].update(DS0=s["A"]["RD0"]), "spill|share a warpgroup"),
+    (lambda s: s["A"].update(DQ1=14), "variable_latency|issue from one warp"),
+    (lambda s: s["A"].update(RD1=s["A"]["EXB1"]), "register|own|spill"),
+    (lambda s: s["M"].update(DS0=s["M"]["EXB0"]), "dependence"),
+])
+def test_fa_bwd_pp_unrealizable_solutions_are_rejected(twfa, mutate, msg):
+    prob, sol = twfa.load_schedule("fa_bwd_pp")
+    s = json.loads(sol)
+    mutate(s)
+    with pytest.raises(ValueError, match=msg):
+        twfa.Plan(prob, json.dumps(s))
+
+
+def test_fa_bwd_pp_without_aliasing_edges_is_rejected(twfa):
+    # the kernel relies on the graph's tensor-memory / shared-memory aliasing edges
+    prob, sol = twfa.load_schedule("fa_bwd_pp")
+    p = json.loads(prob)
+    p["graph"]["edges"] = [e for e in p["graph"]["edges"] if not (e["src"] == "RD0" and e["dst"] == "ST0")]
+    with pytest.raises(ValueError, match="aliasing edge|dependence|validate"):
+        twfa.Plan(json.dumps(p), sol)
