@@ -132,10 +132,6 @@ struct BwdState {
   int q_target, o_target;  // loads the trip program has asked for so far
   uint32_t trace_n;        // records of this warp in the issue trace
   uint32_t* rec;           // the current op's trace record (t_ready stamped after its waits)
-  // MMA warp: 1 + the last global iteration whose Q (dO) tile this warp has
-  // already seen land; a second tensor-core reader of the tile skips the
-  // wait (an observed mbarrier phase stays observed: ~100-400 clk saved)
-  uint32_t q_seen, o_seen;
 };
 // t_ready of the current op's trace record: its inputs have been awaited
 __device__ __forceinline__ void bwd_ready(BwdState& st) {
@@ -560,15 +556,10 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
     if (it == 0) mbar_wait(&bar.kv_full, t.icount & 1);
     // P^T(g-1) was read by DV(g-1) (in order) and, with DS on its own
     // warpgroup, by DS(g-1) (p_read)
-    if (g > 0 && (op.flags & TWFA_OPF_WAIT_PREAD)) {
-      if (st.q_seen == g + 1)
-        mbar_wait(&bar.p_read, (g - 1) & 1);
-      else
-        mbar_wait_all(&bar.q_full[qs], (g / plan.k_depth) & 1, &bar.p_read, (g - 1) & 1);
-    } else if (st.q_seen != g + 1) {
+    if (g > 0 && (op.flags & TWFA_OPF_WAIT_PREAD))
+      mbar_wait_all(&bar.q_full[qs], (g / plan.k_depth) & 1, &bar.p_read, (g - 1) & 1);
+    else
       mbar_wait(&bar.q_full[qs], (g / plan.k_depth) & 1);
-    }
-    st.q_seen = g + 1;
     tc_fence_after();
     bwd_ready(st);
 #if TWFA_BWD_PROF
@@ -587,15 +578,10 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
     __syncwarp();
   } else if (op.kind == TWFA_OP_DP) {
     if (it == 0) mbar_wait(&bar.kv_full, t.icount & 1);
-    if (g > 0) {  // dQ_(g-1) (over dP^T) has been read out
-      if (st.o_seen == g + 1)
-        mbar_wait(&bar.q_free, (g - 1) & 1);
-      else
-        mbar_wait_all(&bar.o_full[os], (g / plan.v_depth) & 1, &bar.q_free, (g - 1) & 1);
-    } else if (st.o_seen != g + 1) {
+    if (g > 0)  // dQ_(g-1) (over dP^T) has been read out
+      mbar_wait_all(&bar.o_full[os], (g / plan.v_depth) & 1, &bar.q_free, (g - 1) & 1);
+    else
       mbar_wait(&bar.o_full[os], (g / plan.v_depth) & 1);
-    }
-    st.o_seen = g + 1;
     tc_fence_after();
     bwd_ready(st);
 #if TWFA_BWD_PROF
@@ -617,14 +603,10 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
     // the accumulator is overwritten at iteration 0: the previous work
     // item's dK / dV must have been read out
     if (it == 0 && t.icount > 0) mbar_wait(&bar.acc_free, (t.icount - 1) & 1);
-    uint32_t& seen = dv ? st.o_seen : st.q_seen;
-    uint64_t* tile_full = dv ? &bar.o_full[os] : &bar.q_full[qs];
-    const uint32_t tile_ph = dv ? (g / plan.v_depth) & 1 : (g / plan.k_depth) & 1;
-    if (seen == g + 1)
-      mbar_wait(dv ? &bar.p_full : &bar.ds_full, g & 1);
+    if (dv)
+      mbar_wait_all(&bar.p_full, g & 1, &bar.o_full[os], (g / plan.v_depth) & 1);
     else
-      mbar_wait_all(dv ? &bar.p_full : &bar.ds_full, g & 1, tile_full, tile_ph);
-    seen = g + 1;
+      mbar_wait_all(&bar.ds_full, g & 1, &bar.q_full[qs], (g / plan.k_depth) & 1);
     tc_fence_after();
     bwd_ready(st);
 #if TWFA_BWD_PROF
@@ -668,7 +650,7 @@ __device__ __forceinline__ void bwd_run(const BwdCtx& c, const TwfaDevicePlan& p
   const int plen = plan.prog_len[c.warp];
   const bool is_load = c.warp == static_cast<uint32_t>(plan.load_warp);
   const bool is_mma = c.warp == static_cast<uint32_t>(plan.mma_warp);
-  BwdState st{0, 0, -1, -1, 0, nullptr, 0, 0};
+  BwdState st{0, 0, -1, -1, 0, nullptr};
   uint32_t gbase = 0, icount = 0;
   for (int i = 0;; ++i, ++icount) {
     int work;
