@@ -79,7 +79,9 @@ int twfa_plan_raw(const twfa_plan* plan, void* dst, size_t cap, size_t* needed);
  * q, k, v, o: [B, H, S, 128] contiguous bf16 device buffers; lse: [B, H, S]
  * fp32 or NULL. causal: key j visible to query i iff j <= i. stream: a
  * cudaStream_t (NULL = legacy default stream). The plan must come from an
- * FA-forward loop problem. */
+ * FA-forward loop problem. Plans with 128-key K/V tiles and an unsplit S run
+ * as clusters of two CTAs (tcgen05 cta_group::2; environment TWFA_PAIR=0
+ * selects one CTA per work tile, with bit-identical results). */
 int twfa_fa_fwd(const twfa_plan* plan, const void* q, const void* k, const void* v, void* o, float* lse,
                 int B, int H, int S, int D, int causal, float softmax_scale, void* stream);
 
