@@ -387,6 +387,27 @@ def realized_schedule(twfa, plan, q, k, v, causal):
             "how": "traced launch, CTA 0, median S1 issue-to-issue; tracing adds ~10%"}
 
 
+def in_kernel_clock(twfa, plan, q, k, v, causal):
+    """The SM clock the forward actually ran at: one traced launch of the same
+    workload right after the timed region (same power state); the kernel
+    stamps clock64 and %globaltimer in CTA 0 after its setup and at its
+    teardown (words 1-4 of the trace). NVML samples (averaged over
+    milliseconds) overstate the clock of a short burst: the board's power
+    limit pulls the clock down within milliseconds of the kernel starting."""
+    import numpy as np
+    import torch
+    nw, cap = plan.describe()["num_warps"], 64
+    tr = torch.zeros(nw * cap * 8, dtype=torch.int32, device=q.device)
+    twfa.fa_fwd(plan, q, k, v, causal=causal, trace=tr, trace_cap=cap)
+    torch.cuda.synchronize()
+    w = tr[:5].cpu().numpy().view(np.uint32).astype(np.int64)
+    clk = (w[3] - w[1]) % (1 << 32)
+    ns = (w[4] - w[2]) % (1 << 32)
+    return {"sm_mhz": round(clk / ns * 1e3) if ns else None, "cta0_ms": round(ns / 1e6, 3),
+            "how": "CTA 0's clock64 / %globaltimer span (setup to teardown) in one traced launch after the "
+                   "timed region"}
+
+
 def ncu_reference(workload):
     """Static ncu evidence for the kernel (profiles/ncu_summary.json): the
     DRAM traffic per launch and the ncu tensor-pipe figure, tagged with the SM
@@ -579,6 +600,15 @@ def run_ours(args, ranks):
                                       "xu_pipe_inst_pct": ncu.get("xu_pipe_inst_pct"), "sm_ghz": ncu.get("sm_ghz"),
                                       "source": "profiles/ncu_summary.json (ncu --set full --clock-control none, "
                                                 "one launch)"}
+    if world == 1 and n_local:
+        # the clock the kernel ran at (NVML's median can miss the power cap's
+        # pull-down in a short timed region); tensor-pipe fraction per clock
+        # from it
+        ik = in_kernel_clock(twfa, plan, q, k, v, causal)
+        line["tensor_pipe"]["in_kernel_clock"] = ik
+        if ik.get("sm_mhz"):
+            line["tensor_pipe"]["busy_frac_at_kernel_clock"] = \
+                achieved * 1e12 / (sms * SM_FLOP_PER_CLK * ik["sm_mhz"] * 1e6)
     if not args.skip_legs:
         line["schedule_realized"] = realized_schedule(twfa, plan, q, k, v, causal)
         # whole work tile, untraced: the modulo schedule's makespan for N

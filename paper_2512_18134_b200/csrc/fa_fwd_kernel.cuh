@@ -173,6 +173,16 @@ __shared__ FaShared g_sh;
 // ordinal of the CTA, K/V iterations of that tile}. A streamed load that
 // runs ahead into the next work tile records that tile and its iteration.
 constexpr int kTraceWords = 8;
+// Record 0 of warp 0 (unused by the op records, which start at 1) holds CTA
+// 0's own clock: words 1 / 2 = clock64 / %globaltimer (ns) after the setup
+// barrier, 3 / 4 = the same at teardown (low 32 bits): the SM clock the
+// kernel ran at, independent of the other CTAs' finishing times.
+__device__ __forceinline__ void trace_clock(const FaArgs& a, int word) {
+  if (a.trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
+    a.trace[word] = static_cast<uint32_t>(clock64());
+    a.trace[word + 1] = static_cast<uint32_t>(global_timer_ns());
+  }
+}
 
 template <bool kTrace>
 __device__ __forceinline__ uint32_t* trace_begin(const FaArgs& a, uint32_t warp, uint32_t& n, int node, int it,
@@ -1106,6 +1116,7 @@ __device__ __forceinline__ FaCtx fa_setup(int tiles, int kd, int vd, int load_wa
   // column 0, lane 0, so the base is the compile-time constant 0
   if (bar.tmem_base != 0) __trap();
   c.tmem = 0;
+  trace_clock(args, 1);
   c.scale_log2 = args.scale_log2;
   c.S = args.S;
   c.BH = args.B * args.H;
@@ -1123,17 +1134,19 @@ __device__ __forceinline__ FaCtx fa_setup(int tiles, int kd, int vd, int load_wa
 }
 
 template <bool P>
-__device__ __forceinline__ void fa_teardown(const FaCtx& c) {
+__device__ __forceinline__ void fa_teardown(const FaCtx& c, const FaArgs& args) {
   if (c.lane == 0) bulk_wait_all();  // epilogue bulk stores of this warp (if any) are complete
   tc_fence_before();
   if constexpr (P) {
     cluster_sync();  // neither CTA leaves while the pair's MMAs may touch its memory
+    trace_clock(args, 3);  // every warp of CTA 0 is done
     if (c.warp == 0) {
       tc_fence_after();
       tmem_dealloc_pair<512>(c.tmem);
     }
   } else {
     __syncthreads();
+    trace_clock(args, 3);
     if (c.warp == 0) {
       tc_fence_after();
       tmem_dealloc<512>(c.tmem);
@@ -1191,7 +1204,7 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
     set_register_class<false>(heavy_wgs);
     run_interp<KV, false, kTrace, P>(c, tm, args, plan.num_tiles, plan.max_stage, plan.load_warp, plan.cr_warp, rg);
   }
-  fa_teardown<P>(c);
+  fa_teardown<P>(c, args);
 }
 
 // ---------------------------------------------------------------- specialized
@@ -1294,7 +1307,7 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
     set_register_class<false>(heavy_wgs);
     spec_dispatch_light<I, kTrace, P>(c, tm, args, std::make_integer_sequence<int, nw>{});
   }
-  fa_teardown<P>(c);
+  fa_teardown<P>(c, args);
 }
 
 bool same_plan(const TwfaDevicePlan& a, const TwfaDevicePlan& b) {

@@ -15,6 +15,11 @@ TWFA_DEV uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 TWFA_DEV uint32_t lane_id() { return threadIdx.x & 31u; }
+TWFA_DEV uint64_t global_timer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 TWFA_DEV uint32_t warp_id() { return __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0); }
 // One lane of the (converged) warp: elect.sync, which ptxas knows selects a
 // single thread, so tcgen05 / TMA issue keeps its operands in uniform registers.
