@@ -677,7 +677,7 @@ def side_legs(twfa, plan, dev, stream):
                                    "algorithmic_bytes": (M * K + N * K + M * N) * 2,
                                    # dram__bytes_read.sum + dram__bytes_write.sum of one launch
                                    # (ncu, profiles/r02b_gemm_policy.txt, default L2 policy)
-                                   "traffic": 1.07e9 + 0.127e9},
+                                   "traffic": 0.994e9 + 0.127e9},
                       "kernel": "twfa::gemm_kernel (CTA pair, cta_group::2, 256x256 tiles, TMA-store epilogue)",
                       "workload": "BASELINE config 2: GEMM mainloop bf16 8192^3 (C = A B^T), 20 launches"}
     return out

@@ -52,6 +52,9 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
   const int local = t % per_group;
   tm = first_m + local % gm;
   tn = local / gm;
+  // odd groups sweep N backwards, so the B columns of the last wave of a
+  // group are the first the next group reads (still in L2)
+  if (group & 1) tn = tiles_n - 1 - tn;
 }
 
 }  // namespace
