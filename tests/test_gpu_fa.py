@@ -319,3 +319,14 @@ def test_cta_pair_against_oracle(twfa, plan, monkeypatch):
     monkeypatch.setenv("TWFA_PAIR", "1")
     _check(twfa, plan, 1, 3, 1000, True, 32)
     _check(twfa, plan, 1, 3, 768, False, 33)
+
+
+@pytest.mark.parametrize("S,causal", [(1, False), (1, True), (17, False), (129, True), (513, False)])
+def test_tiny_and_odd_lengths_in_both_realizations(twfa, plan, S, causal, monkeypatch):
+    """A single key, one query row, lengths one past a tile: the CTA pair's
+    peer rows (and most of the leader's) lie past the sequence end."""
+    q, k, v = _inputs(1, 2, S, 128, 34)
+    monkeypatch.setenv("TWFA_PAIR", "1")
+    _check_qkv(twfa, plan, q, k, v, causal)
+    monkeypatch.setenv("TWFA_PAIR", "0")
+    _check_qkv(twfa, plan, q, k, v, causal)
