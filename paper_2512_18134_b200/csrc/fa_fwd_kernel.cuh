@@ -92,6 +92,17 @@ constexpr float kRescaleLog2 = 8.0f;
 #ifndef TWFA_TMA_EPILOGUE
 #define TWFA_TMA_EPILOGUE 1
 #endif
+// MX_k(g) hands its rescale factors to CR_k(g) through the double-buffered
+// stats slot g % 2. The slot is free again by construction when MX_k(g + 2)
+// writes it: CR_k(g) reads it before arriving o_ready, PV_k(g) waits for
+// o_ready, S_k(g + 2) follows PV_k(g) (in order on one thread, or behind
+// PV_k's commit), and MX_k(g + 2) waits for S_k(g + 2). The explicit
+// slot-empty wait is kept (TWFA_ST_EMPTY = 1): dropping it measured 9 %
+// slower, the mbarrier round trip paces the two softmax warpgroups' turns
+// on MUFU (a MUFU token that makes them alternate strictly: -2 to -4 %).
+#ifndef TWFA_ST_EMPTY
+#define TWFA_ST_EMPTY 1
+#endif
 // What-if knobs for sensitivity experiments (timing only; results are WRONG
 // when set): 1 = half the exponentials on MUFU (the rest reuse them),
 // 3 = MX reads half the row, 4 = no K/V loads after the first ring fill,
@@ -742,7 +753,7 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
     const uint32_t sb = g & 1;
     mbar_wait(&bar.st_full[k][sb], (g >> 1) & 1);
     const float alpha = g_sh.stats[k][sb][c.quad * 32 + lane];
-    warp_arrive(&bar.st_empty[k][sb]);
+    if (TWFA_ST_EMPTY) warp_arrive(&bar.st_empty[k][sb]);
     // with the rescale threshold most iterations keep the max: then O is
     // not touched and the correction only forwards the handoff
     if (it > 0 && !__all_sync(0xffffffffu, alpha == 1.f)) {
@@ -795,7 +806,7 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
             float m = m_old, alpha = 1.f;
             const uint32_t sb = g & 1;
             const float sum = mx_ex_spec<KV, P>(srow, taddr, c.scale_log2, m, alpha, bar.p_part[k][b], [&](float al) {
-              mbar_wait(&bar.st_empty[k][sb], ((g >> 1) & 1) ^ 1);
+              if (TWFA_ST_EMPTY) mbar_wait(&bar.st_empty[k][sb], ((g >> 1) & 1) ^ 1);
               g_sh.stats[k][sb][c.quad * 32 + lane] = al;
               warp_arrive(&bar.st_full[k][sb]);
             }, [&] {
@@ -848,7 +859,7 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
         wr(st.alpha, k, m_new == m_old ? 1.f : fast_exp2(m_old - m_safe));
         wr(st.m_run, k, m_new);
         const uint32_t sb = g & 1;
-        mbar_wait(&bar.st_empty[k][sb], ((g >> 1) & 1) ^ 1);
+        if (TWFA_ST_EMPTY) mbar_wait(&bar.st_empty[k][sb], ((g >> 1) & 1) ^ 1);
         g_sh.stats[k][sb][c.quad * 32 + lane] = rd(st.alpha, k);
         warp_arrive(&bar.st_full[k][sb]);
         trace_mark<kTrace>(tr, 5);
