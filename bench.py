@@ -635,7 +635,8 @@ def run_ours(args, ranks):
 
 def side_legs(twfa, plan, dev, stream):
     """Rank 0, after the timed region: C3 (the round-1 headline shape, short
-    burst) and the C2 GEMM mainloop 8192^3 with its own roofline."""
+    burst), C4 (causal) and the C2 GEMM mainloop 8192^3 with its own
+    roofline."""
     import torch
     peak, _, _ = measured_peaks()
     out = {}
@@ -655,6 +656,22 @@ def side_legs(twfa, plan, dev, stream):
     f = fa_flops(128, 8192, False)
     out["c3"] = {"tflops": f / (ms * 1e-3) / 1e12, "ms": ms, "launches": 20,
                  "workload": "C3 B=4 H=32 S=8192 non-causal, 20 launches back to back"}
+    del q, k, v, o
+    # C4: causal, B=2 H=32 S=16384 (flops of the unmasked triangle)
+    g.manual_seed(2027)
+    q, k, v = (torch.randn(2, 32, 16384, D, device=dev, generator=g).to(torch.bfloat16) for _ in range(3))
+    o = torch.empty_like(q)
+    for _ in range(3):
+        twfa.fa_fwd(plan, q, k, v, causal=True, out=o)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(20):
+        twfa.fa_fwd(plan, q, k, v, causal=True, out=o)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 20
+    out["c4"] = {"tflops": fa_flops(64, 16384, True) / (ms * 1e-3) / 1e12, "ms": ms, "launches": 20,
+                 "workload": "C4 B=2 H=32 S=16384 causal (flops of the unmasked triangle), 20 launches"}
     del q, k, v, o
     gp = twfa.Plan(*twfa.load_schedule("gemm_mainloop"))
     M = N = K = 8192
