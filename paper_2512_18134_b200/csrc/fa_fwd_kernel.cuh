@@ -355,6 +355,9 @@ __device__ __forceinline__ float exp_store_row(const uint32_t (&s)[N], uint32_t 
 // TWFA_LATE_SUM: the row sum of chunks 1.. is taken after the last P part is
 // released (the fp32 P overwrites the consumed S registers), so the FADD2s
 // leave the MUFU-bound path to PV
+#ifndef TWFA_CHUNK_PHASED
+#define TWFA_CHUNK_PHASED 0  // measured: all FFMA2 arguments of a chunk before its MUFU ops, -0.6 % (C3, C4)
+#endif
 #ifndef TWFA_LATE_SUM
 #define TWFA_LATE_SUM 1  // measured: +0.9 % (pair) / +1.4 % (one CTA) per clock under the power cap, +4 % burst
 #endif
@@ -380,10 +383,21 @@ __device__ __forceinline__ float mx_ex_spec(uint32_t (&s)[N], uint32_t taddr, fl
   uint32_t pk0[kRegs];
   auto chunk = [&](int c, float m, uint32_t (&pk)[kRegs]) {
     const float2 nm2 = make_float2(-m, -m);
+    if (TWFA_CHUNK_PHASED) {  // all exponent arguments first, so every MUFU input is ready when it issues
+#pragma unroll
+      for (int i = 0; i < kKeys; i += 2) {
+        const int e = c * kKeys + i;
+        const float2 x = ffma2(make_float2(__uint_as_float(s[e]), __uint_as_float(s[e + 1])), sl2, nm2);
+        s[e] = __float_as_uint(x.x);
+        s[e + 1] = __float_as_uint(x.y);
+      }
+    }
 #pragma unroll
     for (int i = 0; i < kKeys; i += 2) {
       const int e = c * kKeys + i;
-      const float2 x = ffma2(make_float2(__uint_as_float(s[e]), __uint_as_float(s[e + 1])), sl2, nm2);
+      const float2 x = TWFA_CHUNK_PHASED
+                           ? make_float2(__uint_as_float(s[e]), __uint_as_float(s[e + 1]))
+                           : ffma2(make_float2(__uint_as_float(s[e]), __uint_as_float(s[e + 1])), sl2, nm2);
       float2 p;
       if (TWFA_WHATIF == 1 && e >= N / 2) {
         p = x;
