@@ -64,6 +64,26 @@ constexpr uint32_t kSdHi = sdesc_hi(1024);
 #define TWFA_BWD_RED 0
 #endif
 // debug variant: CTA 0 prints per-op enter / exit clocks of iterations 20-21
+// Skip an MMA-warp wait on a barrier phase this warp already saw complete
+// (DK / DQ / DV after ST / DP / DK of the same iteration). An mbarrier wait
+// costs the MMA warp ~160 clk even on a completed phase, and it queues behind
+// the warp's own tcgen05 instructions, so each redundant wait delays the
+// next op's issue while the tensor core drains its short queue.
+#ifndef TWFA_BWD_MEMO
+#define TWFA_BWD_MEMO 1
+#endif
+// RD reads the whole dQ_i row out of tensor memory before staging it
+// (TWFA_BWD_RD_FULL), so q_free -- which DP_(i+1) waits for -- is signalled
+// right after the read instead of after half of the staging and reduction
+#ifndef TWFA_BWD_RD_FULL
+#define TWFA_BWD_RD_FULL 1
+#endif
+#ifndef TWFA_BWD_SOLO
+#define TWFA_BWD_SOLO 0  // measured: 680 vs 693 TF/s (C3); with the loads on warp 14 699
+#endif
+#ifndef TWFA_BWD_LOAD_WARP
+#define TWFA_BWD_LOAD_WARP -1
+#endif
 #ifndef TWFA_BWD_PROF
 #define TWFA_BWD_PROF 0
 #endif
@@ -132,6 +152,9 @@ struct BwdState {
   int q_target, o_target;  // loads the trip program has asked for so far
   uint32_t trace_n;        // records of this warp in the issue trace
   uint32_t* rec;           // the current op's trace record (t_ready stamped after its waits)
+  // MMA warp: iteration + 1 whose Q_i / dO_i / P^T / dS^T this warp has already
+  // seen land (TWFA_BWD_MEMO): a later op of the same iteration skips its wait
+  uint32_t q_seen, o_seen, p_seen, ds_seen;
 };
 // t_ready of the current op's trace record: its inputs have been awaited
 __device__ __forceinline__ void bwd_ready(BwdState& st) {
@@ -165,6 +188,7 @@ __device__ __forceinline__ uint32_t* bwd_trace(const FaBwdArgs& a, const BwdCtx&
 #ifndef TWFA_BWD_LAZY_LOADS
 #define TWFA_BWD_LAZY_LOADS 0  // measured: 712 vs 764 TFLOP/s (C3 shape), eager is faster
 #endif
+template <bool kSolo>
 __device__ __forceinline__ void bwd_top_up(const BwdCtx& c, const FaBwdArgs& a, const BwdItem& t, BwdState& st,
                                            const TwfaDevicePlan& plan, bool is_q, int upto, bool blocking) {
   BwdBarriers& bar = g_bb;
@@ -177,12 +201,12 @@ __device__ __forceinline__ void bwd_top_up(const BwdCtx& c, const FaBwdArgs& a, 
     uint64_t* empty = is_q ? &bar.q_empty[s] : &bar.o_empty[s];
     if (blocking) {
       mbar_wait(empty, ph ^ 1);
-    } else if (!__all_sync(0xffffffffu, mbar_try_wait(empty, ph ^ 1))) {
+    } else if (kSolo ? !mbar_try_wait(empty, ph ^ 1) : !__all_sync(0xffffffffu, mbar_try_wait(empty, ph ^ 1))) {
       return;
     }
     ++next;
     uint64_t* full = is_q ? &bar.q_full[s] : &bar.o_full[s];
-    if (elect_one()) {
+    if (lead<kSolo>()) {
       uint8_t* dst = (is_q ? c.q : c.o) + s * kTile;
       const CUtensorMap* map = is_q ? &a.tm_q : &a.tm_do;
       const int row = (t.q_first + lit) * kT;
@@ -190,7 +214,7 @@ __device__ __forceinline__ void bwd_top_up(const BwdCtx& c, const FaBwdArgs& a, 
       tma_load_3d(dst, map, full, 0, row, t.bh, c.pol);
       tma_load_3d(dst + kHalf, map, full, 64, row, t.bh, c.pol);
     }
-    __syncwarp();
+    wsync<kSolo>();
   }
 }
 
@@ -337,6 +361,7 @@ __device__ __forceinline__ void ds_part(const BwdCtx& c, const FaBwdArgs& a, con
 // RD: dQ_i from TMEM (row = query) -> smem staging (fp32, SW128 boxes of
 // 128 rows x 32 columns) -> cp.reduce.async.bulk add into the fp32 dQ
 // accumulator (the atomic reduction of the paper's backward loop).
+template <bool kFull>
 __device__ __forceinline__ void rd_op(const BwdCtx& c, const FaBwdArgs& a, const BwdItem& t, int it, uint32_t g,
                                       const TwfaDevicePlan& plan, BwdState& st) {
   // staging buffer: Q_i's ring slot when the schedule says so (plan.s_split
@@ -390,6 +415,42 @@ __device__ __forceinline__ void rd_op(const BwdCtx& c, const FaBwdArgs& a, const
     tc_fence_before();
     warp_arrive(&bar.q_free);
     if (leader) mbar_arrive(q_stage ? &bar.q_empty[qs] : &bar.ds_free);
+    return;
+  }
+  if constexpr (kFull) {
+    // the whole dQ_i row comes out of tensor memory first (128 registers),
+    // so DP_(i+1) may overwrite the columns before any staging starts; the
+    // four 32-column boxes then alternate over the two staging halves
+    uint32_t v[128];
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc)
+      tmem_ld32(c.lane_off + kColP + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(&v[cc * 32]));
+    tmem_ld_wait();
+    tc_fence_before();
+    warp_arrive(&bar.q_free);
+#pragma unroll
+    for (int box = 0; box < 4; ++box) {
+      const int hb = box & 1;
+      if (box >= 2) {
+        if (leader) bulk_wait_read_1();  // the reduce of box - 2 has read this half
+        named_bar_sync(nb, 128);
+      }
+      const uint32_t base = smem_u32(stage_buf) + hb * kHalf + r * 128;
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch)
+        st_shared_v4(base + ((ch ^ (r & 7)) << 4), v[box * 32 + 4 * ch], v[box * 32 + 4 * ch + 1],
+                     v[box * 32 + 4 * ch + 2], v[box * 32 + 4 * ch + 3]);
+      fence_proxy_async_shared();
+      named_bar_sync(nb, 128);
+      if (leader) {
+        tma_reduce_add_3d(&a.tm_dq, stage_buf + hb * kHalf, 32 * box, q0, t.bh);
+        bulk_commit();
+      }
+    }
+    if (leader) {
+      bulk_wait_read();
+      mbar_arrive(q_stage ? &bar.q_empty[qs] : &bar.ds_free);
+    }
     return;
   }
   // DQ_i has completed (dq_full): the dS buffer is free for staging. Its two
@@ -472,7 +533,23 @@ __device__ __forceinline__ void kv_epilogue(const BwdCtx& c, const FaBwdArgs& a,
 // warpgroups -- one warpgroup running both (P^T carried in registers) or
 // one each (DS reads P^T back from tensor memory), as the schedule places
 // them.
-enum BwdRole { kLight = 0, kReduce = 1, kExbDs = 2, kExb = 3, kDs = 4 };
+enum BwdRole { kLight = 0, kReduce = 1, kExbDs = 2, kExb = 3, kDs = 4, kReduceFull = 5, kLightSolo = 6 };
+// kLightSolo: the TMA / MMA warp's trip program runs on one elected lane
+// (TWFA_BWD_SOLO). Measured (tools/calib/ubench_mmaloop.cu): a warp that
+// waits, elects a lane for each op's MMAs and re-converges with __syncwarp
+// keeps the tensor core 65-72 % busy on 8-MMA ops of 64 clk each; one lane
+// issuing the same ops (with the same waits) keeps it 89-96 % busy. In the
+// kernels it does not carry over (backward 680 vs 693 TF/s, forward -4 to
+// -9 % per clock), so both default to the warp-wide form.
+__host__ __device__ constexpr bool is_light(int role) { return role == kLight || role == kLightSolo; }
+
+// dS^T(g) has landed. With EXB and DS on one warpgroup, the same warps
+// arrived P^T(g) (p_full) before dS^T(g) (ds_full), so P^T(g) has landed too.
+__device__ __forceinline__ void bwd_wait_ds(BwdState& st, const TwfaDevicePlan& plan, uint32_t g) {
+  mbar_wait(&g_bb.ds_full, g & 1);
+  st.ds_seen = g + 1;
+  if (plan.sm_warp[0] == plan.sm_warp[1]) st.p_seen = g + 1;
+}
 
 // One op of the trip program on this warp, trip r.
 template <int kRole>
@@ -480,12 +557,12 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
                                          BwdState& st, const TwfaDevicePlan& plan, const FaBwdArgs& a) {
   BwdBarriers& bar = g_bb;
   if (op.kind == TWFA_OP_LDQ || op.kind == TWFA_OP_LDO) {
-    if constexpr (kRole == kLight) {
+    if constexpr (is_light(kRole)) {
       const bool is_q = op.kind == TWFA_OP_LDQ;
       const int target = min(t.N - 1, r - static_cast<int>(op.stage) + (is_q ? plan.k_prefetch : plan.v_prefetch));
       (is_q ? st.q_target : st.o_target) = target;
       const int before = is_q ? st.q_next : st.o_next;
-      bwd_top_up(c, a, t, st, plan, is_q, target, !TWFA_BWD_LAZY_LOADS);
+      bwd_top_up<kRole == kLightSolo>(c, a, t, st, plan, is_q, target, !TWFA_BWD_LAZY_LOADS);
       if (a.trace != nullptr)
         for (int lit = before; lit < (is_q ? st.q_next : st.o_next); ++lit) {
           uint32_t* e = bwd_trace(a, c, st, op.node, lit, r, t);
@@ -494,10 +571,10 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
     }
     return;
   }
-  if constexpr (kRole == kLight) {
+  if constexpr (is_light(kRole)) {
     if (TWFA_BWD_LAZY_LOADS) {  // deferred loads: retry without blocking
-      bwd_top_up(c, a, t, st, plan, true, st.q_target, false);
-      bwd_top_up(c, a, t, st, plan, false, st.o_target, false);
+      bwd_top_up<kRole == kLightSolo>(c, a, t, st, plan, true, st.q_target, false);
+      bwd_top_up<kRole == kLightSolo>(c, a, t, st, plan, false, st.o_target, false);
     }
   }
   const int it = r - static_cast<int>(op.stage);
@@ -541,14 +618,15 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
     return;
   }
   if (op.kind == TWFA_OP_RD) {
-    if constexpr (kRole == kReduce) rd_op(c, a, t, it, g, plan, st);
+    if constexpr (kRole == kReduce || kRole == kReduceFull) rd_op<kRole == kReduceFull>(c, a, t, it, g, plan, st);
     return;
   }
-  if constexpr (kRole != kLight) return;
+  if constexpr (!is_light(kRole)) return;
+  constexpr bool kSolo = kRole == kLightSolo;
   // tensor-core ops: warp-uniform descriptors, one elected lane issues
   if (TWFA_BWD_LAZY_LOADS) {  // a deferred load this op needs is forced now
-    if (op.kind == TWFA_OP_ST || op.kind == TWFA_OP_DK) bwd_top_up(c, a, t, st, plan, true, it, true);
-    if (op.kind == TWFA_OP_DP || op.kind == TWFA_OP_DV) bwd_top_up(c, a, t, st, plan, false, it, true);
+    if (op.kind == TWFA_OP_ST || op.kind == TWFA_OP_DK) bwd_top_up<kRole == kLightSolo>(c, a, t, st, plan, true, it, true);
+    if (op.kind == TWFA_OP_DP || op.kind == TWFA_OP_DV) bwd_top_up<kRole == kLightSolo>(c, a, t, st, plan, false, it, true);
   }
   const uint32_t qs = g % plan.k_depth, os = g % plan.v_depth;
   const bool release = op.flags & TWFA_OPF_RELEASE;
@@ -558,15 +636,16 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
     // warpgroup, by DS(g-1) (p_read)
     if (g > 0 && (op.flags & TWFA_OPF_WAIT_PREAD))
       mbar_wait_all(&bar.q_full[qs], (g / plan.k_depth) & 1, &bar.p_read, (g - 1) & 1);
-    else
+    else if (!(TWFA_BWD_MEMO && st.q_seen == g + 1))
       mbar_wait(&bar.q_full[qs], (g / plan.k_depth) & 1);
+    st.q_seen = g + 1;
     tc_fence_after();
     bwd_ready(st);
 #if TWFA_BWD_PROF
     g_prof_ready = clock64();
 #endif
     const uint32_t ad = sd_lo(c.k, 16), bd = sd_lo(c.q + qs * kTile, 16);
-    if (elect_one()) {
+    if (lead<kSolo>()) {
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
         const uint32_t off = ((kk >> 2) * kHalf + (kk & 3) * 32) / 16;
@@ -575,20 +654,24 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
       mma_commit(&bar.s_full);
       if (release) mma_commit(&bar.q_empty[qs]);
     }
-    __syncwarp();
+    wsync<kSolo>();
   } else if (op.kind == TWFA_OP_DP) {
     if (it == 0) mbar_wait(&bar.kv_full, t.icount & 1);
-    if (g > 0)  // dQ_(g-1) (over dP^T) has been read out
+    const bool o_need = !(TWFA_BWD_MEMO && st.o_seen == g + 1);
+    if (g > 0 && o_need)  // dQ_(g-1) (over dP^T) has been read out
       mbar_wait_all(&bar.o_full[os], (g / plan.v_depth) & 1, &bar.q_free, (g - 1) & 1);
-    else
+    else if (g > 0)
+      mbar_wait(&bar.q_free, (g - 1) & 1);
+    else if (o_need)
       mbar_wait(&bar.o_full[os], (g / plan.v_depth) & 1);
+    st.o_seen = g + 1;
     tc_fence_after();
     bwd_ready(st);
 #if TWFA_BWD_PROF
     g_prof_ready = clock64();
 #endif
     const uint32_t ad = sd_lo(c.v, 16), bd = sd_lo(c.o + os * kTile, 16);
-    if (elect_one()) {
+    if (lead<kSolo>()) {
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
         const uint32_t off = ((kk >> 2) * kHalf + (kk & 3) * 32) / 16;
@@ -597,16 +680,26 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
       mma_commit(&bar.dp_full);
       if (release) mma_commit(&bar.o_empty[os]);
     }
-    __syncwarp();
+    wsync<kSolo>();
   } else if (op.kind == TWFA_OP_DV || op.kind == TWFA_OP_DK) {
     const bool dv = op.kind == TWFA_OP_DV;
     // the accumulator is overwritten at iteration 0: the previous work
     // item's dK / dV must have been read out
     if (it == 0 && t.icount > 0) mbar_wait(&bar.acc_free, (t.icount - 1) & 1);
-    if (dv)
-      mbar_wait_all(&bar.p_full, g & 1, &bar.o_full[os], (g / plan.v_depth) & 1);
-    else
-      mbar_wait_all(&bar.ds_full, g & 1, &bar.q_full[qs], (g / plan.k_depth) & 1);
+    if (!TWFA_BWD_MEMO) {
+      if (dv)
+        mbar_wait_all(&bar.p_full, g & 1, &bar.o_full[os], (g / plan.v_depth) & 1);
+      else
+        mbar_wait_all(&bar.ds_full, g & 1, &bar.q_full[qs], (g / plan.k_depth) & 1);
+    } else if (dv) {
+      if (st.p_seen != g + 1) mbar_wait(&bar.p_full, g & 1);
+      if (st.o_seen != g + 1) mbar_wait(&bar.o_full[os], (g / plan.v_depth) & 1);
+      st.p_seen = st.o_seen = g + 1;
+    } else {
+      if (st.ds_seen != g + 1) bwd_wait_ds(st, plan, g);
+      if (st.q_seen != g + 1) mbar_wait(&bar.q_full[qs], (g / plan.k_depth) & 1);
+      st.q_seen = g + 1;
+    }
     tc_fence_after();
     bwd_ready(st);
 #if TWFA_BWD_PROF
@@ -615,15 +708,15 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
     // B = dO_i / Q_i as [K = query][N = d], MN-major
     const uint32_t bd = dv ? sd_lo(c.o + os * kTile, kHalf) : sd_lo(c.q + qs * kTile, kHalf);
     const uint32_t a_t = dv ? kColS : kColP, d_t = dv ? kColDV : kColDK;
-    if (elect_one()) {
+    if (lead<kSolo>()) {
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk)  // 16 queries per K-step: 8 packed bf16 columns of P^T / dS^T
         mma_ts(d_t, a_t + kk * 8, sdesc_join(bd + kk * 2048 / 16, kSdHi), kIdescKM, (it > 0 || kk > 0) ? 1u : 0u);
       if (release) mma_commit(dv ? &bar.o_empty[os] : &bar.q_empty[qs]);
     }
-    __syncwarp();
+    wsync<kSolo>();
   } else if (op.kind == TWFA_OP_DQ) {
-    mbar_wait(&bar.ds_full, g & 1);
+    if (!(TWFA_BWD_MEMO && st.ds_seen == g + 1)) bwd_wait_ds(st, plan, g);
     tc_fence_after();
     bwd_ready(st);
 #if TWFA_BWD_PROF
@@ -632,7 +725,7 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
     // A = dS as [M = query][K = key], MN-major (row = key in smem);
     // B = K as [K = key][N = d], MN-major
     const uint32_t ad = sd_lo(c.ds, kHalf), bd = sd_lo(c.k, kHalf);
-    if (elect_one()) {
+    if (lead<kSolo>()) {
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk)
         mma_ss(kColP, sdesc_join(ad + kk * 2048 / 16, kSdHi), sdesc_join(bd + kk * 2048 / 16, kSdHi), kIdescMM,
@@ -640,17 +733,22 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
       mma_commit(&bar.dq_full);
       if (op.flags & TWFA_OPF_RELEASE) mma_commit(&bar.ds_free);  // dQ staged in the Q slot: dS is free
     }
-    __syncwarp();
+    wsync<kSolo>();
   }
 }
 
 template <int kRole>
 __device__ __forceinline__ void bwd_run(const BwdCtx& c, const TwfaDevicePlan& plan, const FaBwdArgs& a) {
   BwdBarriers& bar = g_bb;
-  const int plen = plan.prog_len[c.warp];
-  const bool is_load = c.warp == static_cast<uint32_t>(plan.load_warp);
+  // TWFA_BWD_LOAD_WARP >= 0: that warp runs the load warp's streamed loads
+  // (and the K / V item loads), the load warp keeps only its other ops
+  const bool loads_only = TWFA_BWD_LOAD_WARP >= 0 && c.warp == static_cast<uint32_t>(TWFA_BWD_LOAD_WARP);
+  const bool skip_loads = TWFA_BWD_LOAD_WARP >= 0 && c.warp == static_cast<uint32_t>(plan.load_warp);
+  const int src = loads_only ? plan.load_warp : static_cast<int>(c.warp);
+  const int plen = plan.prog_len[src];
+  const bool is_load = TWFA_BWD_LOAD_WARP >= 0 ? loads_only : c.warp == static_cast<uint32_t>(plan.load_warp);
   const bool is_mma = c.warp == static_cast<uint32_t>(plan.mma_warp);
-  BwdState st{0, 0, -1, -1, 0, nullptr};
+  BwdState st{0, 0, -1, -1, 0, nullptr, 0, 0, 0, 0};
   uint32_t gbase = 0, icount = 0;
   for (int i = 0;; ++i, ++icount) {
     int work;
@@ -663,33 +761,38 @@ __device__ __forceinline__ void bwd_run(const BwdCtx& c, const TwfaDevicePlan& p
       if (work >= c.num_work) break;
     }
     const BwdItem t = bwd_item(c, a, work, gbase, icount);
-    if constexpr (kRole == kLight) {
+    if constexpr (is_light(kRole)) {
       if (is_load) {  // K and V of the work item
         mbar_wait(&bar.kv_empty, (icount & 1) ^ 1);
-        if (elect_one()) {
+        if (lead<kRole == kLightSolo>()) {
           mbar_arrive_expect_tx(&bar.kv_full, 2 * kTile);
           tma_load_3d(c.k, &a.tm_k, &bar.kv_full, 0, t.kv0, t.bh, c.pol);
           tma_load_3d(c.k + kHalf, &a.tm_k, &bar.kv_full, 64, t.kv0, t.bh, c.pol);
           tma_load_3d(c.v, &a.tm_v, &bar.kv_full, 0, t.kv0, t.bh, c.pol);
           tma_load_3d(c.v + kHalf, &a.tm_v, &bar.kv_full, 64, t.kv0, t.bh, c.pol);
         }
-        __syncwarp();
+        wsync<kRole == kLightSolo>();
       }
     }
     st.q_next = st.o_next = 0;
     st.q_target = st.o_target = -1;
     const int trips = t.N + plan.max_stage;
     for (int rr = -1; rr < trips; ++rr)
-      for (int j = 0; j < plen; ++j) bwd_exec<kRole>(plan.ops[plan.prog[c.warp][j]], rr, c, t, st, plan, a);
-    if constexpr (kRole == kLight) {
+      for (int j = 0; j < plen; ++j) {
+        const TwfaPlanOp& op = plan.ops[plan.prog[src][j]];
+        const bool ld = op.kind == TWFA_OP_LDQ || op.kind == TWFA_OP_LDO;
+        if ((loads_only && !ld) || (skip_loads && ld)) continue;
+        bwd_exec<kRole>(op, rr, c, t, st, plan, a);
+      }
+    if constexpr (is_light(kRole)) {
       if (is_mma) {  // every MMA of the item issued: dK, dV final; K, V free
-        if (elect_one()) {
+        if (lead<kRole == kLightSolo>()) {
           mma_commit(&bar.acc_full);
           mma_commit(&bar.kv_empty);
         }
-        __syncwarp();
+        wsync<kRole == kLightSolo>();
       }
-    } else if constexpr (kRole == kReduce) {
+    } else if constexpr (kRole == kReduce || kRole == kReduceFull) {
       kv_epilogue(c, a, t);
     }
     gbase += static_cast<uint32_t>(t.N);
@@ -765,11 +868,23 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
     setmaxnreg_inc<144>();
     bwd_run<kDs>(c, plan, a);
   } else if (rd) {
-    setmaxnreg_dec<128>();
-    bwd_run<kReduce>(c, plan, a);
+    // with EXB and DS fused on one warpgroup the register file has room for
+    // the whole dQ row in RD (200 + 176 + 8 x 64 per thread-warp class)
+    if (TWFA_BWD_RD_FULL && plan.sm_warp[0] == plan.sm_warp[1]) {
+      setmaxnreg_inc<176>();
+      bwd_run<kReduceFull>(c, plan, a);
+    } else {
+      setmaxnreg_dec<128>();
+      bwd_run<kReduce>(c, plan, a);
+    }
   } else {
     setmaxnreg_dec<64>();
-    bwd_run<kLight>(c, plan, a);
+    if (TWFA_BWD_SOLO) {
+      if (elect_one()) bwd_run<kLightSolo>(c, plan, a);
+      __syncwarp();
+    } else {
+      bwd_run<kLight>(c, plan, a);
+    }
   }
   if (c.lane == 0) bulk_wait_all();
   tc_fence_before();

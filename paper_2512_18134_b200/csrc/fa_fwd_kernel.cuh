@@ -553,7 +553,7 @@ struct Maps {
 // ---------------------------------------------------------------- op bodies
 // One op of the trip program on this warp, trip r. Shared by both kernels:
 // with a compile-time `op` and `rg` every branch below folds.
-template <int KV, bool kHeavy, bool kTrace, bool P>
+template <int KV, bool kHeavy, bool kTrace, bool P, bool kSolo = false>
 __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const FaCtx& c, const WorkTile& t,
                                         WarpState& st, const Rings rg, const Maps& tm, const FaArgs& args) {
   FaBarriers& bar = g_sh.bar;
@@ -588,7 +588,7 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
         const CUtensorMap* map = is_k ? tm.k : tm.v;
         if (!(TWFA_WHATIF == 6 && g >= 8u)) wait_<P>(empty, ph ^ 1);
         trace_mark<kTrace>(tr, 4);
-        if (elect_one()) {
+        if (lead<kSolo>()) {
           if constexpr (P) {
             // this CTA's half: K keys 64r.. (both head-dim halves), V head
             // dims 64r.. (all keys); both halves land on the leader's barrier
@@ -608,7 +608,7 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
             tma_load_3d(dst + G::half, map, full, 64, key0, bh, c.pol_kv);
           }
         }
-        __syncwarp();
+        wsync<kSolo>();
         trace_mark<kTrace>(tr, 5);
       }
     }
@@ -646,7 +646,7 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
     // K rows 64.. (8 SW128 atoms)
     const uint32_t kd = sdesc_lo(smem_u32(c.k_smem + s * G::tile) + (a ? 0u : 64u * 128u), 16);
     const uint32_t d_s = tmem + k * 128 + (a ? 0u : 64u);
-    if (elect_one()) {
+    if (lead<kSolo>()) {
 #pragma unroll
       for (int kk = 0; kk < kHeadDim / 16; ++kk)
         mma_ss(d_s, sdesc_join(qd + ((kk >> 2) * kHalfBytes + (kk & 3) * 32) / 16, kSdescHi),
@@ -655,7 +655,7 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
       mma_commit(&bar.k_empty[s]);
       if (it == N - 1) mma_commit(&bar.q_empty[k]);
     }
-    __syncwarp();
+    wsync<kSolo>();
   } else if (op.kind == TWFA_OP_S) {
     // MMA issue: every lane waits and computes the (warp-uniform)
     // descriptors, so they live in uniform registers; one elected lane
@@ -675,7 +675,7 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
     const uint32_t d_s = tmem + k * 128 + b * KV;
     if constexpr (P) {
       // M = 256 (Q_k of both CTAs), N = 128 keys (64 from each CTA's half)
-      if (elect_one()) {
+      if (lead<kSolo>()) {
 #pragma unroll
         for (int kk = 0; kk < kHeadDim / 16; ++kk)
           mma_ss_pair(d_s, sdesc_join(qd + ((kk >> 2) * kHalfBytes + (kk & 3) * 32) / 16, kSdescHi),
@@ -684,8 +684,8 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
         commit_<P>(&bar.k_empty[s]);
         if (it == N - 1) commit_<P>(&bar.q_empty[k]);
       }
-      __syncwarp();
-    } else if (elect_one()) {
+      wsync<kSolo>();
+    } else if (lead<kSolo>()) {
       if (TWFA_S_HALVES && KV == 128) {
         // keys 0-63, committed on their own, then keys 64-127: the softmax
         // starts on the first half while the second is computed
@@ -708,7 +708,7 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
       mma_commit(&bar.k_empty[s]);
       if (it == N - 1) mma_commit(&bar.q_empty[k]);
     }
-    __syncwarp();
+    wsync<kSolo>();
   } else if (op.kind == TWFA_OP_PV) {
     const uint32_t s = g % rg.vd;
     // P_k arrives in two halves (keys 0-63, 64-127): the first four
@@ -747,7 +747,7 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
         wait_<P>(&bar.p_part[k][b][j], pb);
         tc_fence_after();
       }
-      if (elect_one()) {
+      if (lead<kSolo>()) {
 #pragma unroll
         for (int kk = j * kSteps; kk < (j + 1) * kSteps; ++kk) {  // V is MN-major: 16 keys = 16 rows of 128 B
           if constexpr (P)  // M = 256 (P_k of both CTAs), N = 128 head dims (64 from each CTA's half)
@@ -761,7 +761,7 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
           commit_<P>(&bar.v_empty[s]);
         }
       }
-      __syncwarp();
+      wsync<kSolo>();
     }
   } else if (op.kind == TWFA_OP_CR) {
     const uint32_t sb = g & 1;
@@ -910,14 +910,14 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
 
 // Q sub-tiles of a new work tile (TMA warp, before its trip loop). With CTA
 // pairs each CTA loads its own sub-tile rows onto the leader's barrier.
-template <int KV, bool P>
+template <int KV, bool P, bool kSolo = false>
 __device__ __forceinline__ void load_q(const FaCtx& c, const WorkTile& t, int tiles, const Maps& tm) {
   FaBarriers& bar = g_sh.bar;
   for (int k = 0; k < tiles; ++k) {
     wait_<P>(&bar.q_empty[k], (t.tcount & 1) ^ 1);
     uint8_t* dst = c.q_smem + k * kTileBytes;
     const int row = sub_tile_row<KV, P>(c, t, k);
-    if (elect_one()) {
+    if (lead<kSolo>()) {
       if constexpr (P) {
         if (c.rank == 0) mbar_arrive_expect_tx(&bar.q_full[k], 2 * kTileBytes);
         tma_load_3d_pair(dst, tm.q, &bar.q_full[k], 0, row, t.bh, c.pol_q);
@@ -928,7 +928,7 @@ __device__ __forceinline__ void load_q(const FaCtx& c, const WorkTile& t, int ti
         tma_load_3d(dst + kHalfBytes, tm.q, &bar.q_full[k], 64, row, t.bh, c.pol_q);
       }
     }
-    __syncwarp();
+    wsync<kSolo>();
   }
 }
 
@@ -1024,10 +1024,13 @@ __device__ __forceinline__ int work_of(const FaCtx& c, const FaArgs& args, int i
 
 // cross-tile prefetch (Q on an idle warp, the next tile's first K / V
 // iterations on the TMA warp); 0 = each tile starts from empty rings
+#ifndef TWFA_SOLO
+#define TWFA_SOLO 0  // measured: one-lane TMA / MMA warp -9 % per clock (pair), -4 % (one CTA)
+#endif
 #ifndef TWFA_XTILE
 #define TWFA_XTILE 1
 #endif
-template <int KV, bool P, class Trip>
+template <int KV, bool P, bool kSolo = false, class Trip>
 __device__ __forceinline__ void work_loop(const FaCtx& c, const FaArgs& args, const Maps& tm, int tiles, int max_stage,
                                           bool is_load_warp, bool is_q_warp, const int* cr_warp, WarpState& st,
                                           Trip&& trip) {
@@ -1039,12 +1042,12 @@ __device__ __forceinline__ void work_loop(const FaCtx& c, const FaArgs& args, co
     if (work >= c.num_work) break;
     const WorkTile t = work_tile<KV, P>(c, args, work, gbase, tcount);
     if (TWFA_XTILE && is_q_warp) {  // Q of every tile, as soon as the previous tile's last S_k released it
-      load_q<KV, P>(c, t, tiles, tm);
+      load_q<KV, P, kSolo>(c, t, tiles, tm);
       gbase += static_cast<uint32_t>(t.N);
       continue;
     }
     if (is_load_warp) {
-      if (!TWFA_XTILE || !(c.q_warp >= 0)) load_q<KV, P>(c, t, tiles, tm);
+      if (!TWFA_XTILE || !(c.q_warp >= 0)) load_q<KV, P, kSolo>(c, t, tiles, tm);
       const int nwork = work_of(c, args, round + 1);
       st.next_N = 0;
       if (TWFA_XTILE && nwork < c.num_work) {
@@ -1264,14 +1267,33 @@ __device__ __forceinline__ void fill_progs(int w, int j, std::integer_sequence<i
   ((w == W ? fill_warp_prog<I, W>(j, std::make_integer_sequence<int, TWFA_PLAN(I).prog_len[W]>{}) : void()), ...);
 }
 
-template <int I, int W, bool kTrace, bool P, int... J>
+template <int I, int W, bool kTrace, bool P, bool kSolo, int... J>
 __device__ __forceinline__ void spec_trip(int r, const FaCtx& c, const WorkTile& t, WarpState& st, const Maps& tm,
                                           const FaArgs& args, std::integer_sequence<int, J...>) {
   constexpr bool kHeavy = (TWFA_PLAN(I).heavy_wg_mask >> (W / 4)) & 1;
   constexpr Rings rg{TWFA_PLAN(I).k_depth,    TWFA_PLAN(I).v_depth,    TWFA_PLAN(I).k_prefetch,
                      TWFA_PLAN(I).v_prefetch, TWFA_PLAN(I).ex_ring_len, TWFA_PLAN(I).ex_ring[0],
                      TWFA_PLAN(I).ex_ring[1], TWFA_PLAN(I).s_split};
-  (exec_op<TWFA_PLAN(I).kv_tile, kHeavy, kTrace, P>(spec_op<I, W, J>(), r, c, t, st, rg, tm, args), ...);
+  (exec_op<TWFA_PLAN(I).kv_tile, kHeavy, kTrace, P, kSolo>(spec_op<I, W, J>(), r, c, t, st, rg, tm, args), ...);
+}
+
+// A light role runs on one elected lane (TWFA_SOLO) when its program holds
+// only TMA loads and tensor-core issues: no correction, no epilogue, not the
+// Q warp (lead / wsync in sm100.cuh)
+template <int I, int W>
+__host__ __device__ constexpr bool solo_role() {
+  if (!TWFA_SOLO || ((TWFA_PLAN(I).heavy_wg_mask >> (W / 4)) & 1) || W == TWFA_PLAN(I).q_warp ||
+      TWFA_PLAN(I).prog_len[W] == 0)
+    return false;
+  for (int k = 0; k < TWFA_PLAN(I).num_tiles; ++k)
+    if ((W & ~3) == TWFA_PLAN(I).cr_warp[k]) return false;
+  for (int j = 0; j < TWFA_PLAN(I).prog_len[W]; ++j) {
+    const int kind = TWFA_PLAN(I).ops[TWFA_PLAN(I).prog[W][j]].kind;
+    if (kind != TWFA_OP_LDK && kind != TWFA_OP_LDV && kind != TWFA_OP_S && kind != TWFA_OP_PV &&
+        kind != TWFA_OP_SA && kind != TWFA_OP_SB)
+      return false;
+  }
+  return true;
 }
 
 template <int I, int W, bool kTrace, bool P>
@@ -1280,13 +1302,22 @@ __device__ __forceinline__ void run_spec(const FaCtx& c, const Maps& tm, const F
   constexpr int plen = TWFA_PLAN(I).prog_len[W];
   constexpr bool kLoad = !kHeavy && W == TWFA_PLAN(I).load_warp;
   constexpr int cr_warp[TWFA_MAX_TILES] = {TWFA_PLAN(I).cr_warp[0], TWFA_PLAN(I).cr_warp[1]};
+  constexpr bool kSolo = solo_role<I, W>();
   WarpState st;
   st.trace_n = 0;
-  work_loop<TWFA_PLAN(I).kv_tile, P>(c, args, tm, TWFA_PLAN(I).num_tiles, TWFA_PLAN(I).max_stage, kLoad,
-                                  !kHeavy && static_cast<int>(c.warp) == c.q_warp, cr_warp, st,
-            [&](int r, const WorkTile& t) {
-              spec_trip<I, W, kTrace, P>(r, c, t, st, tm, args, std::make_integer_sequence<int, plen>{});
-            });
+  auto body = [&] {
+    work_loop<TWFA_PLAN(I).kv_tile, P, kSolo>(c, args, tm, TWFA_PLAN(I).num_tiles, TWFA_PLAN(I).max_stage, kLoad,
+                                             !kHeavy && static_cast<int>(c.warp) == c.q_warp, cr_warp, st,
+              [&](int r, const WorkTile& t) {
+                spec_trip<I, W, kTrace, P, kSolo>(r, c, t, st, tm, args, std::make_integer_sequence<int, plen>{});
+              });
+  };
+  if constexpr (kSolo) {
+    if (elect_one()) body();
+    __syncwarp();
+  } else {
+    body();
+  }
 }
 
 // Light roles (TMA, MMA issue, correction) run their specialized trip

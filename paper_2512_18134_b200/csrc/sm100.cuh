@@ -30,6 +30,20 @@ TWFA_DEV bool elect_one() {
       : "=r"(pred));
   return pred != 0;
 }
+// Issue helpers of the TMA / MMA roles: a warp elects one lane per op and
+// re-converges (kSolo = false), or the role already runs on one elected lane
+// for its whole trip loop (kSolo = true: no per-op elect / __syncwarp, which
+// measured 65-72 % -> 89-96 % tensor-core busy on back-to-back 8-MMA ops of
+// 64 clk, tools/calib/ubench_mmaloop.cu).
+template <bool kSolo>
+__device__ __forceinline__ bool lead() {
+  if constexpr (kSolo) return true;
+  else return elect_one();
+}
+template <bool kSolo>
+__device__ __forceinline__ void wsync() {
+  if constexpr (!kSolo) __syncwarp();
+}
 
 // ---------------------------------------------------------------- mbarrier
 TWFA_DEV void mbar_init(uint64_t* bar, uint32_t count) {
