@@ -155,3 +155,13 @@ def test_two_subtile_schedule_matches_oracle(twfa, pp_plans, B, H, S, causal):
     work items than SMs (accumulator hand-off across items)."""
     assert pp_plans[1].describe()["num_tiles"] == 2
     _check(twfa, pp_plans, B, H, S, causal, 40)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_shapes_against_oracle(twfa, plans, seed):
+    """Seeded fuzz over batch, heads, any sequence length up to 700 and
+    causal / non-causal, each against the fp64 oracle."""
+    rng = np.random.default_rng(3000 + seed)
+    B, H = int(rng.integers(1, 3)), int(rng.integers(1, 3))
+    S = int(rng.integers(1, 701))
+    _check(twfa, plans, B, H, S, bool(rng.random() < 0.5), 4000 + seed)
