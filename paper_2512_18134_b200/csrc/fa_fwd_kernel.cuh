@@ -167,6 +167,7 @@ struct __align__(8) FaBarriers {
 
 struct FaShared {
   float stats[TWFA_MAX_TILES][2][kBlockQ];  // MX -> CR rescale factors, double-buffered
+  float mrow[TWFA_MAX_TILES][2][kBlockQ];   // MX -> CR running max (TWFA_CR_EXP; NaN: no offload)
   float lbuf[TWFA_MAX_TILES][2][kBlockQ];   // EX -> epilogue: running max, row sum
   // per-warp trip programs (interpreted roles): one shared load per op
   TwfaPlanOp prog[TWFA_MAX_WARPS][TWFA_MAX_NODES];
@@ -355,13 +356,25 @@ __device__ __forceinline__ float exp_store_row(const uint32_t (&s)[N], uint32_t 
 // TWFA_LATE_SUM: the row sum of chunks 1.. is taken after the last P part is
 // released (the fp32 P overwrites the consumed S registers), so the FADD2s
 // leave the MUFU-bound path to PV
+// The correction warps compute the last 32-key chunk of every row's P in
+// the speculative iterations (TWFA_CR_EXP): exp2 by the FMA-pipe polynomial
+// on warps that are otherwise idle with the rescale threshold, a quarter of
+// the exponentials off the softmax warps' MUFU path. The last P part then
+// waits for the softmax and the correction warps; the correction warps keep
+// their part of the row sum and add it in the epilogue.
+#ifndef TWFA_CR_EXP
+#define TWFA_CR_EXP 0  // measured: -3.4 % per clock (pair, C3), -3 % (C4), -1 % (one CTA)
+#endif
+template <int KV>
+constexpr bool kCrExp = TWFA_CR_EXP && KV == 128;
 #ifndef TWFA_CHUNK_PHASED
 #define TWFA_CHUNK_PHASED 0  // measured: all FFMA2 arguments of a chunk before its MUFU ops, -0.6 % (C3, C4)
 #endif
 #ifndef TWFA_LATE_SUM
 #define TWFA_LATE_SUM 1  // measured: +0.9 % (pair) / +1.4 % (one CTA) per clock under the power cap, +4 % burst
 #endif
-template <int N, bool P, class Handoff, class WaitRest>
+static_assert(!TWFA_CR_EXP || TWFA_LATE_SUM, "TWFA_CR_EXP releases the last P part with the late row sum");
+template <int N, bool P, bool kOff, class Handoff, class WaitRest>
 __device__ __forceinline__ float mx_ex_spec(uint32_t (&s)[N], uint32_t taddr, float sl, float& m_io, float& alpha,
                                             uint64_t* part_bar, Handoff&& handoff, WaitRest&& wait_rest,
                                             uint32_t* trm = nullptr) {
@@ -430,8 +443,10 @@ __device__ __forceinline__ float mx_ex_spec(uint32_t (&s)[N], uint32_t taddr, fl
   handoff(alpha);
   if (TWFA_TRACE_SUB && trm != nullptr) trm[6] = static_cast<uint32_t>(clock64());
   tmem_st<kRegs>(taddr, pk0);
+  // kOff: the last chunk is the correction warps' (TWFA_CR_EXP)
+  constexpr int kChunks = N / kKeys - (kOff ? 1 : 0);
 #pragma unroll
-  for (int c = 1; c < N / kKeys; ++c) {
+  for (int c = 1; c < kChunks; ++c) {
     uint32_t pk[kRegs];
     chunk(c, m_new, pk);
     if ((c * kKeys) % kPartKeys == 0) {
@@ -445,9 +460,12 @@ __device__ __forceinline__ float mx_ex_spec(uint32_t (&s)[N], uint32_t taddr, fl
   tmem_st_wait();
   if constexpr (TWFA_LATE_SUM) {
     tc_fence_before();
-    arrive_mma_<P>(&part_bar[kParts - 1]);  // the last part, before the row sum
+    // the parts from the one holding this warp's last chunk to the last,
+    // before the row sum
 #pragma unroll
-    for (int e = kKeys; e < N; e += 4) {
+    for (int j = (kChunks * kKeys - 1) / kPartKeys; j < kParts; ++j) arrive_mma_<P>(&part_bar[j]);
+#pragma unroll
+    for (int e = kKeys; e < kChunks * kKeys; e += 4) {
       acc[0] = fadd2(acc[0], make_float2(__uint_as_float(s[e]), __uint_as_float(s[e + 1])));
       acc[1] = fadd2(acc[1], make_float2(__uint_as_float(s[e + 2]), __uint_as_float(s[e + 3])));
     }
@@ -516,6 +534,7 @@ __device__ __forceinline__ int valid_keys(const FaArgs& a, int row, int key0) {
 // running per-warp state
 struct WarpState {
   float m_run[TWFA_MAX_TILES], l_run[TWFA_MAX_TILES], alpha[TWFA_MAX_TILES];
+  float l3[TWFA_MAX_TILES];  // correction warps: row-sum share of the offloaded chunk (TWFA_CR_EXP)
   int k_next, v_next;  // next K / V iteration to load (TMA warp); may run into the next tile
   // MMA warp: the last global iteration whose K (V) tile this warp already
   // saw land; a second tensor-core op on the same tile skips the wait
@@ -767,7 +786,38 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
     const uint32_t sb = g & 1;
     mbar_wait(&bar.st_full[k][sb], (g >> 1) & 1);
     const float alpha = g_sh.stats[k][sb][c.quad * 32 + lane];
+    const float m_row = kCrExp<KV> ? g_sh.mrow[k][sb][c.quad * 32 + lane] : 0.f;
     if (TWFA_ST_EMPTY) warp_arrive(&bar.st_empty[k][sb]);
+    if constexpr (kCrExp<KV>) {
+      // the last 32 keys of the row's P when MX_k took the speculative path
+      // (m_row finite for the whole warp; split-S plans never offload)
+      float l3 = it == 0 ? 0.f : rd(st.l3, k) * alpha;
+      if (!rg.split && __all_sync(0xffffffffu, m_row == m_row)) {
+        trace_mark<kTrace>(tr, 4);
+        const uint32_t s_addr = tmem + c.lane_off + k * 128 + b * KV;
+        const float2 sl2 = make_float2(c.scale_log2, c.scale_log2), nm2 = make_float2(-m_row, -m_row);
+        float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint32_t v[16], pk[8];
+          tmem_ld16(s_addr + KV - 32 + h * 16, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; i += 2) {
+            const float2 x = ffma2(make_float2(__uint_as_float(v[i]), __uint_as_float(v[i + 1])), sl2, nm2);
+            const float2 p = poly_exp2x2(x);
+            acc = fadd2(acc, p);
+            pk[i >> 1] = pack_bf16(p.x, p.y);
+          }
+          tmem_st8(s_addr + (KV - 32) / 2 + h * 8, pk);
+        }
+        tmem_st_wait();
+        l3 += acc.x + acc.y;
+      }
+      wr(st.l3, k, l3);
+      tc_fence_before();
+      arrive_mma_<P>(&bar.p_part[k][b][p_parts<P>() - 1]);
+    }
     // with the rescale threshold most iterations keep the max: then O is
     // not touched and the correction only forwards the handoff
     if (it > 0 && !__all_sync(0xffffffffu, alpha == 1.f)) {
@@ -819,9 +869,10 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
           if (spec) {
             float m = m_old, alpha = 1.f;
             const uint32_t sb = g & 1;
-            const float sum = mx_ex_spec<KV, P>(srow, taddr, c.scale_log2, m, alpha, bar.p_part[k][b], [&](float al) {
+            const float sum = mx_ex_spec<KV, P, kCrExp<KV>>(srow, taddr, c.scale_log2, m, alpha, bar.p_part[k][b], [&](float al) {
               if (TWFA_ST_EMPTY) mbar_wait(&bar.st_empty[k][sb], ((g >> 1) & 1) ^ 1);
               g_sh.stats[k][sb][c.quad * 32 + lane] = al;
+              if constexpr (kCrExp<KV>) g_sh.mrow[k][sb][c.quad * 32 + lane] = m;
               warp_arrive(&bar.st_full[k][sb]);
             }, [&] {
               if (TWFA_S_HALVES) {
@@ -875,6 +926,7 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
         const uint32_t sb = g & 1;
         if (TWFA_ST_EMPTY) mbar_wait(&bar.st_empty[k][sb], ((g >> 1) & 1) ^ 1);
         g_sh.stats[k][sb][c.quad * 32 + lane] = rd(st.alpha, k);
+        if constexpr (kCrExp<KV>) g_sh.mrow[k][sb][c.quad * 32 + lane] = __int_as_float(0x7fffffff);  // NaN: all chunks here
         warp_arrive(&bar.st_full[k][sb]);
         trace_mark<kTrace>(tr, 5);
         if (!(op.flags & TWFA_OPF_FUSE_NEXT)) return;
@@ -935,14 +987,15 @@ __device__ __forceinline__ void load_q(const FaCtx& c, const WorkTile& t, int ti
 // Epilogue of sub-tile k on its correction warpgroup: O / l -> bf16 -> global,
 // LSE (the accumulator is final after the last PV_k).
 template <int KV, bool P>
-__device__ __forceinline__ void epilogue(const FaCtx& c, const WorkTile& t, int k, const FaArgs& args) {
+__device__ __forceinline__ void epilogue(const FaCtx& c, const WorkTile& t, int k, const FaArgs& args,
+                                         float l_cr = 0.f) {
   FaBarriers& bar = g_sh.bar;
   const uint32_t lane = c.lane;
   const uint32_t g_last = t.gbase + static_cast<uint32_t>(t.N - 1);
   wait_<P>(&bar.o_done[k][g_last % Kv<KV>::depth], (g_last / Kv<KV>::depth) & 1);
   mbar_wait(&bar.l_full[k], t.tcount & 1);
   const float m = g_sh.lbuf[k][0][c.quad * 32 + lane];
-  const float l = g_sh.lbuf[k][1][c.quad * 32 + lane];
+  const float l = g_sh.lbuf[k][1][c.quad * 32 + lane] + l_cr;  // + the correction warps' share (TWFA_CR_EXP)
   warp_arrive(&bar.l_empty[k]);
   tc_fence_after();
   const int row0 = sub_tile_row<KV, P>(c, t, k);
@@ -1068,7 +1121,7 @@ __device__ __forceinline__ void work_loop(const FaCtx& c, const FaArgs& args, co
     const int trips = t.N + max_stage;
     for (int r = -1; r < trips; ++r) trip(r, t);
     for (int k = 0; k < tiles; ++k)
-      if (static_cast<int>(c.warp & ~3u) == cr_warp[k]) epilogue<KV, P>(c, t, k, args);
+      if (static_cast<int>(c.warp & ~3u) == cr_warp[k]) epilogue<KV, P>(c, t, k, args, kCrExp<KV> ? rd(st.l3, k) : 0.f);
     // iterations of the next tile already in flight keep their count
     st.k_next = max(0, st.k_next - t.N);
     st.v_next = max(0, st.v_next - t.N);
@@ -1099,7 +1152,12 @@ __device__ __forceinline__ FaCtx fa_setup(int tiles, int kd, int vd, int load_wa
       for (int b = 0; b < 2; ++b) {
         mbar_init(&bar.s_full[k][b], 1);
         // warp arrivals of a warpgroup (of both CTAs' warpgroups: the leader's copy)
-        for (int j = 0; j < kPParts; ++j) mbar_init(&bar.p_part[k][b][j], 4 * Kv<KV, P>::rows);
+        // the last part of a 128-key tile also waits for the correction
+        // warps' chunk (TWFA_CR_EXP, every iteration: they arrive without
+        // work when MX_k did all chunks)
+        for (int j = 0; j < kPParts; ++j)
+          mbar_init(&bar.p_part[k][b][j],
+                    4 * Kv<KV, P>::rows * (kCrExp<KV> && !split && j == p_parts<P>() - 1 ? 2 : 1));
         mbar_init(&bar.o_ready[k][b], 4 * Kv<KV, P>::rows);
         mbar_init(&bar.o_done[k][b], 1);
       }
