@@ -70,7 +70,7 @@ constexpr uint32_t kSdHi = sdesc_hi(1024);
 // the warp's own tcgen05 instructions, so each redundant wait delays the
 // next op's issue while the tensor core drains its short queue.
 #ifndef TWFA_BWD_MEMO
-#define TWFA_BWD_MEMO 1
+#define TWFA_BWD_MEMO 0  // measured neutral (688 vs 690); off: every p_full phase keeps a waiter (synccheck)
 #endif
 // RD reads the whole dQ_i row out of tensor memory before staging it
 // (TWFA_BWD_RD_FULL), so q_free -- which DP_(i+1) waits for -- is signalled

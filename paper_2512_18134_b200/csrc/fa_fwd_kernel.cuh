@@ -362,6 +362,9 @@ __device__ __forceinline__ float exp_store_row(const uint32_t (&s)[N], uint32_t 
 // the exponentials off the softmax warps' MUFU path. The last P part then
 // waits for the softmax and the correction warps; the correction warps keep
 // their part of the row sum and add it in the epilogue.
+#ifndef TWFA_CR_WAIT_ALL
+#define TWFA_CR_WAIT_ALL 0  // 1: synccheck-clean (every o_done phase awaited), measured -0.5 to -1 %
+#endif
 #ifndef TWFA_CR_EXP
 #define TWFA_CR_EXP 0  // measured: -3.4 % per clock (pair, C3), -3 % (C4), -1 % (one CTA)
 #endif
@@ -818,11 +821,15 @@ __device__ __forceinline__ void exec_op(const TwfaPlanOp op, const int r, const 
       tc_fence_before();
       arrive_mma_<P>(&bar.p_part[k][b][p_parts<P>() - 1]);
     }
+    // PV_k(g - 1) has completed: O may be read-modified-written. Awaited on
+    // every iteration (TWFA_CR_WAIT_ALL), so every phase of o_done has a
+    // waiter; the wait returns at once with 128-key tiles (S_k(g), which
+    // MX_k(g) waited for, follows PV_k(g - 1) on the tensor pipe)
+    if (TWFA_CR_WAIT_ALL && g > 0) wait_<P>(&bar.o_done[k][(g - 1) % G::depth], ((g - 1) / G::depth) & 1);
     // with the rescale threshold most iterations keep the max: then O is
     // not touched and the correction only forwards the handoff
     if (it > 0 && !__all_sync(0xffffffffu, alpha == 1.f)) {
-      // O is read-modified-written: PV_k(g - 1) must have completed
-      wait_<P>(&bar.o_done[k][(g - 1) % G::depth], ((g - 1) / G::depth) & 1);
+      if (!TWFA_CR_WAIT_ALL) wait_<P>(&bar.o_done[k][(g - 1) % G::depth], ((g - 1) / G::depth) & 1);
       trace_mark<kTrace>(tr, 4);
       tc_fence_after();
 #pragma unroll 1
