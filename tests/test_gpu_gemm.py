@@ -61,3 +61,20 @@ def test_gemm_rejects_unaligned_shapes(twfa, plan, M, N, K):
     b = torch.zeros(N, K, device="cuda", dtype=torch.bfloat16)
     with pytest.raises(ValueError):
         twfa.gemm(plan, a, b)
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_gemm_random_shapes(twfa, plan, seed):
+    """Seeded fuzz over the aligned shape space (M, N multiples of 256, K of
+    64) against torch's fp32 product of the same bf16 inputs: tile counts
+    below, at and above the number of CTA pairs, tall and wide grids."""
+    rng = np.random.default_rng(500 + seed)
+    M, N = 256 * int(rng.integers(1, 17)), 256 * int(rng.integers(1, 17))
+    K = 64 * int(rng.integers(1, 49))
+    g = torch.Generator(device="cuda").manual_seed(600 + seed)
+    a = (torch.randn(M, K, device="cuda", generator=g) / K ** 0.5).to(torch.bfloat16)
+    b = torch.randn(N, K, device="cuda", generator=g).to(torch.bfloat16)
+    c = twfa.gemm(plan, a, b)
+    ref = a.float() @ b.float().t()
+    err = (c.float() - ref).abs().max().item()
+    assert err <= 1e-2 * max(1.0, ref.abs().max().item()), (M, N, K, err)
