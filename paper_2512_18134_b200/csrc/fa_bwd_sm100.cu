@@ -78,6 +78,9 @@ constexpr uint32_t kSdHi = sdesc_hi(1024);
 #ifndef TWFA_BWD_RD_FULL
 #define TWFA_BWD_RD_FULL 1
 #endif
+#ifndef TWFA_BWD_FIXED
+#define TWFA_BWD_FIXED 1
+#endif
 #ifndef TWFA_BWD_SOLO
 #define TWFA_BWD_SOLO 0  // measured: 680 vs 693 TF/s (C3); with the loads on warp 14 699
 #endif
@@ -552,13 +555,16 @@ __device__ __forceinline__ void bwd_wait_ds(BwdState& st, const TwfaDevicePlan& 
 }
 
 // One op of the trip program on this warp, trip r.
-template <int kRole>
+template <int kRole, int kKind = -1>
 __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const BwdCtx& c, const BwdItem& t,
                                          BwdState& st, const TwfaDevicePlan& plan, const FaBwdArgs& a) {
   BwdBarriers& bar = g_bb;
-  if (op.kind == TWFA_OP_LDQ || op.kind == TWFA_OP_LDO) {
+  // kKind >= 0: a call site that knows the op's kind at compile time (the
+  // TMA / MMA warp's fixed program, TWFA_BWD_FIXED): every other branch folds
+  const int kind = kKind >= 0 ? kKind : static_cast<int>(op.kind);
+  if (kind == TWFA_OP_LDQ || kind == TWFA_OP_LDO) {
     if constexpr (is_light(kRole)) {
-      const bool is_q = op.kind == TWFA_OP_LDQ;
+      const bool is_q = kind == TWFA_OP_LDQ;
       const int target = min(t.N - 1, r - static_cast<int>(op.stage) + (is_q ? plan.k_prefetch : plan.v_prefetch));
       (is_q ? st.q_target : st.o_target) = target;
       const int before = is_q ? st.q_next : st.o_next;
@@ -605,10 +611,10 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
     }
   } out_{prof, op.kind, it, clock64()};
 #endif
-  if (op.kind == TWFA_OP_EXB || op.kind == TWFA_OP_DS) {
+  if (kind == TWFA_OP_EXB || kind == TWFA_OP_DS) {
     if constexpr (kRole == kExbDs || kRole == kExb || kRole == kDs) {
       uint32_t p[kT];
-      if (op.kind == TWFA_OP_EXB) {
+      if (kind == TWFA_OP_EXB) {
         exb_part(c, a, t, it, g, p, st);
         if constexpr (kRole == kExbDs) ds_part<true>(c, a, t, it, g, p);  // fused (lowering guarantees)
       } else if constexpr (kRole == kDs) {
@@ -617,7 +623,7 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
     }
     return;
   }
-  if (op.kind == TWFA_OP_RD) {
+  if (kind == TWFA_OP_RD) {
     if constexpr (kRole == kReduce || kRole == kReduceFull) rd_op<kRole == kReduceFull>(c, a, t, it, g, plan, st);
     return;
   }
@@ -625,12 +631,12 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
   constexpr bool kSolo = kRole == kLightSolo;
   // tensor-core ops: warp-uniform descriptors, one elected lane issues
   if (TWFA_BWD_LAZY_LOADS) {  // a deferred load this op needs is forced now
-    if (op.kind == TWFA_OP_ST || op.kind == TWFA_OP_DK) bwd_top_up<kRole == kLightSolo>(c, a, t, st, plan, true, it, true);
-    if (op.kind == TWFA_OP_DP || op.kind == TWFA_OP_DV) bwd_top_up<kRole == kLightSolo>(c, a, t, st, plan, false, it, true);
+    if (kind == TWFA_OP_ST || kind == TWFA_OP_DK) bwd_top_up<kRole == kLightSolo>(c, a, t, st, plan, true, it, true);
+    if (kind == TWFA_OP_DP || kind == TWFA_OP_DV) bwd_top_up<kRole == kLightSolo>(c, a, t, st, plan, false, it, true);
   }
   const uint32_t qs = g % plan.k_depth, os = g % plan.v_depth;
   const bool release = op.flags & TWFA_OPF_RELEASE;
-  if (op.kind == TWFA_OP_ST) {
+  if (kind == TWFA_OP_ST) {
     if (it == 0) mbar_wait(&bar.kv_full, t.icount & 1);
     // P^T(g-1) was read by DV(g-1) (in order) and, with DS on its own
     // warpgroup, by DS(g-1) (p_read)
@@ -655,7 +661,7 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
       if (release) mma_commit(&bar.q_empty[qs]);
     }
     wsync<kSolo>();
-  } else if (op.kind == TWFA_OP_DP) {
+  } else if (kind == TWFA_OP_DP) {
     if (it == 0) mbar_wait(&bar.kv_full, t.icount & 1);
     const bool o_need = !(TWFA_BWD_MEMO && st.o_seen == g + 1);
     if (g > 0 && o_need)  // dQ_(g-1) (over dP^T) has been read out
@@ -681,8 +687,8 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
       if (release) mma_commit(&bar.o_empty[os]);
     }
     wsync<kSolo>();
-  } else if (op.kind == TWFA_OP_DV || op.kind == TWFA_OP_DK) {
-    const bool dv = op.kind == TWFA_OP_DV;
+  } else if (kind == TWFA_OP_DV || kind == TWFA_OP_DK) {
+    const bool dv = kind == TWFA_OP_DV;
     // the accumulator is overwritten at iteration 0: the previous work
     // item's dK / dV must have been read out
     if (it == 0 && t.icount > 0) mbar_wait(&bar.acc_free, (t.icount - 1) & 1);
@@ -715,7 +721,7 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
       if (release) mma_commit(dv ? &bar.o_empty[os] : &bar.q_empty[qs]);
     }
     wsync<kSolo>();
-  } else if (op.kind == TWFA_OP_DQ) {
+  } else if (kind == TWFA_OP_DQ) {
     if (!(TWFA_BWD_MEMO && st.ds_seen == g + 1)) bwd_wait_ds(st, plan, g);
     tc_fence_after();
     bwd_ready(st);
@@ -748,6 +754,18 @@ __device__ __forceinline__ void bwd_run(const BwdCtx& c, const TwfaDevicePlan& p
   const int plen = plan.prog_len[src];
   const bool is_load = TWFA_BWD_LOAD_WARP >= 0 ? loads_only : c.warp == static_cast<uint32_t>(plan.load_warp);
   const bool is_mma = c.warp == static_cast<uint32_t>(plan.mma_warp);
+  // TWFA_BWD_FIXED: the TMA / MMA warp whose program is the production order
+  // runs it unrolled with every op's kind known at compile time
+  constexpr int kFixed[7] = {TWFA_OP_ST, TWFA_OP_LDQ, TWFA_OP_LDO, TWFA_OP_DP, TWFA_OP_DK, TWFA_OP_DQ, TWFA_OP_DV};
+  bool fixed = false;
+  TwfaPlanOp fx[7];
+  if constexpr (kRole == kLight) {
+    fixed = TWFA_BWD_FIXED && plen == 7 && is_load && is_mma && !loads_only && !skip_loads;
+    for (int j = 0; j < 7 && fixed; ++j) {
+      fx[j] = plan.ops[plan.prog[src][j]];
+      fixed = fx[j].kind == kFixed[j];
+    }
+  }
   BwdState st{0, 0, -1, -1, 0, nullptr, 0, 0, 0, 0};
   uint32_t gbase = 0, icount = 0;
   for (int i = 0;; ++i, ++icount) {
@@ -777,6 +795,19 @@ __device__ __forceinline__ void bwd_run(const BwdCtx& c, const TwfaDevicePlan& p
     st.q_next = st.o_next = 0;
     st.q_target = st.o_target = -1;
     const int trips = t.N + plan.max_stage;
+    if (fixed) {
+      // the production TMA / MMA program [ST LDQ LDO DP DK DQ DV], each op
+      // compiled for its own kind (TWFA_BWD_FIXED)
+      for (int rr = -1; rr < trips; ++rr) {
+        bwd_exec<kRole, TWFA_OP_ST>(fx[0], rr, c, t, st, plan, a);
+        bwd_exec<kRole, TWFA_OP_LDQ>(fx[1], rr, c, t, st, plan, a);
+        bwd_exec<kRole, TWFA_OP_LDO>(fx[2], rr, c, t, st, plan, a);
+        bwd_exec<kRole, TWFA_OP_DP>(fx[3], rr, c, t, st, plan, a);
+        bwd_exec<kRole, TWFA_OP_DK>(fx[4], rr, c, t, st, plan, a);
+        bwd_exec<kRole, TWFA_OP_DQ>(fx[5], rr, c, t, st, plan, a);
+        bwd_exec<kRole, TWFA_OP_DV>(fx[6], rr, c, t, st, plan, a);
+      }
+    } else
     for (int rr = -1; rr < trips; ++rr)
       for (int j = 0; j < plen; ++j) {
         const TwfaPlanOp& op = plan.ops[plan.prog[src][j]];
