@@ -76,7 +76,7 @@ constexpr uint32_t kSdHi = sdesc_hi(1024);
 // (TWFA_BWD_RD_FULL), so q_free -- which DP_(i+1) waits for -- is signalled
 // right after the read instead of after half of the staging and reduction
 #ifndef TWFA_BWD_RD_FULL
-#define TWFA_BWD_RD_FULL 1
+#define TWFA_BWD_RD_FULL 0  // measured with TWFA_BWD_FIXED: 749 vs 766-770 TF/s (C3 shape)
 #endif
 #ifndef TWFA_BWD_FIXED
 #define TWFA_BWD_FIXED 1
