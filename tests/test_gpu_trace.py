@@ -155,3 +155,32 @@ def test_steady_state_cycles_per_trip(twfa):
     print(f"\nsteady-state cycles per trip (traced): measured {steady:.0f}, predicted I*unit = {predicted}, "
           f"ratio {steady / predicted:.2f}")
     assert predicted <= steady <= 1.6 * predicted
+
+
+def test_untraced_cycles_per_trip_near_the_model(twfa):
+    """The production forward at the C3 shape with tracing reduced to CTA 0's
+    clock stamps (trace_cap = 2: no op records): CTA 0's clock64 span over its
+    K/V trips, tile boundaries included, against the calibrated model's
+    I x unit. Measured 1.14 x (C3, tile boundaries included); the bound is 1.2 x."""
+    prob, sol = twfa.load_schedule("fa_fwd")
+    plan = twfa.Plan(prob, sol)
+    d = plan.describe()
+    B, H, S = 4, 32, 8192
+    g = torch.Generator(device="cuda").manual_seed(2026)
+    q, k, v = (torch.randn(B, H, S, 128, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
+    tr = torch.zeros(d["num_warps"] * 2 * 8, dtype=torch.int32, device="cuda")
+    twfa.fa_fwd(plan, q, k, v)  # warm
+    twfa.fa_fwd(plan, q, k, v, trace=tr, trace_cap=2)
+    torch.cuda.synchronize()
+    w = tr[:5].cpu().numpy().view(np.uint32).astype(np.int64)
+    span = (w[3] - w[1]) % (1 << 32)
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    pair = d.get("cta_pair", False) and os.environ.get("TWFA_PAIR", "1") != "0"
+    units, rows = (sms // 2, 512) if pair else (sms, 256)  # work units and their query rows
+    tiles = B * H * (S // rows)
+    trips = -(-tiles // units) * (S // 128)
+    per_trip = span / trips
+    predicted = d["I"] * 256
+    print(f"\nuntraced clk per trip (CTA 0, boundaries included): {per_trip:.0f}, I x unit {predicted}, "
+          f"ratio {per_trip / predicted:.3f}")
+    assert predicted <= per_trip <= 1.2 * predicted
