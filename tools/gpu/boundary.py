@@ -6,11 +6,12 @@ plan = twfa.Plan(prob, sol)
 ids = [n["id"] for n in json.loads(prob)["graph"]["nodes"]]
 nw, cap = 16, 8192
 tr = torch.zeros(nw * cap * 8, dtype=torch.int32, device="cuda")
-q, k, v = (torch.randn(4, 32, 8192, 128, device="cuda").to(torch.bfloat16) for _ in range(3))
+S = int(os.environ.get("S", "8192"))
+q, k, v = (torch.randn(4, 32, S, 128, device="cuda").to(torch.bfloat16) for _ in range(3))
 twfa.fa_fwd(plan, q, k, v); twfa.fa_fwd(plan, q, k, v, trace=tr, trace_cap=cap); torch.cuda.synchronize()
 t = tr.cpu().numpy().view(np.uint32).reshape(nw, cap, 8).astype(np.int64)
 recs = []
-for w in (0, 4, 8, 15):
+for w in (0, 3, 4, 7, 8, 11, 15):
     for i in range(int(t[w, 0, 0])):
         e = [int(x) for x in t[w, 1 + i, :6]]
         if e[2] >= 1 << 31: e[2] -= 1 << 32
