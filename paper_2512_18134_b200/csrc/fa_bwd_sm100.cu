@@ -78,6 +78,9 @@ constexpr uint32_t kSdHi = sdesc_hi(1024);
 #ifndef TWFA_BWD_RD_FULL
 #define TWFA_BWD_RD_FULL 0  // measured with TWFA_BWD_FIXED: 749 vs 766-770 TF/s (C3 shape)
 #endif
+#ifndef TWFA_BWD_CDEPTH
+#define TWFA_BWD_CDEPTH 1
+#endif
 #ifndef TWFA_BWD_FIXED
 #define TWFA_BWD_FIXED 1
 #endif
@@ -191,12 +194,12 @@ __device__ __forceinline__ uint32_t* bwd_trace(const FaBwdArgs& a, const BwdCtx&
 #ifndef TWFA_BWD_LAZY_LOADS
 #define TWFA_BWD_LAZY_LOADS 0  // measured: 712 vs 764 TFLOP/s (C3 shape), eager is faster
 #endif
-template <bool kSolo>
+template <bool kSolo, int kDepth = 0>
 __device__ __forceinline__ void bwd_top_up(const BwdCtx& c, const FaBwdArgs& a, const BwdItem& t, BwdState& st,
                                            const TwfaDevicePlan& plan, bool is_q, int upto, bool blocking) {
   BwdBarriers& bar = g_bb;
   int& next = is_q ? st.q_next : st.o_next;
-  const int depth = is_q ? plan.k_depth : plan.v_depth;
+  const int depth = kDepth > 0 ? kDepth : is_q ? plan.k_depth : plan.v_depth;  // kDepth: known ring depth
   while (next <= upto) {
     const int lit = next;
     const uint32_t g = t.gbase + static_cast<uint32_t>(lit);
@@ -568,7 +571,8 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
       const int target = min(t.N - 1, r - static_cast<int>(op.stage) + (is_q ? plan.k_prefetch : plan.v_prefetch));
       (is_q ? st.q_target : st.o_target) = target;
       const int before = is_q ? st.q_next : st.o_next;
-      bwd_top_up<kRole == kLightSolo>(c, a, t, st, plan, is_q, target, !TWFA_BWD_LAZY_LOADS);
+      if constexpr (kKind >= 0 && TWFA_BWD_CDEPTH) bwd_top_up<kRole == kLightSolo, 2>(c, a, t, st, plan, is_q, target, !TWFA_BWD_LAZY_LOADS);
+      else bwd_top_up<kRole == kLightSolo>(c, a, t, st, plan, is_q, target, !TWFA_BWD_LAZY_LOADS);
       if (a.trace != nullptr)
         for (int lit = before; lit < (is_q ? st.q_next : st.o_next); ++lit) {
           uint32_t* e = bwd_trace(a, c, st, op.node, lit, r, t);
@@ -634,16 +638,20 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
     if (kind == TWFA_OP_ST || kind == TWFA_OP_DK) bwd_top_up<kRole == kLightSolo>(c, a, t, st, plan, true, it, true);
     if (kind == TWFA_OP_DP || kind == TWFA_OP_DV) bwd_top_up<kRole == kLightSolo>(c, a, t, st, plan, false, it, true);
   }
-  const uint32_t qs = g % plan.k_depth, os = g % plan.v_depth;
+  // ring depths: compile-time 2 on the fixed production program (checked
+  // before it is taken), the plan's otherwise
+  const uint32_t kd = kKind >= 0 && TWFA_BWD_CDEPTH ? 2u : static_cast<uint32_t>(plan.k_depth);
+  const uint32_t vd = kKind >= 0 && TWFA_BWD_CDEPTH ? 2u : static_cast<uint32_t>(plan.v_depth);
+  const uint32_t qs = g % kd, os = g % vd;
   const bool release = op.flags & TWFA_OPF_RELEASE;
   if (kind == TWFA_OP_ST) {
     if (it == 0) mbar_wait(&bar.kv_full, t.icount & 1);
     // P^T(g-1) was read by DV(g-1) (in order) and, with DS on its own
     // warpgroup, by DS(g-1) (p_read)
     if (g > 0 && (op.flags & TWFA_OPF_WAIT_PREAD))
-      mbar_wait_all(&bar.q_full[qs], (g / plan.k_depth) & 1, &bar.p_read, (g - 1) & 1);
+      mbar_wait_all(&bar.q_full[qs], (g / kd) & 1, &bar.p_read, (g - 1) & 1);
     else if (!(TWFA_BWD_MEMO && st.q_seen == g + 1))
-      mbar_wait(&bar.q_full[qs], (g / plan.k_depth) & 1);
+      mbar_wait(&bar.q_full[qs], (g / kd) & 1);
     st.q_seen = g + 1;
     tc_fence_after();
     bwd_ready(st);
@@ -665,11 +673,11 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
     if (it == 0) mbar_wait(&bar.kv_full, t.icount & 1);
     const bool o_need = !(TWFA_BWD_MEMO && st.o_seen == g + 1);
     if (g > 0 && o_need)  // dQ_(g-1) (over dP^T) has been read out
-      mbar_wait_all(&bar.o_full[os], (g / plan.v_depth) & 1, &bar.q_free, (g - 1) & 1);
+      mbar_wait_all(&bar.o_full[os], (g / vd) & 1, &bar.q_free, (g - 1) & 1);
     else if (g > 0)
       mbar_wait(&bar.q_free, (g - 1) & 1);
     else if (o_need)
-      mbar_wait(&bar.o_full[os], (g / plan.v_depth) & 1);
+      mbar_wait(&bar.o_full[os], (g / vd) & 1);
     st.o_seen = g + 1;
     tc_fence_after();
     bwd_ready(st);
@@ -694,16 +702,16 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
     if (it == 0 && t.icount > 0) mbar_wait(&bar.acc_free, (t.icount - 1) & 1);
     if (!TWFA_BWD_MEMO) {
       if (dv)
-        mbar_wait_all(&bar.p_full, g & 1, &bar.o_full[os], (g / plan.v_depth) & 1);
+        mbar_wait_all(&bar.p_full, g & 1, &bar.o_full[os], (g / vd) & 1);
       else
-        mbar_wait_all(&bar.ds_full, g & 1, &bar.q_full[qs], (g / plan.k_depth) & 1);
+        mbar_wait_all(&bar.ds_full, g & 1, &bar.q_full[qs], (g / kd) & 1);
     } else if (dv) {
       if (st.p_seen != g + 1) mbar_wait(&bar.p_full, g & 1);
-      if (st.o_seen != g + 1) mbar_wait(&bar.o_full[os], (g / plan.v_depth) & 1);
+      if (st.o_seen != g + 1) mbar_wait(&bar.o_full[os], (g / vd) & 1);
       st.p_seen = st.o_seen = g + 1;
     } else {
       if (st.ds_seen != g + 1) bwd_wait_ds(st, plan, g);
-      if (st.q_seen != g + 1) mbar_wait(&bar.q_full[qs], (g / plan.k_depth) & 1);
+      if (st.q_seen != g + 1) mbar_wait(&bar.q_full[qs], (g / kd) & 1);
       st.q_seen = g + 1;
     }
     tc_fence_after();
@@ -760,7 +768,8 @@ __device__ __forceinline__ void bwd_run(const BwdCtx& c, const TwfaDevicePlan& p
   bool fixed = false;
   TwfaPlanOp fx[7];
   if constexpr (kRole == kLight) {
-    fixed = TWFA_BWD_FIXED && plen == 7 && is_load && is_mma && !loads_only && !skip_loads;
+    fixed = TWFA_BWD_FIXED && plen == 7 && is_load && is_mma && !loads_only && !skip_loads && plan.k_depth == 2 &&
+            plan.v_depth == 2;
     for (int j = 0; j < 7 && fixed; ++j) {
       fx[j] = plan.ops[plan.prog[src][j]];
       fixed = fx[j].kind == kFixed[j];
