@@ -323,15 +323,19 @@ __device__ __forceinline__ void kv_epilogue_pp(const PpCtx& c, const FaBwdArgs& 
   warp_arrive(&bar.acc_free);
 }
 
+#ifndef TWFA_BWD_FIXED
+#define TWFA_BWD_FIXED 1
+#endif
 enum PpRole { kPpLight = 0, kPpReduce = 1, kPpExbDs = 2 };
 
-template <int kRole>
+template <int kRole, int kKind = -1>
 __device__ __forceinline__ void pp_exec(const TwfaPlanOp op, const int r, const PpCtx& c, const PpItem& t,
                                         PpState& st, const TwfaDevicePlan& plan, const FaBwdArgs& a) {
   PpBarriers& bar = g_pb;
-  if (op.kind == TWFA_OP_LDQ || op.kind == TWFA_OP_LDO) {
+  const int kind = kKind >= 0 ? kKind : static_cast<int>(op.kind);  // kKind: known at the call site
+  if (kind == TWFA_OP_LDQ || kind == TWFA_OP_LDO) {
     if constexpr (kRole == kPpLight) {
-      const bool is_q = op.kind == TWFA_OP_LDQ;
+      const bool is_q = kind == TWFA_OP_LDQ;
       const int target = min(t.N - 1, r - static_cast<int>(op.stage) + (is_q ? plan.k_prefetch : plan.v_prefetch));
       const int before = is_q ? st.q_next : st.o_next;
       pp_top_up(c, a, t, st, plan, is_q, target);
@@ -354,12 +358,12 @@ __device__ __forceinline__ void pp_exec(const TwfaPlanOp op, const int r, const 
     }
   } trace_done_{a.trace != nullptr ? pp_trace(a, c, st, op.node, it, r, t) : nullptr};
   st.rec = trace_done_.e;
-  if (op.kind == TWFA_OP_EXB || op.kind == TWFA_OP_DS) {
+  if (kind == TWFA_OP_EXB || kind == TWFA_OP_DS) {
     if constexpr (kRole == kPpExbDs)
-      if (op.kind == TWFA_OP_EXB) exb_ds(c, a, t, it, g, k, st);  // DS_k fused (lowering guarantees)
+      if (kind == TWFA_OP_EXB) exb_ds(c, a, t, it, g, k, st);  // DS_k fused (lowering guarantees)
     return;
   }
-  if (op.kind == TWFA_OP_RD) {
+  if (kind == TWFA_OP_RD) {
     if constexpr (kRole == kPpReduce) rd_pp(c, a, t, it, g, k, st);
     return;
   }
@@ -369,8 +373,8 @@ __device__ __forceinline__ void pp_exec(const TwfaPlanOp op, const int r, const 
   const bool release = op.flags & TWFA_OPF_RELEASE;
   uint8_t* const qk = c.q + qs * kTile + k * kSubRows;  // Q_k rows of the tile (both head-dim halves + kHalf)
   uint8_t* const ok = c.o + os * kTile + k * kSubRows;
-  if (op.kind == TWFA_OP_ST || op.kind == TWFA_OP_DP) {
-    const bool is_s = op.kind == TWFA_OP_ST;
+  if (kind == TWFA_OP_ST || kind == TWFA_OP_DP) {
+    const bool is_s = kind == TWFA_OP_ST;
     if (it == 0) mbar_wait(&bar.kv_full, t.icount & 1);
     if (is_s) {
       // S^T_k(g) overwrites dQ^T_k(g-1), which RD_k(g-1) must have read out
@@ -399,8 +403,8 @@ __device__ __forceinline__ void pp_exec(const TwfaPlanOp op, const int r, const 
       if (release) mma_commit(is_s ? &bar.q_empty[qs] : &bar.o_empty[os]);
     }
     __syncwarp();
-  } else if (op.kind == TWFA_OP_DV || op.kind == TWFA_OP_DK) {
-    const bool dv = op.kind == TWFA_OP_DV;
+  } else if (kind == TWFA_OP_DV || kind == TWFA_OP_DK) {
+    const bool dv = kind == TWFA_OP_DV;
     bool& started = dv ? st.dv_started : st.dk_started;
     // the accumulator is overwritten by the item's first MMA: the previous
     // work item's dK / dV must have been read out
@@ -427,7 +431,7 @@ __device__ __forceinline__ void pp_exec(const TwfaPlanOp op, const int r, const 
     }
     __syncwarp();
     started = true;
-  } else if (op.kind == TWFA_OP_DQ) {
+  } else if (kind == TWFA_OP_DQ) {
     mbar_wait(&bar.ds_full[k], g & 1);
     tc_fence_after();
     pp_ready(st);
@@ -452,6 +456,17 @@ __device__ __forceinline__ void pp_run(const PpCtx& c, const TwfaDevicePlan& pla
   const bool is_load = c.warp == static_cast<uint32_t>(plan.load_warp);
   const bool is_mma = c.warp == static_cast<uint32_t>(plan.mma_warp);
   PpState st{0, 0, 0, nullptr, false, false, 0, 0};
+  constexpr int kFixed[12] = {TWFA_OP_ST, TWFA_OP_LDQ, TWFA_OP_ST, TWFA_OP_DP, TWFA_OP_LDO, TWFA_OP_DP,
+                              TWFA_OP_DV, TWFA_OP_DQ, TWFA_OP_DV, TWFA_OP_DQ, TWFA_OP_DK, TWFA_OP_DK};
+  bool fixed = false;
+  TwfaPlanOp fx[12];
+  if constexpr (kRole == kPpLight) {
+    fixed = TWFA_BWD_FIXED && plen == 12 && is_load && is_mma;
+    for (int j = 0; j < 12 && fixed; ++j) {
+      fx[j] = plan.ops[plan.prog[c.warp][j]];
+      fixed = fx[j].kind == kFixed[j];
+    }
+  }
   uint32_t gbase = 0, icount = 0;
   for (int i = 0;; ++i, ++icount) {
     int work;
@@ -480,6 +495,24 @@ __device__ __forceinline__ void pp_run(const PpCtx& c, const TwfaDevicePlan& pla
     st.q_next = st.o_next = 0;
     st.dv_started = st.dk_started = false;
     const int trips = t.N + plan.max_stage;
+    if (fixed) {
+      // the committed TMA / MMA program, each op compiled for its kind
+      // (TWFA_BWD_FIXED, as in fa_bwd_sm100.cu)
+      for (int rr = -1; rr < trips; ++rr) {
+        pp_exec<kRole, TWFA_OP_ST>(fx[0], rr, c, t, st, plan, a);
+        pp_exec<kRole, TWFA_OP_LDQ>(fx[1], rr, c, t, st, plan, a);
+        pp_exec<kRole, TWFA_OP_ST>(fx[2], rr, c, t, st, plan, a);
+        pp_exec<kRole, TWFA_OP_DP>(fx[3], rr, c, t, st, plan, a);
+        pp_exec<kRole, TWFA_OP_LDO>(fx[4], rr, c, t, st, plan, a);
+        pp_exec<kRole, TWFA_OP_DP>(fx[5], rr, c, t, st, plan, a);
+        pp_exec<kRole, TWFA_OP_DV>(fx[6], rr, c, t, st, plan, a);
+        pp_exec<kRole, TWFA_OP_DQ>(fx[7], rr, c, t, st, plan, a);
+        pp_exec<kRole, TWFA_OP_DV>(fx[8], rr, c, t, st, plan, a);
+        pp_exec<kRole, TWFA_OP_DQ>(fx[9], rr, c, t, st, plan, a);
+        pp_exec<kRole, TWFA_OP_DK>(fx[10], rr, c, t, st, plan, a);
+        pp_exec<kRole, TWFA_OP_DK>(fx[11], rr, c, t, st, plan, a);
+      }
+    } else
     for (int rr = -1; rr < trips; ++rr)
       for (int j = 0; j < plen; ++j) pp_exec<kRole>(plan.ops[plan.prog[c.warp][j]], rr, c, t, st, plan, a);
     if constexpr (kRole == kPpLight) {
