@@ -751,7 +751,7 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
   }
 }
 
-template <int kRole>
+template <int kRole, bool kSpec>
 __device__ __forceinline__ void bwd_run(const BwdCtx& c, const TwfaDevicePlan& plan, const FaBwdArgs& a) {
   BwdBarriers& bar = g_bb;
   // TWFA_BWD_LOAD_WARP >= 0: that warp runs the load warp's streamed loads
@@ -768,7 +768,7 @@ __device__ __forceinline__ void bwd_run(const BwdCtx& c, const TwfaDevicePlan& p
   bool fixed = false;
   TwfaPlanOp fx[7];
   if constexpr (kRole == kLight) {
-    fixed = TWFA_BWD_FIXED && plen == 7 && is_load && is_mma && !loads_only && !skip_loads && plan.k_depth == 2 &&
+    fixed = kSpec && plen == 7 && is_load && is_mma && !loads_only && !skip_loads && plan.k_depth == 2 &&
             plan.v_depth == 2;
     for (int j = 0; j < 7 && fixed; ++j) {
       fx[j] = plan.ops[plan.prog[src][j]];
@@ -816,6 +816,8 @@ __device__ __forceinline__ void bwd_run(const BwdCtx& c, const TwfaDevicePlan& p
         bwd_exec<kRole, TWFA_OP_DQ>(fx[5], rr, c, t, st, plan, a);
         bwd_exec<kRole, TWFA_OP_DV>(fx[6], rr, c, t, st, plan, a);
       }
+    } else if (kSpec && kRole == kLight && is_mma) {
+      __trap();  // the host launches the specialized kernel only for the fixed program
     } else
     for (int rr = -1; rr < trips; ++rr)
       for (int j = 0; j < plen; ++j) {
@@ -839,6 +841,11 @@ __device__ __forceinline__ void bwd_run(const BwdCtx& c, const TwfaDevicePlan& p
   }
 }
 
+// kSpec: the production TMA / MMA program [ST LDQ LDO DP DK DQ DV] compiled
+// for its op kinds (TWFA_BWD_FIXED), and no generic op loop in that role --
+// the generic loop's code alone costs the role 5 % (810 vs 775 TF/s, C3
+// shape). The host picks the instantiation (bwd_fixed_program).
+template <bool kSpec>
 __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
     fa_bwd_kernel(const __grid_constant__ TwfaDevicePlan plan, const __grid_constant__ FaBwdArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -900,30 +907,30 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
   // (64) and a dP^T chunk, RD half a dQ row; the TMA / MMA warps need few
   if (exb && ds) {
     setmaxnreg_inc<200>();
-    bwd_run<kExbDs>(c, plan, a);
+    bwd_run<kExbDs, kSpec>(c, plan, a);
   } else if (exb) {
     setmaxnreg_inc<168>();
-    bwd_run<kExb>(c, plan, a);
+    bwd_run<kExb, kSpec>(c, plan, a);
   } else if (ds) {
     setmaxnreg_inc<144>();
-    bwd_run<kDs>(c, plan, a);
+    bwd_run<kDs, kSpec>(c, plan, a);
   } else if (rd) {
     // with EXB and DS fused on one warpgroup the register file has room for
     // the whole dQ row in RD (200 + 176 + 8 x 64 per thread-warp class)
     if (TWFA_BWD_RD_FULL && plan.sm_warp[0] == plan.sm_warp[1]) {
       setmaxnreg_inc<176>();
-      bwd_run<kReduceFull>(c, plan, a);
+      bwd_run<kReduceFull, kSpec>(c, plan, a);
     } else {
       setmaxnreg_dec<128>();
-      bwd_run<kReduce>(c, plan, a);
+      bwd_run<kReduce, kSpec>(c, plan, a);
     }
   } else {
     setmaxnreg_dec<64>();
     if (TWFA_BWD_SOLO) {
-      if (elect_one()) bwd_run<kLightSolo>(c, plan, a);
+      if (elect_one()) bwd_run<kLightSolo, false>(c, plan, a);
       __syncwarp();
     } else {
-      bwd_run<kLight>(c, plan, a);
+      bwd_run<kLight, kSpec>(c, plan, a);
     }
   }
   if (c.lane == 0) bulk_wait_all();
@@ -990,6 +997,21 @@ size_t fa_bwd_workspace_bytes(int B, int H, int S) {
   return rows * 128 * sizeof(float) + rows * sizeof(float);
 }
 
+// host mirror of the device-side condition of the fixed program: the TMA /
+// MMA warp (one warp) holds exactly [ST LDQ LDO DP DK DQ DV], Q and dO rings
+// two deep, the default one-warp roles
+bool bwd_fixed_program(const TwfaDevicePlan& plan) {
+  if (plan.num_tiles != 1 || plan.k_depth != 2 || plan.v_depth != 2 || plan.mma_warp != plan.load_warp ||
+      TWFA_BWD_SOLO || TWFA_BWD_LOAD_WARP >= 0)
+    return false;
+  const int w = plan.mma_warp;
+  static const int kinds[7] = {TWFA_OP_ST, TWFA_OP_LDQ, TWFA_OP_LDO, TWFA_OP_DP, TWFA_OP_DK, TWFA_OP_DQ, TWFA_OP_DV};
+  if (w < 0 || w >= TWFA_MAX_WARPS || plan.prog_len[w] != 7) return false;
+  for (int j = 0; j < 7; ++j)
+    if (plan.ops[plan.prog[w][j]].kind != kinds[j]) return false;
+  return true;
+}
+
 cudaError_t fa_bwd_launch(const TwfaDevicePlan& plan, const FaBwdArgs& args, const __nv_bfloat16* o,
                           const __nv_bfloat16* dout, __nv_bfloat16* dq, int grid, cudaStream_t stream) {
   const int64_t rows = static_cast<int64_t>(args.B) * args.H * args.S;
@@ -1000,9 +1022,15 @@ cudaError_t fa_bwd_launch(const TwfaDevicePlan& plan, const FaBwdArgs& args, con
     e = fa_bwd_pp_main_launch(plan, args, grid, stream);
   } else {
     const size_t smem = fa_bwd_smem_bytes(plan);
-    e = cudaFuncSetAttribute(fa_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    const bool spec = TWFA_BWD_FIXED && bwd_fixed_program(plan);
+    const void* kern = spec ? reinterpret_cast<const void*>(&fa_bwd_kernel<true>)
+                            : reinterpret_cast<const void*>(&fa_bwd_kernel<false>);
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    fa_bwd_kernel<<<grid, TWFA_MAX_WARPS * 32, smem, stream>>>(plan, args);
+    if (spec)
+      fa_bwd_kernel<true><<<grid, TWFA_MAX_WARPS * 32, smem, stream>>>(plan, args);
+    else
+      fa_bwd_kernel<false><<<grid, TWFA_MAX_WARPS * 32, smem, stream>>>(plan, args);
     e = cudaGetLastError();
   }
   if (e != cudaSuccess) return e;
