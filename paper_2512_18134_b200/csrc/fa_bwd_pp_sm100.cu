@@ -449,7 +449,7 @@ __device__ __forceinline__ void pp_exec(const TwfaPlanOp op, const int r, const 
   }
 }
 
-template <int kRole>
+template <int kRole, bool kSpec>
 __device__ __forceinline__ void pp_run(const PpCtx& c, const TwfaDevicePlan& plan, const FaBwdArgs& a, int rd_k) {
   PpBarriers& bar = g_pb;
   const int plen = plan.prog_len[c.warp];
@@ -461,7 +461,7 @@ __device__ __forceinline__ void pp_run(const PpCtx& c, const TwfaDevicePlan& pla
   bool fixed = false;
   TwfaPlanOp fx[12];
   if constexpr (kRole == kPpLight) {
-    fixed = TWFA_BWD_FIXED && plen == 12 && is_load && is_mma;
+    fixed = kSpec && plen == 12 && is_load && is_mma;
     for (int j = 0; j < 12 && fixed; ++j) {
       fx[j] = plan.ops[plan.prog[c.warp][j]];
       fixed = fx[j].kind == kFixed[j];
@@ -512,6 +512,8 @@ __device__ __forceinline__ void pp_run(const PpCtx& c, const TwfaDevicePlan& pla
         pp_exec<kRole, TWFA_OP_DK>(fx[10], rr, c, t, st, plan, a);
         pp_exec<kRole, TWFA_OP_DK>(fx[11], rr, c, t, st, plan, a);
       }
+    } else if (kSpec && kRole == kPpLight && is_mma) {
+      __trap();  // the host launches the specialized kernel only for the fixed program
     } else
     for (int rr = -1; rr < trips; ++rr)
       for (int j = 0; j < plen; ++j) pp_exec<kRole>(plan.ops[plan.prog[c.warp][j]], rr, c, t, st, plan, a);
@@ -530,6 +532,7 @@ __device__ __forceinline__ void pp_run(const PpCtx& c, const TwfaDevicePlan& pla
   }
 }
 
+template <bool kSpec>  // the committed 12-op TMA / MMA program in its own instantiation
 __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
     fa_bwd_pp_kernel(const __grid_constant__ TwfaDevicePlan plan, const __grid_constant__ FaBwdArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -588,13 +591,13 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
   // and the packed dS; RD a 64-float dQ^T row; the TMA / MMA warps few
   if (wg == plan.sm_warp[0] || wg == plan.sm_warp[1]) {
     setmaxnreg_inc<184>();
-    pp_run<kPpExbDs>(c, plan, a, -1);
+    pp_run<kPpExbDs, kSpec>(c, plan, a, -1);
   } else if (wg == plan.cr_warp[0] || wg == plan.cr_warp[1]) {
     setmaxnreg_dec<96>();
-    pp_run<kPpReduce>(c, plan, a, wg == plan.cr_warp[0] ? 0 : 1);
+    pp_run<kPpReduce, kSpec>(c, plan, a, wg == plan.cr_warp[0] ? 0 : 1);
   } else {
     setmaxnreg_dec<48>();
-    pp_run<kPpLight>(c, plan, a, -1);
+    pp_run<kPpLight, kSpec>(c, plan, a, -1);
   }
   if (c.lane == 0) bulk_wait_all();
   tc_fence_before();
@@ -611,12 +614,28 @@ size_t fa_bwd_pp_smem_bytes(const TwfaDevicePlan& plan) {
   return static_cast<size_t>(2 + plan.k_depth + plan.v_depth) * kTile + 2 * kDsBytes + 1024;
 }
 
+// host mirror of the device-side condition of the fixed 12-op program
+static bool pp_fixed_program(const TwfaDevicePlan& plan) {
+  static const int kinds[12] = {TWFA_OP_ST, TWFA_OP_LDQ, TWFA_OP_ST, TWFA_OP_DP, TWFA_OP_LDO, TWFA_OP_DP,
+                                TWFA_OP_DV, TWFA_OP_DQ, TWFA_OP_DV, TWFA_OP_DQ, TWFA_OP_DK, TWFA_OP_DK};
+  const int w = plan.mma_warp;
+  if (w != plan.load_warp || w < 0 || w >= TWFA_MAX_WARPS || plan.prog_len[w] != 12) return false;
+  for (int j = 0; j < 12; ++j)
+    if (plan.ops[plan.prog[w][j]].kind != kinds[j]) return false;
+  return true;
+}
+
 cudaError_t fa_bwd_pp_main_launch(const TwfaDevicePlan& plan, const FaBwdArgs& args, int grid, cudaStream_t stream) {
   const size_t smem = fa_bwd_pp_smem_bytes(plan);
-  cudaError_t e =
-      cudaFuncSetAttribute(fa_bwd_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  const bool spec = TWFA_BWD_FIXED && pp_fixed_program(plan);
+  const void* kern = spec ? reinterpret_cast<const void*>(&fa_bwd_pp_kernel<true>)
+                          : reinterpret_cast<const void*>(&fa_bwd_pp_kernel<false>);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  fa_bwd_pp_kernel<<<grid, TWFA_MAX_WARPS * 32, smem, stream>>>(plan, args);
+  if (spec)
+    fa_bwd_pp_kernel<true><<<grid, TWFA_MAX_WARPS * 32, smem, stream>>>(plan, args);
+  else
+    fa_bwd_pp_kernel<false><<<grid, TWFA_MAX_WARPS * 32, smem, stream>>>(plan, args);
   return cudaGetLastError();
 }
 
