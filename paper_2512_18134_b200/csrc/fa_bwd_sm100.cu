@@ -81,6 +81,9 @@ constexpr uint32_t kSdHi = sdesc_hi(1024);
 #ifndef TWFA_BWD_CDEPTH
 #define TWFA_BWD_CDEPTH 1
 #endif
+#ifndef TWFA_BWD_HEAVY_SPEC
+#define TWFA_BWD_HEAVY_SPEC 1
+#endif
 #ifndef TWFA_BWD_FIXED
 #define TWFA_BWD_FIXED 1
 #endif
@@ -767,6 +770,12 @@ __device__ __forceinline__ void bwd_run(const BwdCtx& c, const TwfaDevicePlan& p
   constexpr int kFixed[7] = {TWFA_OP_ST, TWFA_OP_LDQ, TWFA_OP_LDO, TWFA_OP_DP, TWFA_OP_DK, TWFA_OP_DQ, TWFA_OP_DV};
   bool fixed = false;
   TwfaPlanOp fx[7];
+  if constexpr (kSpec && TWFA_BWD_HEAVY_SPEC && (kRole == kExbDs || kRole == kReduce)) {
+    // the production warpgroup programs [EXB DS] and [RD] (host-checked)
+    fixed = true;
+    fx[0] = plan.ops[plan.prog[src][0]];
+    if (kRole == kExbDs) fx[1] = plan.ops[plan.prog[src][1]];
+  }
   if constexpr (kRole == kLight) {
     fixed = kSpec && plen == 7 && is_load && is_mma && !loads_only && !skip_loads && plan.k_depth == 2 &&
             plan.v_depth == 2;
@@ -804,7 +813,14 @@ __device__ __forceinline__ void bwd_run(const BwdCtx& c, const TwfaDevicePlan& p
     st.q_next = st.o_next = 0;
     st.q_target = st.o_target = -1;
     const int trips = t.N + plan.max_stage;
-    if (fixed) {
+    if (kSpec && TWFA_BWD_HEAVY_SPEC && kRole == kExbDs) {
+      for (int rr = -1; rr < trips; ++rr) {
+        bwd_exec<kRole, TWFA_OP_EXB>(fx[0], rr, c, t, st, plan, a);
+        bwd_exec<kRole, TWFA_OP_DS>(fx[1], rr, c, t, st, plan, a);
+      }
+    } else if (kSpec && TWFA_BWD_HEAVY_SPEC && kRole == kReduce) {
+      for (int rr = -1; rr < trips; ++rr) bwd_exec<kRole, TWFA_OP_RD>(fx[0], rr, c, t, st, plan, a);
+    } else if (fixed) {
       // the production TMA / MMA program [ST LDQ LDO DP DK DQ DV], each op
       // compiled for its own kind (TWFA_BWD_FIXED)
       for (int rr = -1; rr < trips; ++rr) {
@@ -1004,6 +1020,13 @@ bool bwd_fixed_program(const TwfaDevicePlan& plan) {
   if (plan.num_tiles != 1 || plan.k_depth != 2 || plan.v_depth != 2 || plan.mma_warp != plan.load_warp ||
       TWFA_BWD_SOLO || TWFA_BWD_LOAD_WARP >= 0)
     return false;
+  if (TWFA_BWD_HEAVY_SPEC) {  // the fused [EXB DS] warpgroup and the [RD] warpgroup
+    const int e = plan.sm_warp[0], r = plan.cr_warp[0];
+    if (e != plan.sm_warp[1] || e < 0 || r < 0 || plan.prog_len[e] != 2 || plan.prog_len[r] != 1 ||
+        plan.ops[plan.prog[e][0]].kind != TWFA_OP_EXB || plan.ops[plan.prog[e][1]].kind != TWFA_OP_DS ||
+        plan.ops[plan.prog[r][0]].kind != TWFA_OP_RD)
+      return false;
+  }
   const int w = plan.mma_warp;
   static const int kinds[7] = {TWFA_OP_ST, TWFA_OP_LDQ, TWFA_OP_LDO, TWFA_OP_DP, TWFA_OP_DK, TWFA_OP_DQ, TWFA_OP_DV};
   if (w < 0 || w >= TWFA_MAX_WARPS || plan.prog_len[w] != 7) return false;
