@@ -561,7 +561,7 @@ __device__ __forceinline__ void bwd_wait_ds(BwdState& st, const TwfaDevicePlan& 
 }
 
 // One op of the trip program on this warp, trip r.
-template <int kRole, int kKind = -1>
+template <int kRole, int kKind = -1, bool kTrace = true>
 __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const BwdCtx& c, const BwdItem& t,
                                          BwdState& st, const TwfaDevicePlan& plan, const FaBwdArgs& a) {
   BwdBarriers& bar = g_bb;
@@ -576,7 +576,7 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
       const int before = is_q ? st.q_next : st.o_next;
       if constexpr (kKind >= 0 && TWFA_BWD_CDEPTH) bwd_top_up<kRole == kLightSolo, 2>(c, a, t, st, plan, is_q, target, !TWFA_BWD_LAZY_LOADS);
       else bwd_top_up<kRole == kLightSolo>(c, a, t, st, plan, is_q, target, !TWFA_BWD_LAZY_LOADS);
-      if (a.trace != nullptr)
+      if (kTrace && a.trace != nullptr)
         for (int lit = before; lit < (is_q ? st.q_next : st.o_next); ++lit) {
           uint32_t* e = bwd_trace(a, c, st, op.node, lit, r, t);
           if (e) e[5] = e[3];
@@ -599,7 +599,7 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
     __device__ ~TraceDone() {
       if (e) e[5] = static_cast<uint32_t>(clock64());
     }
-  } trace_done_{a.trace != nullptr ? bwd_trace(a, c, st, op.node, it, r, t) : nullptr};
+  } trace_done_{kTrace && a.trace != nullptr ? bwd_trace(a, c, st, op.node, it, r, t) : nullptr};
   st.rec = trace_done_.e;
 #if TWFA_BWD_PROF
   const bool prof = blockIdx.x == 0 && c.lane == 0 && (c.warp & 3u) == 3 && t.icount == 0 && (it == 20 || it == 21);
@@ -657,7 +657,7 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
       mbar_wait(&bar.q_full[qs], (g / kd) & 1);
     st.q_seen = g + 1;
     tc_fence_after();
-    bwd_ready(st);
+    if (kTrace) bwd_ready(st);
 #if TWFA_BWD_PROF
     g_prof_ready = clock64();
 #endif
@@ -683,7 +683,7 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
       mbar_wait(&bar.o_full[os], (g / vd) & 1);
     st.o_seen = g + 1;
     tc_fence_after();
-    bwd_ready(st);
+    if (kTrace) bwd_ready(st);
 #if TWFA_BWD_PROF
     g_prof_ready = clock64();
 #endif
@@ -718,7 +718,7 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
       st.q_seen = g + 1;
     }
     tc_fence_after();
-    bwd_ready(st);
+    if (kTrace) bwd_ready(st);
 #if TWFA_BWD_PROF
     g_prof_ready = clock64();
 #endif
@@ -735,7 +735,7 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
   } else if (kind == TWFA_OP_DQ) {
     if (!(TWFA_BWD_MEMO && st.ds_seen == g + 1)) bwd_wait_ds(st, plan, g);
     tc_fence_after();
-    bwd_ready(st);
+    if (kTrace) bwd_ready(st);
 #if TWFA_BWD_PROF
     g_prof_ready = clock64();
 #endif
@@ -754,7 +754,7 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
   }
 }
 
-template <int kRole, bool kSpec>
+template <int kRole, bool kSpec, bool kTrace>
 __device__ __forceinline__ void bwd_run(const BwdCtx& c, const TwfaDevicePlan& plan, const FaBwdArgs& a) {
   BwdBarriers& bar = g_bb;
   // TWFA_BWD_LOAD_WARP >= 0: that warp runs the load warp's streamed loads
@@ -815,22 +815,22 @@ __device__ __forceinline__ void bwd_run(const BwdCtx& c, const TwfaDevicePlan& p
     const int trips = t.N + plan.max_stage;
     if (kSpec && TWFA_BWD_HEAVY_SPEC && kRole == kExbDs) {
       for (int rr = -1; rr < trips; ++rr) {
-        bwd_exec<kRole, TWFA_OP_EXB>(fx[0], rr, c, t, st, plan, a);
-        bwd_exec<kRole, TWFA_OP_DS>(fx[1], rr, c, t, st, plan, a);
+        bwd_exec<kRole, TWFA_OP_EXB, kTrace>(fx[0], rr, c, t, st, plan, a);
+        bwd_exec<kRole, TWFA_OP_DS, kTrace>(fx[1], rr, c, t, st, plan, a);
       }
     } else if (kSpec && TWFA_BWD_HEAVY_SPEC && kRole == kReduce) {
-      for (int rr = -1; rr < trips; ++rr) bwd_exec<kRole, TWFA_OP_RD>(fx[0], rr, c, t, st, plan, a);
+      for (int rr = -1; rr < trips; ++rr) bwd_exec<kRole, TWFA_OP_RD, kTrace>(fx[0], rr, c, t, st, plan, a);
     } else if (fixed) {
       // the production TMA / MMA program [ST LDQ LDO DP DK DQ DV], each op
       // compiled for its own kind (TWFA_BWD_FIXED)
       for (int rr = -1; rr < trips; ++rr) {
-        bwd_exec<kRole, TWFA_OP_ST>(fx[0], rr, c, t, st, plan, a);
-        bwd_exec<kRole, TWFA_OP_LDQ>(fx[1], rr, c, t, st, plan, a);
-        bwd_exec<kRole, TWFA_OP_LDO>(fx[2], rr, c, t, st, plan, a);
-        bwd_exec<kRole, TWFA_OP_DP>(fx[3], rr, c, t, st, plan, a);
-        bwd_exec<kRole, TWFA_OP_DK>(fx[4], rr, c, t, st, plan, a);
-        bwd_exec<kRole, TWFA_OP_DQ>(fx[5], rr, c, t, st, plan, a);
-        bwd_exec<kRole, TWFA_OP_DV>(fx[6], rr, c, t, st, plan, a);
+        bwd_exec<kRole, TWFA_OP_ST, kTrace>(fx[0], rr, c, t, st, plan, a);
+        bwd_exec<kRole, TWFA_OP_LDQ, kTrace>(fx[1], rr, c, t, st, plan, a);
+        bwd_exec<kRole, TWFA_OP_LDO, kTrace>(fx[2], rr, c, t, st, plan, a);
+        bwd_exec<kRole, TWFA_OP_DP, kTrace>(fx[3], rr, c, t, st, plan, a);
+        bwd_exec<kRole, TWFA_OP_DK, kTrace>(fx[4], rr, c, t, st, plan, a);
+        bwd_exec<kRole, TWFA_OP_DQ, kTrace>(fx[5], rr, c, t, st, plan, a);
+        bwd_exec<kRole, TWFA_OP_DV, kTrace>(fx[6], rr, c, t, st, plan, a);
       }
     } else if (kSpec && kRole == kLight && is_mma) {
       __trap();  // the host launches the specialized kernel only for the fixed program
@@ -840,7 +840,7 @@ __device__ __forceinline__ void bwd_run(const BwdCtx& c, const TwfaDevicePlan& p
         const TwfaPlanOp& op = plan.ops[plan.prog[src][j]];
         const bool ld = op.kind == TWFA_OP_LDQ || op.kind == TWFA_OP_LDO;
         if ((loads_only && !ld) || (skip_loads && ld)) continue;
-        bwd_exec<kRole>(op, rr, c, t, st, plan, a);
+        bwd_exec<kRole, -1, kTrace>(op, rr, c, t, st, plan, a);
       }
     if constexpr (is_light(kRole)) {
       if (is_mma) {  // every MMA of the item issued: dK, dV final; K, V free
@@ -861,7 +861,7 @@ __device__ __forceinline__ void bwd_run(const BwdCtx& c, const TwfaDevicePlan& p
 // for its op kinds (TWFA_BWD_FIXED), and no generic op loop in that role --
 // the generic loop's code alone costs the role 5 % (810 vs 775 TF/s, C3
 // shape). The host picks the instantiation (bwd_fixed_program).
-template <bool kSpec>
+template <bool kSpec, bool kTrace>
 __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
     fa_bwd_kernel(const __grid_constant__ TwfaDevicePlan plan, const __grid_constant__ FaBwdArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -923,30 +923,30 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
   // (64) and a dP^T chunk, RD half a dQ row; the TMA / MMA warps need few
   if (exb && ds) {
     setmaxnreg_inc<200>();
-    bwd_run<kExbDs, kSpec>(c, plan, a);
+    bwd_run<kExbDs, kSpec, kTrace>(c, plan, a);
   } else if (exb) {
     setmaxnreg_inc<168>();
-    bwd_run<kExb, kSpec>(c, plan, a);
+    bwd_run<kExb, kSpec, kTrace>(c, plan, a);
   } else if (ds) {
     setmaxnreg_inc<144>();
-    bwd_run<kDs, kSpec>(c, plan, a);
+    bwd_run<kDs, kSpec, kTrace>(c, plan, a);
   } else if (rd) {
     // with EXB and DS fused on one warpgroup the register file has room for
     // the whole dQ row in RD (200 + 176 + 8 x 64 per thread-warp class)
     if (TWFA_BWD_RD_FULL && plan.sm_warp[0] == plan.sm_warp[1]) {
       setmaxnreg_inc<176>();
-      bwd_run<kReduceFull, kSpec>(c, plan, a);
+      bwd_run<kReduceFull, kSpec, kTrace>(c, plan, a);
     } else {
       setmaxnreg_dec<128>();
-      bwd_run<kReduce, kSpec>(c, plan, a);
+      bwd_run<kReduce, kSpec, kTrace>(c, plan, a);
     }
   } else {
     setmaxnreg_dec<64>();
     if (TWFA_BWD_SOLO) {
-      if (elect_one()) bwd_run<kLightSolo, false>(c, plan, a);
+      if (elect_one()) bwd_run<kLightSolo, false, kTrace>(c, plan, a);
       __syncwarp();
     } else {
-      bwd_run<kLight, kSpec>(c, plan, a);
+      bwd_run<kLight, kSpec, kTrace>(c, plan, a);
     }
   }
   if (c.lane == 0) bulk_wait_all();
@@ -1046,14 +1046,23 @@ cudaError_t fa_bwd_launch(const TwfaDevicePlan& plan, const FaBwdArgs& args, con
   } else {
     const size_t smem = fa_bwd_smem_bytes(plan);
     const bool spec = TWFA_BWD_FIXED && bwd_fixed_program(plan);
-    const void* kern = spec ? reinterpret_cast<const void*>(&fa_bwd_kernel<true>)
-                            : reinterpret_cast<const void*>(&fa_bwd_kernel<false>);
+    // traced launches run the instantiation with the issue-trace code; the
+    // others have it compiled out (+3 %, C3 shape)
+    const bool tr = args.trace != nullptr;
+    const void* kern = spec ? (tr ? reinterpret_cast<const void*>(&fa_bwd_kernel<true, true>)
+                                  : reinterpret_cast<const void*>(&fa_bwd_kernel<true, false>))
+                            : (tr ? reinterpret_cast<const void*>(&fa_bwd_kernel<false, true>)
+                                  : reinterpret_cast<const void*>(&fa_bwd_kernel<false, false>));
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    if (spec)
-      fa_bwd_kernel<true><<<grid, TWFA_MAX_WARPS * 32, smem, stream>>>(plan, args);
+    if (spec && tr)
+      fa_bwd_kernel<true, true><<<grid, TWFA_MAX_WARPS * 32, smem, stream>>>(plan, args);
+    else if (spec)
+      fa_bwd_kernel<true, false><<<grid, TWFA_MAX_WARPS * 32, smem, stream>>>(plan, args);
+    else if (tr)
+      fa_bwd_kernel<false, true><<<grid, TWFA_MAX_WARPS * 32, smem, stream>>>(plan, args);
     else
-      fa_bwd_kernel<false><<<grid, TWFA_MAX_WARPS * 32, smem, stream>>>(plan, args);
+      fa_bwd_kernel<false, false><<<grid, TWFA_MAX_WARPS * 32, smem, stream>>>(plan, args);
     e = cudaGetLastError();
   }
   if (e != cudaSuccess) return e;
