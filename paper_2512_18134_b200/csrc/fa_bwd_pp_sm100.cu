@@ -328,7 +328,7 @@ __device__ __forceinline__ void kv_epilogue_pp(const PpCtx& c, const FaBwdArgs& 
 #endif
 enum PpRole { kPpLight = 0, kPpReduce = 1, kPpExbDs = 2 };
 
-template <int kRole, int kKind = -1>
+template <int kRole, int kKind = -1, bool kTrace = true>
 __device__ __forceinline__ void pp_exec(const TwfaPlanOp op, const int r, const PpCtx& c, const PpItem& t,
                                         PpState& st, const TwfaDevicePlan& plan, const FaBwdArgs& a) {
   PpBarriers& bar = g_pb;
@@ -339,7 +339,7 @@ __device__ __forceinline__ void pp_exec(const TwfaPlanOp op, const int r, const 
       const int target = min(t.N - 1, r - static_cast<int>(op.stage) + (is_q ? plan.k_prefetch : plan.v_prefetch));
       const int before = is_q ? st.q_next : st.o_next;
       pp_top_up(c, a, t, st, plan, is_q, target);
-      if (a.trace != nullptr)
+      if (kTrace && a.trace != nullptr)
         for (int lit = before; lit < (is_q ? st.q_next : st.o_next); ++lit) {
           uint32_t* e = pp_trace(a, c, st, op.node, lit, r, t);
           if (e) e[4] = e[5] = e[3];
@@ -356,7 +356,7 @@ __device__ __forceinline__ void pp_exec(const TwfaPlanOp op, const int r, const 
     __device__ ~TraceDone() {
       if (e) e[5] = static_cast<uint32_t>(clock64());
     }
-  } trace_done_{a.trace != nullptr ? pp_trace(a, c, st, op.node, it, r, t) : nullptr};
+  } trace_done_{kTrace && a.trace != nullptr ? pp_trace(a, c, st, op.node, it, r, t) : nullptr};
   st.rec = trace_done_.e;
   if (kind == TWFA_OP_EXB || kind == TWFA_OP_DS) {
     if constexpr (kRole == kPpExbDs)
@@ -390,7 +390,7 @@ __device__ __forceinline__ void pp_exec(const TwfaPlanOp op, const int r, const 
       st.o_seen = g + 1;
     }
     tc_fence_after();
-    pp_ready(st);
+    if (kTrace) pp_ready(st);
     const uint32_t ad = sd_lo(is_s ? c.k : c.v, 16), bd = sd_lo(is_s ? qk : ok, 16);
     const uint32_t d_t = is_s ? col_s(k) : col_p(k);
     if (elect_one()) {
@@ -418,7 +418,7 @@ __device__ __forceinline__ void pp_exec(const TwfaPlanOp op, const int r, const 
       mbar_wait_all(dv ? &bar.p_full[k] : &bar.ds_full[k], g & 1, tile_full, tile_ph);
     seen = g + 1;
     tc_fence_after();
-    pp_ready(st);
+    if (kTrace) pp_ready(st);
     // B = dO_k / Q_k as [K = query][N = d], MN-major (the two 64-dim halves kHalf apart)
     const uint32_t bd = sd_lo(dv ? ok : qk, kHalf);
     const uint32_t a_t = dv ? col_s(k) : col_p(k), d_t = dv ? kColDV : kColDK;
@@ -434,7 +434,7 @@ __device__ __forceinline__ void pp_exec(const TwfaPlanOp op, const int r, const 
   } else if (kind == TWFA_OP_DQ) {
     mbar_wait(&bar.ds_full[k], g & 1);
     tc_fence_after();
-    pp_ready(st);
+    if (kTrace) pp_ready(st);
     // A = K^T as [M = d][K = key] (MN-major: the two 64-dim halves kHalf
     // apart), B = dS^T_k as [K = key][N = query] (MN-major, one 64-query atom)
     const uint32_t ad = sd_lo(c.k, kHalf), bd = sd_lo(c.ds + k * kDsBytes, kHalf);
@@ -449,7 +449,7 @@ __device__ __forceinline__ void pp_exec(const TwfaPlanOp op, const int r, const 
   }
 }
 
-template <int kRole, bool kSpec>
+template <int kRole, bool kSpec, bool kTrace>
 __device__ __forceinline__ void pp_run(const PpCtx& c, const TwfaDevicePlan& plan, const FaBwdArgs& a, int rd_k) {
   PpBarriers& bar = g_pb;
   const int plen = plan.prog_len[c.warp];
@@ -499,24 +499,24 @@ __device__ __forceinline__ void pp_run(const PpCtx& c, const TwfaDevicePlan& pla
       // the committed TMA / MMA program, each op compiled for its kind
       // (TWFA_BWD_FIXED, as in fa_bwd_sm100.cu)
       for (int rr = -1; rr < trips; ++rr) {
-        pp_exec<kRole, TWFA_OP_ST>(fx[0], rr, c, t, st, plan, a);
-        pp_exec<kRole, TWFA_OP_LDQ>(fx[1], rr, c, t, st, plan, a);
-        pp_exec<kRole, TWFA_OP_ST>(fx[2], rr, c, t, st, plan, a);
-        pp_exec<kRole, TWFA_OP_DP>(fx[3], rr, c, t, st, plan, a);
-        pp_exec<kRole, TWFA_OP_LDO>(fx[4], rr, c, t, st, plan, a);
-        pp_exec<kRole, TWFA_OP_DP>(fx[5], rr, c, t, st, plan, a);
-        pp_exec<kRole, TWFA_OP_DV>(fx[6], rr, c, t, st, plan, a);
-        pp_exec<kRole, TWFA_OP_DQ>(fx[7], rr, c, t, st, plan, a);
-        pp_exec<kRole, TWFA_OP_DV>(fx[8], rr, c, t, st, plan, a);
-        pp_exec<kRole, TWFA_OP_DQ>(fx[9], rr, c, t, st, plan, a);
-        pp_exec<kRole, TWFA_OP_DK>(fx[10], rr, c, t, st, plan, a);
-        pp_exec<kRole, TWFA_OP_DK>(fx[11], rr, c, t, st, plan, a);
+        pp_exec<kRole, TWFA_OP_ST, kTrace>(fx[0], rr, c, t, st, plan, a);
+        pp_exec<kRole, TWFA_OP_LDQ, kTrace>(fx[1], rr, c, t, st, plan, a);
+        pp_exec<kRole, TWFA_OP_ST, kTrace>(fx[2], rr, c, t, st, plan, a);
+        pp_exec<kRole, TWFA_OP_DP, kTrace>(fx[3], rr, c, t, st, plan, a);
+        pp_exec<kRole, TWFA_OP_LDO, kTrace>(fx[4], rr, c, t, st, plan, a);
+        pp_exec<kRole, TWFA_OP_DP, kTrace>(fx[5], rr, c, t, st, plan, a);
+        pp_exec<kRole, TWFA_OP_DV, kTrace>(fx[6], rr, c, t, st, plan, a);
+        pp_exec<kRole, TWFA_OP_DQ, kTrace>(fx[7], rr, c, t, st, plan, a);
+        pp_exec<kRole, TWFA_OP_DV, kTrace>(fx[8], rr, c, t, st, plan, a);
+        pp_exec<kRole, TWFA_OP_DQ, kTrace>(fx[9], rr, c, t, st, plan, a);
+        pp_exec<kRole, TWFA_OP_DK, kTrace>(fx[10], rr, c, t, st, plan, a);
+        pp_exec<kRole, TWFA_OP_DK, kTrace>(fx[11], rr, c, t, st, plan, a);
       }
     } else if (kSpec && kRole == kPpLight && is_mma) {
       __trap();  // the host launches the specialized kernel only for the fixed program
     } else
     for (int rr = -1; rr < trips; ++rr)
-      for (int j = 0; j < plen; ++j) pp_exec<kRole>(plan.ops[plan.prog[c.warp][j]], rr, c, t, st, plan, a);
+      for (int j = 0; j < plen; ++j) pp_exec<kRole, -1, kTrace>(plan.ops[plan.prog[c.warp][j]], rr, c, t, st, plan, a);
     if constexpr (kRole == kPpLight) {
       if (is_mma) {  // every MMA of the item issued: dK, dV final; K, V free
         if (elect_one()) {
@@ -532,7 +532,7 @@ __device__ __forceinline__ void pp_run(const PpCtx& c, const TwfaDevicePlan& pla
   }
 }
 
-template <bool kSpec>  // the committed 12-op TMA / MMA program in its own instantiation
+template <bool kSpec, bool kTrace>  // the committed 12-op TMA / MMA program in its own instantiation; kTrace: issue trace compiled in
 __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
     fa_bwd_pp_kernel(const __grid_constant__ TwfaDevicePlan plan, const __grid_constant__ FaBwdArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -591,13 +591,13 @@ __global__ void __launch_bounds__(TWFA_MAX_WARPS * 32, 1)
   // and the packed dS; RD a 64-float dQ^T row; the TMA / MMA warps few
   if (wg == plan.sm_warp[0] || wg == plan.sm_warp[1]) {
     setmaxnreg_inc<184>();
-    pp_run<kPpExbDs, kSpec>(c, plan, a, -1);
+    pp_run<kPpExbDs, kSpec, kTrace>(c, plan, a, -1);
   } else if (wg == plan.cr_warp[0] || wg == plan.cr_warp[1]) {
     setmaxnreg_dec<96>();
-    pp_run<kPpReduce, kSpec>(c, plan, a, wg == plan.cr_warp[0] ? 0 : 1);
+    pp_run<kPpReduce, kSpec, kTrace>(c, plan, a, wg == plan.cr_warp[0] ? 0 : 1);
   } else {
     setmaxnreg_dec<48>();
-    pp_run<kPpLight, kSpec>(c, plan, a, -1);
+    pp_run<kPpLight, kSpec, kTrace>(c, plan, a, -1);
   }
   if (c.lane == 0) bulk_wait_all();
   tc_fence_before();
@@ -628,14 +628,21 @@ static bool pp_fixed_program(const TwfaDevicePlan& plan) {
 cudaError_t fa_bwd_pp_main_launch(const TwfaDevicePlan& plan, const FaBwdArgs& args, int grid, cudaStream_t stream) {
   const size_t smem = fa_bwd_pp_smem_bytes(plan);
   const bool spec = TWFA_BWD_FIXED && pp_fixed_program(plan);
-  const void* kern = spec ? reinterpret_cast<const void*>(&fa_bwd_pp_kernel<true>)
-                          : reinterpret_cast<const void*>(&fa_bwd_pp_kernel<false>);
+  const bool tr = args.trace != nullptr;
+  const void* kern = spec ? (tr ? reinterpret_cast<const void*>(&fa_bwd_pp_kernel<true, true>)
+                                : reinterpret_cast<const void*>(&fa_bwd_pp_kernel<true, false>))
+                          : (tr ? reinterpret_cast<const void*>(&fa_bwd_pp_kernel<false, true>)
+                                : reinterpret_cast<const void*>(&fa_bwd_pp_kernel<false, false>));
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  if (spec)
-    fa_bwd_pp_kernel<true><<<grid, TWFA_MAX_WARPS * 32, smem, stream>>>(plan, args);
+  if (spec && tr)
+    fa_bwd_pp_kernel<true, true><<<grid, TWFA_MAX_WARPS * 32, smem, stream>>>(plan, args);
+  else if (spec)
+    fa_bwd_pp_kernel<true, false><<<grid, TWFA_MAX_WARPS * 32, smem, stream>>>(plan, args);
+  else if (tr)
+    fa_bwd_pp_kernel<false, true><<<grid, TWFA_MAX_WARPS * 32, smem, stream>>>(plan, args);
   else
-    fa_bwd_pp_kernel<false><<<grid, TWFA_MAX_WARPS * 32, smem, stream>>>(plan, args);
+    fa_bwd_pp_kernel<false, false><<<grid, TWFA_MAX_WARPS * 32, smem, stream>>>(plan, args);
   return cudaGetLastError();
 }
 
