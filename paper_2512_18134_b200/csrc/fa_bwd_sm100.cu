@@ -84,6 +84,9 @@ constexpr uint32_t kSdHi = sdesc_hi(1024);
 #ifndef TWFA_BWD_HEAVY_SPEC
 #define TWFA_BWD_HEAVY_SPEC 1
 #endif
+#ifndef TWFA_BWD_CFLAGS
+#define TWFA_BWD_CFLAGS 1
+#endif
 #ifndef TWFA_BWD_FIXED
 #define TWFA_BWD_FIXED 1
 #endif
@@ -646,12 +649,15 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
   const uint32_t kd = kKind >= 0 && TWFA_BWD_CDEPTH ? 2u : static_cast<uint32_t>(plan.k_depth);
   const uint32_t vd = kKind >= 0 && TWFA_BWD_CDEPTH ? 2u : static_cast<uint32_t>(plan.v_depth);
   const uint32_t qs = g % kd, os = g % vd;
-  const bool release = op.flags & TWFA_OPF_RELEASE;
+  // the fixed production program's flags are host-checked (bwd_fixed_program):
+  // DK releases Q_i, DV releases dO_i, nothing else releases or waits on p_read
+  const bool release = (kKind >= 0 && TWFA_BWD_CFLAGS) ? (kind == TWFA_OP_DK || kind == TWFA_OP_DV)
+                                                      : static_cast<bool>(op.flags & TWFA_OPF_RELEASE);
   if (kind == TWFA_OP_ST) {
     if (it == 0) mbar_wait(&bar.kv_full, t.icount & 1);
     // P^T(g-1) was read by DV(g-1) (in order) and, with DS on its own
     // warpgroup, by DS(g-1) (p_read)
-    if (g > 0 && (op.flags & TWFA_OPF_WAIT_PREAD))
+    if (g > 0 && !(kKind >= 0 && TWFA_BWD_CFLAGS) && (op.flags & TWFA_OPF_WAIT_PREAD))
       mbar_wait_all(&bar.q_full[qs], (g / kd) & 1, &bar.p_read, (g - 1) & 1);
     else if (!(TWFA_BWD_MEMO && st.q_seen == g + 1))
       mbar_wait(&bar.q_full[qs], (g / kd) & 1);
@@ -748,7 +754,8 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
         mma_ss(kColP, sdesc_join(ad + kk * 2048 / 16, kSdHi), sdesc_join(bd + kk * 2048 / 16, kSdHi), kIdescMM,
                kk > 0);
       mma_commit(&bar.dq_full);
-      if (op.flags & TWFA_OPF_RELEASE) mma_commit(&bar.ds_free);  // dQ staged in the Q slot: dS is free
+      if (!(kKind >= 0 && TWFA_BWD_CFLAGS) && (op.flags & TWFA_OPF_RELEASE))
+        mma_commit(&bar.ds_free);  // dQ staged in the Q slot: dS is free
     }
     wsync<kSolo>();
   }
@@ -1030,8 +1037,14 @@ bool bwd_fixed_program(const TwfaDevicePlan& plan) {
   const int w = plan.mma_warp;
   static const int kinds[7] = {TWFA_OP_ST, TWFA_OP_LDQ, TWFA_OP_LDO, TWFA_OP_DP, TWFA_OP_DK, TWFA_OP_DQ, TWFA_OP_DV};
   if (w < 0 || w >= TWFA_MAX_WARPS || plan.prog_len[w] != 7) return false;
-  for (int j = 0; j < 7; ++j)
-    if (plan.ops[plan.prog[w][j]].kind != kinds[j]) return false;
+  for (int j = 0; j < 7; ++j) {
+    const TwfaPlanOp& op = plan.ops[plan.prog[w][j]];
+    if (op.kind != kinds[j]) return false;
+    if (TWFA_BWD_CFLAGS) {  // the flags the specialized kernel assumes
+      const bool rel = op.kind == TWFA_OP_DK || op.kind == TWFA_OP_DV;
+      if (((op.flags & TWFA_OPF_RELEASE) != 0) != rel || (op.flags & TWFA_OPF_WAIT_PREAD)) return false;
+    }
+  }
   return true;
 }
 
