@@ -373,13 +373,14 @@ __device__ __forceinline__ void ds_part(const BwdCtx& c, const FaBwdArgs& a, con
 // RD: dQ_i from TMEM (row = query) -> smem staging (fp32, SW128 boxes of
 // 128 rows x 32 columns) -> cp.reduce.async.bulk add into the fp32 dQ
 // accumulator (the atomic reduction of the paper's backward loop).
-template <bool kFull>
+template <bool kFull, bool kKnown = false>
 __device__ __forceinline__ void rd_op(const BwdCtx& c, const FaBwdArgs& a, const BwdItem& t, int it, uint32_t g,
                                       const TwfaDevicePlan& plan, BwdState& st) {
   // staging buffer: Q_i's ring slot when the schedule says so (plan.s_split
-  // for the backward family; DK_i is complete once DQ_i is), else dS's
-  const bool q_stage = plan.s_split != 0;
-  const uint32_t qs = g % plan.k_depth;
+  // for the backward family; DK_i is complete once DQ_i is), else dS's.
+  // kKnown: the specialized kernel's host-checked plan (dS staging, depth 2)
+  const bool q_stage = kKnown ? false : plan.s_split != 0;
+  const uint32_t qs = g % (kKnown ? 2u : static_cast<uint32_t>(plan.k_depth));
   uint8_t* const stage_buf = q_stage ? c.q + qs * kTile : c.ds;
   BwdBarriers& bar = g_bb;
   const int q0 = (t.q_first + it) * kT;
@@ -574,7 +575,9 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
   if (kind == TWFA_OP_LDQ || kind == TWFA_OP_LDO) {
     if constexpr (is_light(kRole)) {
       const bool is_q = kind == TWFA_OP_LDQ;
-      const int target = min(t.N - 1, r - static_cast<int>(op.stage) + (is_q ? plan.k_prefetch : plan.v_prefetch));
+      const int target = (kKind >= 0 && TWFA_BWD_CFLAGS)
+                             ? min(t.N - 1, r + 1)  // stage 0, prefetch 1: host-checked
+                             : min(t.N - 1, r - static_cast<int>(op.stage) + (is_q ? plan.k_prefetch : plan.v_prefetch));
       (is_q ? st.q_target : st.o_target) = target;
       const int before = is_q ? st.q_next : st.o_next;
       if constexpr (kKind >= 0 && TWFA_BWD_CDEPTH) bwd_top_up<kRole == kLightSolo, 2>(c, a, t, st, plan, is_q, target, !TWFA_BWD_LAZY_LOADS);
@@ -593,7 +596,7 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
       bwd_top_up<kRole == kLightSolo>(c, a, t, st, plan, false, st.o_target, false);
     }
   }
-  const int it = r - static_cast<int>(op.stage);
+  const int it = r - ((kKind >= 0 && TWFA_BWD_CFLAGS) ? 0 : static_cast<int>(op.stage));  // stage 0: host-checked
   if (it < 0 || it >= t.N) return;
   const uint32_t g = t.gbase + static_cast<uint32_t>(it);
   // one record per op instance; t_done stamped when the op body returns
@@ -634,7 +637,8 @@ __device__ __forceinline__ void bwd_exec(const TwfaPlanOp op, const int r, const
     return;
   }
   if (kind == TWFA_OP_RD) {
-    if constexpr (kRole == kReduce || kRole == kReduceFull) rd_op<kRole == kReduceFull>(c, a, t, it, g, plan, st);
+    if constexpr (kRole == kReduce || kRole == kReduceFull)
+      rd_op<kRole == kReduceFull, kKind >= 0 && TWFA_BWD_CFLAGS>(c, a, t, it, g, plan, st);
     return;
   }
   if constexpr (!is_light(kRole)) return;
@@ -819,7 +823,7 @@ __device__ __forceinline__ void bwd_run(const BwdCtx& c, const TwfaDevicePlan& p
     }
     st.q_next = st.o_next = 0;
     st.q_target = st.o_target = -1;
-    const int trips = t.N + plan.max_stage;
+    const int trips = t.N + ((kSpec && TWFA_BWD_CFLAGS) ? 0 : plan.max_stage);
     if (kSpec && TWFA_BWD_HEAVY_SPEC && kRole == kExbDs) {
       for (int rr = -1; rr < trips; ++rr) {
         bwd_exec<kRole, TWFA_OP_EXB, kTrace>(fx[0], rr, c, t, st, plan, a);
@@ -1027,6 +1031,11 @@ bool bwd_fixed_program(const TwfaDevicePlan& plan) {
   if (plan.num_tiles != 1 || plan.k_depth != 2 || plan.v_depth != 2 || plan.mma_warp != plan.load_warp ||
       TWFA_BWD_SOLO || TWFA_BWD_LOAD_WARP >= 0)
     return false;
+  if (TWFA_BWD_CFLAGS && (plan.max_stage != 0 || plan.k_prefetch != 1 || plan.v_prefetch != 1 || plan.s_split != 0))
+    return false;
+  if (TWFA_BWD_CFLAGS)
+    for (int v = 0; v < plan.num_nodes; ++v)
+      if (plan.ops[v].stage != 0) return false;
   if (TWFA_BWD_HEAVY_SPEC) {  // the fused [EXB DS] warpgroup and the [RD] warpgroup
     const int e = plan.sm_warp[0], r = plan.cr_warp[0];
     if (e != plan.sm_warp[1] || e < 0 || r < 0 || plan.prog_len[e] != 2 || plan.prog_len[r] != 1 ||
