@@ -114,14 +114,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     const uint64_t pol_a = (pm == 1 || pm == 2 || pm == 4) ? policy_evict_last() : policy_evict_normal();
     const uint64_t pol_b = pm == 2 ? policy_evict_last() : (pm == 1 || pm == 3) ? policy_evict_first()
                                                                                  : policy_evict_normal();
-    uint32_t g = 0;
+    // ring slot and phase advanced incrementally (no division per k-block)
+    uint32_t s = 0, ph = 0;
     for (int t = pair; t < num_tiles; t += num_pairs) {
       int tm, tn;
       tile_coords(t, tiles_m, tiles_n, group_m, tm, tn);
       const int row_a = tm * kPairM + static_cast<int>(rank) * kBM;
       const int row_b = tn * kPairN + static_cast<int>(rank) * kBN;
-      for (int kb = 0; kb < kblocks; ++kb, ++g) {
-        const uint32_t s = g % stages, ph = (g / stages) & 1;
+      for (int kb = 0; kb < kblocks; ++kb, s = s + 1 == static_cast<uint32_t>(stages) ? (ph ^= 1u, 0u) : s + 1) {
         mbar_wait_cluster(&bar->empty[s], ph ^ 1);
         uint8_t* sa = smem + s * kStageBytes;
         if (elect_one()) {
@@ -137,13 +137,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       // MMA: D += A B^T, one 256x256x16 pair instruction per 16-wide k slice.
       // Every lane waits and computes the (uniform) descriptors; one elected
       // lane issues, so the operands stay in uniform registers.
-      uint32_t g = 0, lt = 0;
+      uint32_t s = 0, ph = 0, lt = 0;
       for (int t = pair; t < num_tiles; t += num_pairs, ++lt) {
         const uint32_t acc = lt & 1, acc_ph = (lt >> 1) & 1;
         mbar_wait_cluster(&bar->acc_empty[acc], acc_ph ^ 1);
         tc_fence_after();
-        for (int kb = 0; kb < kblocks; ++kb, ++g) {
-          const uint32_t s = g % stages, ph = (g / stages) & 1;
+        for (int kb = 0; kb < kblocks; ++kb, s = s + 1 == static_cast<uint32_t>(stages) ? (ph ^= 1u, 0u) : s + 1) {
           mbar_wait_cluster(&bar->full[s], ph);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + s * kStageBytes);
